@@ -1,0 +1,170 @@
+/*
+ * sgap.h -- C ABI of the B200 (sm_100a) CSR SpMM engine for the Sgap
+ * (arXiv 2209.02882) schedule space.  Drop-in for the executor of the
+ * reference package `spmmlab` (paths relative to /root/reference/pkg/src/spmmlab).
+ *
+ * The reference boundary is the Python function
+ *     sim.run(kernel: LoweredKernel, a: CsrMatrix, b: DenseMatrix,
+ *             c0: DenseMatrix | None = None, *, precision="double")
+ *         -> (DenseMatrix, SimMetrics)                       (sim.py:431-487)
+ * whose LoweredKernel comes from runner.build_kernel (runner.py:141-156) =
+ * templates.algorithm_template (templates.py:220-235) + lowering.lower
+ * (lowering.py:649-696).  The entry points below replace:
+ *
+ *   sgap_legality_rule    space.legality_rule            space.py:177-204
+ *   sgap_build_kernel     runner.build_kernel            runner.py:141-156
+ *                         (family + divisibility gates   templates.py:82-202,
+ *                          + grid/block geometry)         lowering.py:218-243,649-696)
+ *   sgap_block_starts     lowering.compute_block_starts  lowering.py:119-128
+ *   sgap_run              sim.run                        sim.py:431-487
+ *   sgap_seg_reduce_group sim.exec_seg_reduce_group      sim.py:139-165
+ *   sgap_atomic_add_group sim.exec_atomic_add_group      sim.py:112-136
+ *
+ * Conventions: plain pointers and sizes; every pointer named d_* is device
+ * memory, the caller owns all buffers, the library allocates nothing and
+ * keeps no mutable global state (reentrant, one call per stream).  All work is
+ * stream-ordered on the `stream` argument (a cudaStream_t passed as void*; NULL
+ * is the legacy default stream).  Status codes mirror the reference's Python
+ * exceptions (see sgap_status_t).
+ */
+#ifndef SGAP_H_
+#define SGAP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SGAP_ABI_VERSION 1
+
+typedef enum {
+    SGAP_OK = 0,
+    SGAP_ERR_ILLEGAL_POINT = 1,   /* templates.IllegalPointError(rule)      */
+    SGAP_ERR_NO_TEMPLATE = 2,     /* build_kernel -> None ("no_template")   */
+    SGAP_ERR_SHAPE = 3,           /* sim.run ValueError: shape mismatch     */
+    SGAP_ERR_PRECISION = 4,       /* sim.run ValueError: unknown precision  */
+    SGAP_ERR_CUDA = 5,            /* CUDA runtime / launch failure          */
+    SGAP_ERR_ARG = 6,             /* bad argument (null, misaligned, range) */
+    SGAP_ERR_FAULT = 7,           /* sim.SimulationFault: group invariant   */
+    SGAP_ERR_CONFIG = 8           /* lowering.LoweringError: KernelConfig   */
+} sgap_status_t;
+
+/* Template families (templates.py:46-58). */
+typedef enum {
+    SGAP_NNZ_MULTIPLE = 0,   /* nnz:g,col:c,r:1    EB + serial (TACO)        */
+    SGAP_ROW_MULTIPLE = 1,   /* row:g,col:c,r:1    RB + serial               */
+    SGAP_ROW_RECIPROCAL = 2, /* row:1/g,col:c,r:g  RB + parallel group       */
+    SGAP_NNZ_ONE = 3         /* nnz:1,col:c,r      EB + segment (r>1) / atomic (r=1) */
+} sgap_family_t;
+
+typedef enum { SGAP_F32 = 0, SGAP_F64 = 1 } sgap_dtype_t;
+
+/* A schedule point {<data, col>, r} (space.py:55-122). */
+typedef enum { SGAP_KIND_NNZ = 0, SGAP_KIND_ROW = 1 } sgap_data_kind_t;
+typedef enum { SGAP_AMT_RECIPROCAL = 0, SGAP_AMT_ONE = 1, SGAP_AMT_MULTIPLE = 2 } sgap_amount_kind_t;
+
+typedef struct {
+    int32_t data_kind;     /* sgap_data_kind_t                              */
+    int32_t data_amount;   /* sgap_amount_kind_t                            */
+    int32_t data_param;    /* g (>= 2) for 1/g or g; ignored for ONE         */
+    int32_t col_amount;    /* sgap_amount_kind_t                            */
+    int32_t col_param;     /* c (>= 2) for 1/c or c; ignored for ONE         */
+    int32_t r;             /* group width r >= 1                             */
+} sgap_point_t;
+
+/* The lowered kernel: the reference's LoweredKernel integers (grid_size,
+ * block_size, family, whether block_starts exist) plus the split factors the
+ * device kernels need.  Filled by sgap_build_kernel; a caller that already
+ * holds a reference LoweredKernel may fill it directly from its fields. */
+typedef struct {
+    int32_t family;         /* sgap_family_t                                 */
+    int32_t n;              /* KernelConfig.n: dense width N                 */
+    int32_t p;              /* KernelConfig.p: parallelism budget            */
+    int32_t g;              /* data split factor (1 for ONE)                 */
+    int32_t c;              /* column coarsening (1 for ONE)                 */
+    int32_t r;              /* group width                                   */
+    int64_t chunk;          /* units per logical block: nnz positions
+                               (nnz-*), rows (row-multiple), fused (i,k)
+                               cells (row-reciprocal)                        */
+    int64_t grid_size;      /* == LoweredKernel.grid_size                    */
+    int64_t block_size;     /* == LoweredKernel.block_size                   */
+    int32_t has_block_starts; /* == (LoweredKernel.block_starts is not None) */
+    int32_t hw_block;       /* hardware CTA size chosen for sm_100a (0=auto) */
+} sgap_kernel_t;
+
+/* CSR operand on the device (matrices.py:38-86 with int32 indices). */
+typedef struct {
+    int64_t num_rows;
+    int64_t num_cols;
+    int64_t nnz;
+    const int32_t *d_row_ptr;  /* [num_rows + 1] */
+    const int32_t *d_col_idx;  /* [nnz]          */
+    const void *d_vals;        /* [nnz] float or double (sgap_dtype_t)      */
+} sgap_csr_t;
+
+int sgap_abi_version(void);
+const char *sgap_status_string(int status);
+
+/* space.legality_rule: 0 when legal, else the first rule (1..3) that fires. */
+int sgap_legality_rule(const sgap_point_t *point);
+
+/* runner.build_kernel without the LLIR: family selection, divisibility
+ * gates, launch geometry.  Returns SGAP_OK, SGAP_ERR_ILLEGAL_POINT (rule in
+ * *rule_out), SGAP_ERR_NO_TEMPLATE or SGAP_ERR_CONFIG (n < 1, p not a positive
+ * warp multiple). */
+int sgap_build_kernel(const sgap_point_t *point, int32_t n, int32_t p,
+                      int64_t num_rows, int64_t nnz, sgap_kernel_t *out,
+                      int32_t *rule_out);
+
+/* lowering.compute_block_starts on the device: d_starts[b] (b = 0..num_blocks)
+ * = last r in [0, num_rows] with row_ptr[r] <= b*chunk.  int32 output. */
+int sgap_block_starts(const int32_t *d_row_ptr, int64_t num_rows, int64_t chunk,
+                      int64_t num_blocks, int32_t *d_starts, void *stream);
+
+/* sim.run: C (+)= A @ B on the device.
+ *   d_b: [a->num_cols x kernel->n] row-major, d_c: [a->num_rows x n] row-major.
+ *   accumulate = 1: C += A@B (c0 already in d_c, sim.py:439-441);
+ *   accumulate = 0: C = A@B (d_c is overwritten; zero-fill included).
+ *   d_block_starts: [grid_size + 1] from sgap_block_starts; required when
+ *   kernel->has_block_starts.
+ *   d_writebacks: optional (NULL = off) device counter, incremented by the
+ *   number of output writebacks (== SimMetrics.atomic_ops of the reference
+ *   simulator for the same kernel; 0 for row-multiple).                      */
+int sgap_run(const sgap_kernel_t *kernel, const sgap_csr_t *a, const void *d_b,
+             void *d_c, int32_t dtype, int32_t accumulate,
+             const int32_t *d_block_starts, unsigned long long *d_writebacks,
+             void *stream);
+
+/* The dense reference product that runner.verify_point checks against
+ * (runner.py:193-194 -> matrices.dense_spmm_oracle, matrices.py:241-254),
+ * evaluated on the device: C[i,k] in float64, ascending-p accumulation with
+ * separately rounded multiply and add, i.e. bit-identical to the reference
+ * oracle on the same (widened) inputs.  d_c: [num_rows x n] float64.        */
+int sgap_reference_spmm_f64(const sgap_csr_t *a, const void *d_b, int32_t n,
+                            int32_t dtype, double *d_c, void *stream);
+
+/* Device restatements of the simulator's group macros over lane vectors
+ * (lanes = multiple of group_size, group_size in {1,2,4,8,16,32}).  They run
+ * the same warp-shuffle code as the SpMM kernels.
+ *   d_idx [lanes] int64, d_val [lanes] (dtype), d_active [lanes] uint8 (NULL =
+ *   all active), d_out [out_len] (dtype, accumulated into),
+ *   d_writebacks: counter (required), d_fault: int64 initialised by the caller
+ *   to INT64_MAX; receives the smallest lane that violates the group invariant
+ *   (diverging index / decreasing index), if any.                            */
+int sgap_seg_reduce_group(const int64_t *d_idx, const void *d_val,
+                          const uint8_t *d_active, int64_t lanes,
+                          int32_t group_size, void *d_out, int64_t out_len,
+                          int32_t dtype, unsigned long long *d_writebacks,
+                          long long *d_fault, void *stream);
+int sgap_atomic_add_group(const int64_t *d_idx, const void *d_val,
+                          const uint8_t *d_active, int64_t lanes,
+                          int32_t group_size, void *d_out, int64_t out_len,
+                          int32_t dtype, unsigned long long *d_writebacks,
+                          long long *d_fault, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SGAP_H_ */

@@ -1,0 +1,388 @@
+// sgap_api.cu -- the C ABI (include/sgap.h): host-side planning that mirrors
+// the reference's template gates and launch geometry, and stream-ordered
+// dispatch of the sm_100a kernels.  No allocation, no global mutable state.
+#include <climits>
+#include <cstdint>
+#include <cstring>
+
+#include <cuda_runtime.h>
+
+#include "../../include/sgap.h"
+#include "sgap_kernels.cuh"
+
+using namespace sgap;
+
+namespace {
+
+constexpr int kHwBlock = 256;
+
+inline long long ceil_div(long long a, long long b) { return (a + b - 1) / b; }
+
+inline int pow2_floor(long long x) {
+    int p = 1;
+    while ((long long)p * 2 <= x && p < 32) p *= 2;
+    return p;
+}
+
+inline int amount_units(int kind, int param) { return kind == SGAP_AMT_ONE ? 1 : param; }
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int launch_status() {
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SGAP_OK : SGAP_ERR_CUDA;
+}
+
+inline unsigned grid_for(long long items_per_warp_units, int block) {
+    // warps needed, then CTAs; kernels grid-stride past this cap
+    long long warps = items_per_warp_units;
+    long long ctas = ceil_div(warps, block / 32);
+    if (ctas < 1) ctas = 1;
+    if (ctas > (1LL << 30)) ctas = 1LL << 30;
+    return (unsigned)ctas;
+}
+
+bool aligned(const void *p, size_t bytes) {
+    return (reinterpret_cast<uintptr_t>(p) % bytes) == 0;
+}
+
+// ------------------------------------------------------------------ dispatch
+
+template <typename T, int V>
+int run_row_multiple(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
+                     int acc, cudaStream_t st) {
+    const int N = k.n, L = N / V;
+    int S = 0;
+    if (L <= 32 && (32 % L) == 0) S = L;
+    else if (L % 32 == 0) S = 32;
+    const long long total = ceil_div(a.num_rows, k.g) * (long long)L;
+    const int blk = k.hw_block > 0 ? k.hw_block : kHwBlock;
+    k_row_multiple<T, V><<<grid_for(ceil_div(total, 32), blk), blk, 0, st>>>(
+        a.d_row_ptr, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, (int)a.num_rows, N,
+        k.g, S, acc);
+    return launch_status();
+}
+
+template <typename T, int V, int G>
+int run_row_reciprocal_g(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
+                         int acc, unsigned long long *wb, cudaStream_t st) {
+    const long long cells = a.num_rows * (long long)k.n;
+    const long long total = ceil_div(cells, V) * G;
+    const int blk = k.hw_block > 0 ? k.hw_block : kHwBlock;
+    k_row_reciprocal<T, V, G><<<grid_for(ceil_div(total, 32), blk), blk, 0, st>>>(
+        a.d_row_ptr, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, (int)a.num_rows, k.n,
+        acc, wb);
+    return launch_status();
+}
+
+template <typename T, int V>
+int run_row_reciprocal(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C, int acc,
+                       unsigned long long *wb, cudaStream_t st) {
+    switch (k.g) {
+        case 2: return run_row_reciprocal_g<T, V, 2>(k, a, B, C, acc, wb, st);
+        case 4: return run_row_reciprocal_g<T, V, 4>(k, a, B, C, acc, wb, st);
+        case 8: return run_row_reciprocal_g<T, V, 8>(k, a, B, C, acc, wb, st);
+        case 16: return run_row_reciprocal_g<T, V, 16>(k, a, B, C, acc, wb, st);
+        case 32: return run_row_reciprocal_g<T, V, 32>(k, a, B, C, acc, wb, st);
+        default: return SGAP_ERR_NO_TEMPLATE;
+    }
+}
+
+template <typename T, int V, int R>
+int run_nnz_one_r(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
+                  const int *starts, unsigned long long *wb, cudaStream_t st) {
+    const int NT = k.n / V;
+    const int TW = pow2_floor(NT < 32 / R ? NT : 32 / R);
+    const int Q = 32 / TW;
+    const long long total_pos = k.grid_size * k.chunk;
+    const long long items = ceil_div(total_pos, Q);
+    const int blk = k.hw_block > 0 ? k.hw_block : kHwBlock;
+    k_nnz_one<T, V, R><<<grid_for(items, blk), blk, 0, st>>>(
+        a.d_row_ptr, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, starts,
+        (int)a.num_rows, k.n, a.nnz, k.chunk, k.grid_size, TW, wb);
+    return launch_status();
+}
+
+template <typename T, int V>
+int run_nnz_one(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
+                const int *starts, unsigned long long *wb, cudaStream_t st) {
+    switch (k.r) {
+        case 1: return run_nnz_one_r<T, V, 1>(k, a, B, C, starts, wb, st);
+        case 2: return run_nnz_one_r<T, V, 2>(k, a, B, C, starts, wb, st);
+        case 4: return run_nnz_one_r<T, V, 4>(k, a, B, C, starts, wb, st);
+        case 8: return run_nnz_one_r<T, V, 8>(k, a, B, C, starts, wb, st);
+        case 16: return run_nnz_one_r<T, V, 16>(k, a, B, C, starts, wb, st);
+        case 32: return run_nnz_one_r<T, V, 32>(k, a, B, C, starts, wb, st);
+        default: return SGAP_ERR_NO_TEMPLATE;
+    }
+}
+
+template <typename T, int V>
+int run_nnz_multiple(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
+                     const int *starts, unsigned long long *wb, cudaStream_t st) {
+    const int NT = k.n / V;
+    const int TW = pow2_floor(NT);
+    const int SG = 32 / TW;
+    const long long chunks = k.grid_size * (k.chunk / k.g);
+    const long long items = ceil_div(chunks, SG);
+    const int blk = k.hw_block > 0 ? k.hw_block : kHwBlock;
+    k_nnz_multiple<T, V><<<grid_for(items, blk), blk, 0, st>>>(
+        a.d_row_ptr, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, starts,
+        (int)a.num_rows, k.n, a.nnz, k.g, k.chunk, k.grid_size, TW, wb);
+    return launch_status();
+}
+
+template <typename T, int V>
+int run_family(const sgap_kernel_t &k, const sgap_csr_t &a, const void *b, void *c, int acc,
+               const int *starts, unsigned long long *wb, cudaStream_t st) {
+    const T *B = static_cast<const T *>(b);
+    T *C = static_cast<T *>(c);
+    switch (k.family) {
+        case SGAP_ROW_MULTIPLE: return run_row_multiple<T, V>(k, a, B, C, acc, st);
+        case SGAP_ROW_RECIPROCAL: return run_row_reciprocal<T, V>(k, a, B, C, acc, wb, st);
+        case SGAP_NNZ_ONE: return run_nnz_one<T, V>(k, a, B, C, starts, wb, st);
+        case SGAP_NNZ_MULTIPLE: return run_nnz_multiple<T, V>(k, a, B, C, starts, wb, st);
+        default: return SGAP_ERR_ARG;
+    }
+}
+
+template <typename T>
+int run_typed(const sgap_kernel_t &k, const sgap_csr_t &a, const void *b, void *c, int acc,
+              const int *starts, unsigned long long *wb, cudaStream_t st) {
+    switch (k.c) {
+        case 1: return run_family<T, 1>(k, a, b, c, acc, starts, wb, st);
+        case 2: return run_family<T, 2>(k, a, b, c, acc, starts, wb, st);
+        case 4: return run_family<T, 4>(k, a, b, c, acc, starts, wb, st);
+        default: return SGAP_ERR_NO_TEMPLATE;
+    }
+}
+
+template <typename T>
+int prim_dispatch(bool seg, const int64_t *idx, const void *val, const uint8_t *active,
+                  int64_t lanes, int gs, void *out, int64_t out_len,
+                  unsigned long long *wb, long long *fault, cudaStream_t st) {
+    const long long items = ceil_div(lanes, 32);
+    const unsigned grid = grid_for(items, kHwBlock);
+    auto *I = reinterpret_cast<const long long *>(idx);
+    auto *Vv = static_cast<const T *>(val);
+    auto *O = static_cast<T *>(out);
+#define SGAP_PRIM(RR)                                                                    \
+    case RR:                                                                              \
+        if (seg) k_seg_reduce_prim<T, RR><<<grid, kHwBlock, 0, st>>>(I, Vv, active, lanes, \
+                                                                      O, out_len, wb, fault); \
+        else k_atomic_add_prim<T, RR><<<grid, kHwBlock, 0, st>>>(I, Vv, active, lanes, O,   \
+                                                                  out_len, wb, fault);      \
+        break;
+    switch (gs) {
+        SGAP_PRIM(1)
+        SGAP_PRIM(2)
+        SGAP_PRIM(4)
+        SGAP_PRIM(8)
+        SGAP_PRIM(16)
+        SGAP_PRIM(32)
+        default: return SGAP_ERR_ARG;
+    }
+#undef SGAP_PRIM
+    return launch_status();
+}
+
+int prim_entry(bool seg, const int64_t *idx, const void *val, const uint8_t *active,
+               int64_t lanes, int32_t gs, void *out, int64_t out_len, int32_t dtype,
+               unsigned long long *wb, long long *fault, void *stream) {
+    if (lanes < 0 || gs < 1 || gs > 32 || (gs & (gs - 1)) || lanes % gs) return SGAP_ERR_ARG;
+    if (wb == nullptr || fault == nullptr) return SGAP_ERR_ARG;
+    if (lanes == 0) return SGAP_OK;
+    if (idx == nullptr || val == nullptr || out == nullptr) return SGAP_ERR_ARG;
+    if (dtype == SGAP_F32)
+        return prim_dispatch<float>(seg, idx, val, active, lanes, gs, out, out_len, wb, fault,
+                                    as_stream(stream));
+    if (dtype == SGAP_F64)
+        return prim_dispatch<double>(seg, idx, val, active, lanes, gs, out, out_len, wb, fault,
+                                     as_stream(stream));
+    return SGAP_ERR_PRECISION;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sgap_abi_version(void) { return SGAP_ABI_VERSION; }
+
+const char *sgap_status_string(int status) {
+    switch (status) {
+        case SGAP_OK: return "ok";
+        case SGAP_ERR_ILLEGAL_POINT: return "illegal point";
+        case SGAP_ERR_NO_TEMPLATE: return "no template covers the point";
+        case SGAP_ERR_SHAPE: return "shape mismatch";
+        case SGAP_ERR_PRECISION: return "unknown precision";
+        case SGAP_ERR_CUDA: return "CUDA error";
+        case SGAP_ERR_ARG: return "bad argument";
+        case SGAP_ERR_FAULT: return "group invariant violated";
+        case SGAP_ERR_CONFIG: return "bad kernel config";
+        default: return "unknown status";
+    }
+}
+
+// space.legality_rule (space.py:177-204).
+int sgap_legality_rule(const sgap_point_t *pt) {
+    if (pt == nullptr) return -1;
+    const bool data_recip = pt->data_amount == SGAP_AMT_RECIPROCAL;
+    const bool col_recip = pt->col_amount == SGAP_AMT_RECIPROCAL;
+    if (pt->data_kind == SGAP_KIND_NNZ) return (data_recip || col_recip) ? 1 : 0;
+    if (data_recip) {
+        if (pt->r < pt->data_param) return 2;  // r/g < 1
+        if (col_recip) return 3;
+    }
+    return 0;
+}
+
+// runner.build_kernel = templates.template_family + the per-family gates
+// (templates.py:82-202) + lowering geometry (lowering.py:218-243, 649-696).
+int sgap_build_kernel(const sgap_point_t *pt, int32_t n, int32_t p, int64_t num_rows,
+                      int64_t nnz, sgap_kernel_t *out, int32_t *rule_out) {
+    if (pt == nullptr || out == nullptr) return SGAP_ERR_ARG;
+    if (rule_out) *rule_out = 0;
+    if (n < 1 || p < 32 || p % 32 != 0) return SGAP_ERR_CONFIG;
+    const int rule = sgap_legality_rule(pt);
+    if (rule != 0) {
+        if (rule_out) *rule_out = rule;
+        return SGAP_ERR_ILLEGAL_POINT;
+    }
+    if (pt->col_amount == SGAP_AMT_RECIPROCAL) return SGAP_ERR_NO_TEMPLATE;
+    std::memset(out, 0, sizeof(*out));
+    const long long N = n, P = p;
+    const long long c = amount_units(pt->col_amount, pt->col_param);
+    const long long g = amount_units(pt->data_amount, pt->data_param);
+    const long long r = pt->r;
+    out->n = n;
+    out->p = p;
+    out->c = (int)c;
+    out->g = (int)g;
+    out->r = (int)r;
+    if (pt->data_kind == SGAP_KIND_NNZ) {
+        if (pt->data_amount == SGAP_AMT_ONE) {
+            if (N % c || (P * c) % N) return SGAP_ERR_NO_TEMPLATE;
+            const long long npb = P * c / N;
+            if (r > 1 && (32 % r || npb % r || r > npb)) return SGAP_ERR_NO_TEMPLATE;
+            out->family = SGAP_NNZ_ONE;
+            out->chunk = npb;
+            out->grid_size = nnz ? ceil_div(nnz, npb) : 0;
+            out->block_size = P;
+            out->has_block_starts = 1;
+        } else if (pt->data_amount == SGAP_AMT_MULTIPLE && r == 1) {
+            if (N % c || (P * c) % N || (P * g * c) % N) return SGAP_ERR_NO_TEMPLATE;
+            const long long chunk = P * g * c / N;
+            if (((P * c / N) * c) % 32) return SGAP_ERR_NO_TEMPLATE;
+            out->family = SGAP_NNZ_MULTIPLE;
+            out->chunk = chunk;
+            out->grid_size = nnz ? ceil_div(nnz, chunk) : 0;
+            out->block_size = (chunk / g) * c;
+            out->has_block_starts = 1;
+        } else {
+            return SGAP_ERR_NO_TEMPLATE;
+        }
+    } else {
+        if (pt->data_amount == SGAP_AMT_RECIPROCAL) {
+            if (r != g) return SGAP_ERR_NO_TEMPLATE;
+            if (N % c || (c * P) % g || P % g || 32 % g) return SGAP_ERR_NO_TEMPLATE;
+            const long long cells = c * P / g;
+            out->family = SGAP_ROW_RECIPROCAL;
+            out->chunk = cells;
+            out->grid_size = ceil_div(num_rows * N, cells);
+            out->block_size = P;
+        } else {
+            if (r != 1) return SGAP_ERR_NO_TEMPLATE;
+            if (N % c || (P * g * c) % N || (P * c) % N) return SGAP_ERR_NO_TEMPLATE;
+            const long long rows = P * g * c / N;
+            out->family = SGAP_ROW_MULTIPLE;
+            out->chunk = rows;
+            out->grid_size = ceil_div(num_rows, rows);
+            out->block_size = P;
+        }
+    }
+    return SGAP_OK;
+}
+
+int sgap_block_starts(const int32_t *d_row_ptr, int64_t num_rows, int64_t chunk,
+                      int64_t num_blocks, int32_t *d_starts, void *stream) {
+    if (chunk < 1 || num_blocks < 0 || num_rows < 0) return SGAP_ERR_ARG;
+    if (d_row_ptr == nullptr || d_starts == nullptr) return SGAP_ERR_ARG;
+    const long long n = num_blocks + 1;
+    k_block_starts<<<(unsigned)ceil_div(n, 256), 256, 0, as_stream(stream)>>>(
+        d_row_ptr, num_rows, chunk, num_blocks, d_starts);
+    return launch_status();
+}
+
+int sgap_run(const sgap_kernel_t *k, const sgap_csr_t *a, const void *d_b, void *d_c,
+             int32_t dtype, int32_t accumulate, const int32_t *d_block_starts,
+             unsigned long long *d_writebacks, void *stream) {
+    if (k == nullptr || a == nullptr) return SGAP_ERR_ARG;
+    if (dtype != SGAP_F32 && dtype != SGAP_F64) return SGAP_ERR_PRECISION;
+    if (k->n < 1 || k->c < 1 || k->n % k->c) return SGAP_ERR_CONFIG;
+    if (a->num_rows < 0 || a->num_cols < 0 || a->nnz < 0) return SGAP_ERR_SHAPE;
+    if (a->num_rows > INT_MAX - 1 || a->nnz > INT_MAX) return SGAP_ERR_SHAPE;
+    const size_t esz = dtype == SGAP_F32 ? 4 : 8;
+    const long long out_elems = a->num_rows * (long long)k->n;
+    cudaStream_t st = as_stream(stream);
+    if (out_elems == 0) return SGAP_OK;
+    if (d_c == nullptr || a->d_row_ptr == nullptr) return SGAP_ERR_ARG;
+    if (a->nnz > 0 && (d_b == nullptr || a->d_col_idx == nullptr || a->d_vals == nullptr))
+        return SGAP_ERR_ARG;
+    const size_t vec_bytes = esz * (size_t)(k->c == 4 && esz == 8 ? 2 : k->c);
+    if ((d_b && !aligned(d_b, vec_bytes)) || !aligned(d_c, vec_bytes)) return SGAP_ERR_ARG;
+    const bool eb = k->family == SGAP_NNZ_ONE || k->family == SGAP_NNZ_MULTIPLE;
+    if (eb && k->grid_size > 0 && d_block_starts == nullptr) return SGAP_ERR_ARG;
+    if (k->family == SGAP_NNZ_MULTIPLE && (k->g < 1 || k->chunk % k->g)) return SGAP_ERR_CONFIG;
+    if (eb && !accumulate) {
+        // atomic-writeback families accumulate into C: zero-fill (counts as
+        // part of the SpMM).
+        if (cudaMemsetAsync(d_c, 0, (size_t)out_elems * esz, st) != cudaSuccess)
+            return SGAP_ERR_CUDA;
+    }
+    if (eb && k->grid_size == 0) return SGAP_OK;
+    if (dtype == SGAP_F32)
+        return run_typed<float>(*k, *a, d_b, d_c, accumulate, d_block_starts, d_writebacks, st);
+    return run_typed<double>(*k, *a, d_b, d_c, accumulate, d_block_starts, d_writebacks, st);
+}
+
+int sgap_reference_spmm_f64(const sgap_csr_t *a, const void *d_b, int32_t n, int32_t dtype,
+                            double *d_c, void *stream) {
+    if (a == nullptr || n < 1) return SGAP_ERR_ARG;
+    if (dtype != SGAP_F32 && dtype != SGAP_F64) return SGAP_ERR_PRECISION;
+    if (a->num_rows > INT_MAX - 1 || a->nnz > INT_MAX) return SGAP_ERR_SHAPE;
+    const long long cells = a->num_rows * (long long)n;
+    if (cells == 0) return SGAP_OK;
+    if (d_c == nullptr || a->d_row_ptr == nullptr) return SGAP_ERR_ARG;
+    if (a->nnz > 0 && (d_b == nullptr || a->d_col_idx == nullptr || a->d_vals == nullptr))
+        return SGAP_ERR_ARG;
+    long long blocks = ceil_div(cells, kHwBlock);
+    if (blocks > (1LL << 30)) blocks = 1LL << 30;
+    cudaStream_t st = as_stream(stream);
+    if (dtype == SGAP_F32)
+        k_reference_f64<float><<<(unsigned)blocks, kHwBlock, 0, st>>>(
+            a->d_row_ptr, a->d_col_idx, static_cast<const float *>(a->d_vals),
+            static_cast<const float *>(d_b), d_c, (int)a->num_rows, n);
+    else
+        k_reference_f64<double><<<(unsigned)blocks, kHwBlock, 0, st>>>(
+            a->d_row_ptr, a->d_col_idx, static_cast<const double *>(a->d_vals),
+            static_cast<const double *>(d_b), d_c, (int)a->num_rows, n);
+    return launch_status();
+}
+
+int sgap_seg_reduce_group(const int64_t *d_idx, const void *d_val, const uint8_t *d_active,
+                          int64_t lanes, int32_t group_size, void *d_out, int64_t out_len,
+                          int32_t dtype, unsigned long long *d_writebacks, long long *d_fault,
+                          void *stream) {
+    return prim_entry(true, d_idx, d_val, d_active, lanes, group_size, d_out, out_len, dtype,
+                      d_writebacks, d_fault, stream);
+}
+
+int sgap_atomic_add_group(const int64_t *d_idx, const void *d_val, const uint8_t *d_active,
+                          int64_t lanes, int32_t group_size, void *d_out, int64_t out_len,
+                          int32_t dtype, unsigned long long *d_writebacks, long long *d_fault,
+                          void *stream) {
+    return prim_entry(false, d_idx, d_val, d_active, lanes, group_size, d_out, out_len, dtype,
+                      d_writebacks, d_fault, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,230 @@
+// sgap_device.cuh -- device building blocks shared by the SpMM families:
+// vector gathers/stores/reductions over B and C rows, the clamped row search,
+// and the warp-shuffle group reductions that replace the simulator's macros
+// (sim.py:112-165; declared-only in the reference's emitted CUDA, cuda.py:52-56).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sgap {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+// ---------------------------------------------------------------------------
+// c-wide column vectors (c in {1,2,4}); the per-lane unit of a B-row gather and
+// of a C writeback.  A column tile of c consecutive floats is one 4/8/16-byte
+// access; (32/lanes_per_row) tiles of one B row form one coalesced request.
+// ---------------------------------------------------------------------------
+template <typename T, int V>
+struct Vec {
+    T v[V];
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int x = 0; x < V; ++x) v[x] = T(0);
+    }
+};
+
+template <typename T, int V>
+__device__ __forceinline__ void ldg_vec(Vec<T, V> &o, const T *p);
+
+template <>
+__device__ __forceinline__ void ldg_vec<float, 1>(Vec<float, 1> &o, const float *p) {
+    o.v[0] = __ldg(p);
+}
+template <>
+__device__ __forceinline__ void ldg_vec<float, 2>(Vec<float, 2> &o, const float *p) {
+    const float2 t = __ldg(reinterpret_cast<const float2 *>(p));
+    o.v[0] = t.x; o.v[1] = t.y;
+}
+template <>
+__device__ __forceinline__ void ldg_vec<float, 4>(Vec<float, 4> &o, const float *p) {
+    const float4 t = __ldg(reinterpret_cast<const float4 *>(p));
+    o.v[0] = t.x; o.v[1] = t.y; o.v[2] = t.z; o.v[3] = t.w;
+}
+template <>
+__device__ __forceinline__ void ldg_vec<double, 1>(Vec<double, 1> &o, const double *p) {
+    o.v[0] = __ldg(p);
+}
+template <>
+__device__ __forceinline__ void ldg_vec<double, 2>(Vec<double, 2> &o, const double *p) {
+    const double2 t = __ldg(reinterpret_cast<const double2 *>(p));
+    o.v[0] = t.x; o.v[1] = t.y;
+}
+template <>
+__device__ __forceinline__ void ldg_vec<double, 4>(Vec<double, 4> &o, const double *p) {
+    const double2 t0 = __ldg(reinterpret_cast<const double2 *>(p));
+    const double2 t1 = __ldg(reinterpret_cast<const double2 *>(p) + 1);
+    o.v[0] = t0.x; o.v[1] = t0.y; o.v[2] = t1.x; o.v[3] = t1.y;
+}
+
+// Plain (read-modify-)write of an exclusively owned C tile.  C is written
+// exactly once per kernel, so the store is marked evict-first (st.global.cs)
+// to keep L2 for the B rows that are re-gathered.
+template <typename T, int V>
+__device__ __forceinline__ void store_vec(T *p, const Vec<T, V> &a, bool accumulate) {
+    Vec<T, V> o = a;
+    if (accumulate) {
+#pragma unroll
+        for (int x = 0; x < V; ++x) o.v[x] += p[x];
+    }
+    if constexpr (sizeof(T) * V == 16) {
+        if constexpr (sizeof(T) == 4)
+            __stcs(reinterpret_cast<float4 *>(p), make_float4(o.v[0], o.v[1], o.v[2], o.v[3]));
+        else
+            __stcs(reinterpret_cast<double2 *>(p), make_double2(o.v[0], o.v[1]));
+    } else if constexpr (sizeof(T) * V == 8 && sizeof(T) == 4) {
+        __stcs(reinterpret_cast<float2 *>(p), make_float2(o.v[0], o.v[1]));
+    } else if constexpr (V == 4) {  // double x4
+        __stcs(reinterpret_cast<double2 *>(p), make_double2(o.v[0], o.v[1]));
+        __stcs(reinterpret_cast<double2 *>(p) + 1, make_double2(o.v[2], o.v[3]));
+    } else {
+#pragma unroll
+        for (int x = 0; x < V; ++x) __stcs(p + x, o.v[x]);
+    }
+}
+
+// Atomic writeback of a C tile that other lanes may also update
+// (red.global.add.{f32,v2.f32,v4.f32,f64}; the result is unused so ptxas
+// emits REDG).
+template <typename T, int V>
+__device__ __forceinline__ void red_vec(T *p, const Vec<T, V> &a) {
+    if constexpr (sizeof(T) == 4 && V == 4) {
+        atomicAdd(reinterpret_cast<float4 *>(p), make_float4(a.v[0], a.v[1], a.v[2], a.v[3]));
+    } else if constexpr (sizeof(T) == 4 && V == 2) {
+        atomicAdd(reinterpret_cast<float2 *>(p), make_float2(a.v[0], a.v[1]));
+    } else {
+#pragma unroll
+        for (int x = 0; x < V; ++x) atomicAdd(p + x, a.v[x]);
+    }
+}
+
+template <typename T, int V>
+__device__ __forceinline__ void fma_vec(Vec<T, V> &acc, T a, const Vec<T, V> &b) {
+#pragma unroll
+    for (int x = 0; x < V; ++x) acc.v[x] = fma(a, b.v[x], acc.v[x]);
+}
+
+template <typename T, int V>
+__device__ __forceinline__ void add_vec(Vec<T, V> &acc, const Vec<T, V> &b) {
+#pragma unroll
+    for (int x = 0; x < V; ++x) acc.v[x] += b.v[x];
+}
+
+// ---------------------------------------------------------------------------
+// binary_search_before (lowering.py:99-116; device text cuda.py:37-50):
+// largest p in [lo, hi) with a[p] <= target, clamped to lo.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int search_before(const int *__restrict__ a, int lo, int hi,
+                                             long long target) {
+    if (hi <= lo) return lo;
+    if ((long long)__ldg(a + lo) > target) return lo;
+    while (hi - lo > 1) {
+        const int mid = (int)(((unsigned)lo + (unsigned)hi) >> 1);
+        if ((long long)__ldg(a + mid) <= target) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+// Row a position-chunked lane resolves to (lowering.py:459-500): clamped
+// search in the block window [starts[b], min(starts[b+1]+1, M)), then -- for
+// in-range positions -- the forward advance over rows ending at the position.
+__device__ __forceinline__ int lane_row(const int *__restrict__ rp,
+                                        const int *__restrict__ starts, long long block,
+                                        long long pos, long long nnz, int M) {
+    int hi = __ldg(starts + block + 1) + 1;
+    hi = hi < M ? hi : M;
+    int i = search_before(rp, __ldg(starts + block), hi, pos);
+    if (pos < nnz) {
+        while (pos == (long long)__ldg(rp + i + 1)) ++i;
+    }
+    return i;
+}
+
+// ---------------------------------------------------------------------------
+// Segment group (SegReduceGroup, sim.py:139-165): within each aligned group of
+// R lanes, runs of equal key among ACTIVE lanes (inactive lanes do not break a
+// run) each produce one writeback from the run's last active lane.
+// The segment heads come from one ballot; the run sums from a log2(R)-step
+// shfl_up scan restricted to the distance to the lane's head.
+// ---------------------------------------------------------------------------
+struct SegLanes {
+    bool head;        // first active lane of a run
+    bool tail;        // last active lane of a run: owns the writeback
+    bool decreasing;  // key below the previous active key (group invariant broken)
+    int dist;         // lanes back to the run head (scan reach)
+};
+
+template <int R, typename K>
+__device__ __forceinline__ SegLanes seg_lanes(K key, bool active) {
+    const unsigned lane = lane_id();
+    const unsigned gbase = lane & ~(unsigned)(R - 1);
+    const unsigned gmask = (R >= 32) ? kFull : (((1u << R) - 1u) << gbase);
+    const unsigned le = kFull >> (31u - lane);
+    const unsigned act = __ballot_sync(kFull, active) & gmask;
+    const unsigned below = act & (le ^ (1u << lane));
+    const int prev = below ? 31 - __clz(below) : (int)lane;
+    const K prev_key = __shfl_sync(kFull, key, prev);
+    SegLanes s;
+    s.head = active && (below == 0u || prev_key != key);
+    s.decreasing = active && below != 0u && key < prev_key;
+    const unsigned heads = __ballot_sync(kFull, s.head);
+    const unsigned above = act & ~le;
+    const int next = above ? __ffs(above) - 1 : -1;
+    s.tail = active && (next < 0 || ((heads >> next) & 1u));
+    const unsigned hb = heads & le & gmask;
+    s.dist = hb ? (int)lane - (31 - __clz(hb)) : 0;
+    return s;
+}
+
+template <int R, typename T>
+__device__ __forceinline__ T seg_scan(T v, int dist) {
+#pragma unroll
+    for (int d = 1; d < R; d <<= 1) {
+        const T up = __shfl_up_sync(kFull, v, d, R);
+        if (d <= dist) v += up;
+    }
+    return v;
+}
+
+template <int R, typename T, int V>
+__device__ __forceinline__ void seg_scan_vec(Vec<T, V> &a, int dist) {
+#pragma unroll
+    for (int d = 1; d < R; d <<= 1) {
+#pragma unroll
+        for (int x = 0; x < V; ++x) {
+            const T up = __shfl_up_sync(kFull, a.v[x], d, R);
+            if (d <= dist) a.v[x] += up;
+        }
+    }
+}
+
+// Parallel group (AtomicAddGroup, sim.py:112-136): xor-tree sum over R lanes;
+// every lane ends with the group total.
+template <int R, typename T>
+__device__ __forceinline__ T group_sum(T v) {
+#pragma unroll
+    for (int off = R / 2; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off, R);
+    return v;
+}
+
+template <int R, typename T, int V>
+__device__ __forceinline__ void group_sum_vec(Vec<T, V> &a) {
+#pragma unroll
+    for (int off = R / 2; off > 0; off >>= 1) {
+#pragma unroll
+        for (int x = 0; x < V; ++x) a.v[x] += __shfl_xor_sync(kFull, a.v[x], off, R);
+    }
+}
+
+// Warp-aggregated writeback counter (SimMetrics.atomic_ops).
+__device__ __forceinline__ void flush_count(unsigned long long *counter, unsigned long long mine) {
+    if (counter == nullptr) return;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) mine += __shfl_xor_sync(kFull, mine, off);
+    if (lane_id() == 0 && mine) atomicAdd(counter, mine);
+}
+
+}  // namespace sgap

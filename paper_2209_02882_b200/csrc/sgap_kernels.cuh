@@ -1,0 +1,433 @@
+// sgap_kernels.cuh -- the four Sgap template families as sm_100a kernels.
+//
+// Each kernel keeps the reference family's work decomposition -- which
+// positions/rows/cells form one reduction, which lanes reduce together, where
+// a writeback happens (so SimMetrics.atomic_ops is reproduced exactly) -- and
+// chooses its own hardware lane mapping: lanes run along the dense columns in
+// c-wide vectors wherever the family allows it, so a B-row gather and a C-row
+// writeback are one coalesced request per warp.
+//
+// Reference (paths relative to /root/reference/pkg/src/spmmlab/):
+//   k_row_multiple     row:g,col:c,r:1     templates.py:137-154, lowering.py:416-420,573-585,643-646
+//   k_row_reciprocal   row:1/g,col:c,r:g   templates.py:157-177, lowering.py:427-439,587-624
+//   k_nnz_one          nnz:1,col:c,r       templates.py:180-202, lowering.py:459-488,526-537,626-642
+//   k_nnz_multiple     nnz:g,col:c,r:1     templates.py:114-134, lowering.py:490-500,539-571
+#pragma once
+
+#include "sgap_device.cuh"
+
+namespace sgap {
+
+// Warp-uniform grid-stride iteration over warp work items.
+#define SGAP_WARP_LOOP(item, items)                                                     \
+    for (long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;     \
+         item < (items); item += ((long long)gridDim.x * blockDim.x) >> 5)
+
+constexpr int kBatch = 4;  // independent gathers kept in flight per lane
+
+// ===========================================================================
+// RB + serial reduction: row:g,col:c,r:1 (row-multiple).
+// Logical thread (rg, t): rows rg*g .. rg*g+g-1, columns t*c .. t*c+c-1,
+// serial dot product over each row, one plain store per (row, tile)
+// (cuda_row_multiple.cu:37-43).  Hardware: L = N/c lanes per row group; when
+// L divides 32 (or is a multiple of 32) the lanes sharing a row stage that
+// row's (col, val) pairs with one coalesced load and shuffle them, which also
+// lets kBatch B-row gathers issue back to back.
+// ===========================================================================
+template <typename T, int V>
+__global__ void __launch_bounds__(256)
+k_row_multiple(const int *__restrict__ rp, const int *__restrict__ ci,
+               const T *__restrict__ av, const T *__restrict__ B, T *__restrict__ C,
+               int M, int N, int g, int S, int accumulate) {
+    const int L = N / V;
+    const long long groups = ((long long)M + g - 1) / g;
+    const long long total = groups * L;           // logical threads
+    const long long items = (total + 31) >> 5;
+    const unsigned lane = lane_id();
+    SGAP_WARP_LOOP(item, items) {
+        const long long h = item * 32 + lane;
+        const bool live = h < total;
+        const long long rg = live ? h / L : 0;
+        const int t = live ? (int)(h - rg * L) : 0;
+        const long long kcol = (long long)t * V;
+        for (int s = 0; s < g; ++s) {
+            const long long i = rg * g + s;
+            const bool row_ok = live && i < M;
+            const int beg = row_ok ? __ldg(rp + i) : 0;
+            const int len = row_ok ? __ldg(rp + i + 1) - beg : 0;
+            Vec<T, V> acc[kBatch];
+#pragma unroll
+            for (int u = 0; u < kBatch; ++u) acc[u].zero();
+            if (S > 0) {
+                // Staged: S lanes (aligned) share the row; warp-uniform trip count.
+                const int maxlen = __reduce_max_sync(kFull, len);
+                const int sl = (int)(lane & (unsigned)(S - 1));
+                for (int base = 0; base < maxlen; base += S) {
+                    int my_c = 0;
+                    T my_v = T(0);
+                    if (base + sl < len) {
+                        my_c = __ldg(ci + beg + base + sl);
+                        my_v = __ldg(av + beg + base + sl);
+                    }
+                    const int cnt = min(S, maxlen - base);
+                    for (int j = 0; j < cnt; j += kBatch) {
+                        int cc[kBatch];
+                        T vv[kBatch];
+#pragma unroll
+                        for (int u = 0; u < kBatch; ++u) {
+                            cc[u] = __shfl_sync(kFull, my_c, j + u, S);
+                            vv[u] = __shfl_sync(kFull, my_v, j + u, S);
+                        }
+                        Vec<T, V> bv[kBatch];
+#pragma unroll
+                        for (int u = 0; u < kBatch; ++u) {
+                            if (j + u < cnt && base + j + u < len)
+                                ldg_vec<T, V>(bv[u], B + (long long)cc[u] * N + kcol);
+                            else {
+                                bv[u].zero();
+                                vv[u] = T(0);
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < kBatch; ++u) fma_vec<T, V>(acc[u], vv[u], bv[u]);
+                    }
+                }
+            } else {
+                // Direct: row lanes straddle warps; each lane walks the row.
+                int p = beg;
+                const int end = beg + len;
+                for (; p + kBatch <= end; p += kBatch) {
+                    int cc[kBatch];
+                    T vv[kBatch];
+                    Vec<T, V> bv[kBatch];
+#pragma unroll
+                    for (int u = 0; u < kBatch; ++u) {
+                        cc[u] = __ldg(ci + p + u);
+                        vv[u] = __ldg(av + p + u);
+                    }
+#pragma unroll
+                    for (int u = 0; u < kBatch; ++u)
+                        ldg_vec<T, V>(bv[u], B + (long long)cc[u] * N + kcol);
+#pragma unroll
+                    for (int u = 0; u < kBatch; ++u) fma_vec<T, V>(acc[u], vv[u], bv[u]);
+                }
+                for (; p < end; ++p) {
+                    Vec<T, V> bv;
+                    ldg_vec<T, V>(bv, B + (long long)__ldg(ci + p) * N + kcol);
+                    fma_vec<T, V>(acc[0], __ldg(av + p), bv);
+                }
+            }
+#pragma unroll
+            for (int u = 1; u < kBatch; ++u) add_vec<T, V>(acc[0], acc[u]);
+            if (row_ok) store_vec<T, V>(C + i * N + kcol, acc[0], accumulate != 0);
+        }
+    }
+}
+
+// ===========================================================================
+// RB + parallel group reduction: row:1/g,col:c,r:g (row-reciprocal).
+// A group of G lanes owns c consecutive fused cells io = i*N + k (one row, c
+// columns); lane j accumulates positions begin+j, begin+j+G, ...
+// (cuda_row_reciprocal.cu:39-46), then the AtomicAddGroup becomes an
+// xor-shuffle tree and a single exclusive store by the group's lane 0.
+// ===========================================================================
+template <typename T, int V, int G>
+__global__ void __launch_bounds__(256)
+k_row_reciprocal(const int *__restrict__ rp, const int *__restrict__ ci,
+                 const T *__restrict__ av, const T *__restrict__ B, T *__restrict__ C,
+                 int M, int N, int accumulate, unsigned long long *wb) {
+    const long long cells = (long long)M * N;
+    const long long groups = (cells + V - 1) / V;
+    const long long total = groups * G;
+    const long long items = (total + 31) >> 5;
+    const unsigned lane = lane_id();
+    unsigned long long nwb = 0;
+    SGAP_WARP_LOOP(item, items) {
+        const long long h = item * 32 + lane;
+        const long long grp = h / G;
+        const int j = (int)(h % G);
+        const long long io0 = grp * V;
+        const bool ok = io0 < cells;
+        const long long i = ok ? io0 / N : 0;
+        const long long k0 = ok ? io0 - i * N : 0;
+        const int beg = ok ? __ldg(rp + i) : 0;
+        const int end = ok ? __ldg(rp + i + 1) : 0;
+        Vec<T, V> acc[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) acc[u].zero();
+        int p = beg + j;
+        for (; p + (kBatch - 1) * G < end; p += kBatch * G) {
+            int cc[kBatch];
+            T vv[kBatch];
+            Vec<T, V> bv[kBatch];
+#pragma unroll
+            for (int u = 0; u < kBatch; ++u) {
+                cc[u] = __ldg(ci + p + u * G);
+                vv[u] = __ldg(av + p + u * G);
+            }
+#pragma unroll
+            for (int u = 0; u < kBatch; ++u) ldg_vec<T, V>(bv[u], B + (long long)cc[u] * N + k0);
+#pragma unroll
+            for (int u = 0; u < kBatch; ++u) fma_vec<T, V>(acc[u], vv[u], bv[u]);
+        }
+        for (; p < end; p += G) {
+            Vec<T, V> bv;
+            ldg_vec<T, V>(bv, B + (long long)__ldg(ci + p) * N + k0);
+            fma_vec<T, V>(acc[0], __ldg(av + p), bv);
+        }
+#pragma unroll
+        for (int u = 1; u < kBatch; ++u) add_vec<T, V>(acc[0], acc[u]);
+        group_sum_vec<G, T, V>(acc[0]);
+        if (ok && j == 0) {
+            store_vec<T, V>(C + i * N + k0, acc[0], accumulate != 0);
+            nwb += V;
+        }
+    }
+    flush_count(wb, nwb);
+}
+
+// ===========================================================================
+// EB + segment group (r > 1) / EB + atomic (r = 1): nnz:1,col:c,r (nnz-one).
+// Logical thread = one position x one c-wide column tile; positions are padded
+// to grid*npb and out-of-range lanes are zero-extended with the clamped search
+// row (cuda_nnz_one_segment.cu:33-49).  Segment groups are aligned runs of r
+// positions (npb % r == 0 makes block boundaries group boundaries).
+// Hardware: a warp holds Q positions x TW tiles (Q*TW = 32, r | Q, lanes
+// position-fastest), so each r-group is r consecutive lanes for the segmented
+// scan while the TW tiles of one position form a coalesced B-row gather and
+// C-row writeback.  One row search per position serves every tile.
+// ===========================================================================
+template <typename T, int V, int R>
+__global__ void __launch_bounds__(256)
+k_nnz_one(const int *__restrict__ rp, const int *__restrict__ ci, const T *__restrict__ av,
+          const T *__restrict__ B, T *__restrict__ C, const int *__restrict__ starts,
+          int M, int N, long long nnz, long long npb, long long grid, int TW,
+          unsigned long long *wb) {
+    const int NT = N / V;
+    const int Q = 32 / TW;
+    const long long total_pos = grid * npb;
+    const long long items = (total_pos + Q - 1) / Q;
+    const unsigned lane = lane_id();
+    const int ql = (int)(lane & (unsigned)(Q - 1));
+    const int tl = (int)(lane / (unsigned)Q);
+    unsigned long long nwb = 0;
+    SGAP_WARP_LOOP(item, items) {
+        const long long pos = item * Q + ql;
+        const bool in_grid = pos < total_pos;
+        const bool in_nnz = pos < nnz;
+        int row = 0;
+        if (in_grid) row = lane_row(rp, starts, pos / npb, pos, nnz, M);
+        const int col = in_nnz ? __ldg(ci + pos) : 0;
+        const T a = in_nnz ? __ldg(av + pos) : T(0);
+        SegLanes sl{};
+        if constexpr (R > 1) sl = seg_lanes<R, int>(row, in_grid);
+        const T *brow = B + (long long)col * N;
+        T *crow = C + (long long)row * N;
+        for (int tt = 0; tt < NT; tt += TW) {
+            const int tile = tt + tl;
+            const bool tok = tile < NT;
+            Vec<T, V> prod;
+            prod.zero();
+            if (in_nnz && tok) {
+                Vec<T, V> bv;
+                ldg_vec<T, V>(bv, brow + (long long)tile * V);
+#pragma unroll
+                for (int x = 0; x < V; ++x) prod.v[x] = a * bv.v[x];
+            }
+            if constexpr (R == 1) {
+                if (in_nnz && tok) {
+                    red_vec<T, V>(crow + (long long)tile * V, prod);
+                    nwb += V;
+                }
+            } else {
+                seg_scan_vec<R, T, V>(prod, sl.dist);
+                if (sl.tail && tok) {
+                    red_vec<T, V>(crow + (long long)tile * V, prod);
+                    nwb += V;
+                }
+            }
+        }
+    }
+    flush_count(wb, nwb);
+}
+
+// ===========================================================================
+// EB + serial reduction: nnz:g,col:c,r:1 (nnz-multiple, the TACO nnz split).
+// Logical work = one aligned chunk of g positions x one column; the walk
+// tracks its row with the block-window search plus forward advance, flushing
+// an atomic at every row change and once at the end -- also for chunks past
+// nnz (cuda_nnz_multiple.cu:33-53).  Hardware: TW lanes x c columns per chunk,
+// 32/TW chunks per warp; kBatch positions' (col, val) and B rows are fetched
+// before the serial flush logic consumes them.
+// ===========================================================================
+template <typename T, int V>
+__global__ void __launch_bounds__(256)
+k_nnz_multiple(const int *__restrict__ rp, const int *__restrict__ ci,
+               const T *__restrict__ av, const T *__restrict__ B, T *__restrict__ C,
+               const int *__restrict__ starts, int M, int N, long long nnz, int g,
+               long long chunk, long long grid, int TW, unsigned long long *wb) {
+    const int NT = N / V;
+    const int SG = 32 / TW;
+    const long long cpb = chunk / g;
+    const long long total_chunks = grid * cpb;
+    const long long items = (total_chunks + SG - 1) / SG;
+    const unsigned lane = lane_id();
+    const int sg = (int)(lane / (unsigned)TW);
+    const int tl = (int)(lane & (unsigned)(TW - 1));
+    unsigned long long nwb = 0;
+    SGAP_WARP_LOOP(item, items) {
+        const long long ch = item * SG + sg;
+        if (ch >= total_chunks) continue;
+        const long long base = ch * g;
+        const long long end = min(base + (long long)g, nnz);
+        int hi = __ldg(starts + ch / cpb + 1) + 1;
+        hi = hi < M ? hi : M;
+        const int row0 = search_before(rp, __ldg(starts + ch / cpb), hi, base);
+        for (int tile = tl; tile < NT; tile += TW) {
+            const long long kcol = (long long)tile * V;
+            int row = row0;
+            long long nb = __ldg(rp + row + 1);
+            Vec<T, V> acc;
+            acc.zero();
+            long long pos = base;
+            for (; pos < end; pos += kBatch) {
+                int cc[kBatch];
+                T vv[kBatch];
+                Vec<T, V> bv[kBatch];
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) {
+                    const bool ok = pos + u < end;
+                    cc[u] = ok ? __ldg(ci + pos + u) : 0;
+                    vv[u] = ok ? __ldg(av + pos + u) : T(0);
+                }
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) {
+                    if (pos + u < end) ldg_vec<T, V>(bv[u], B + (long long)cc[u] * N + kcol);
+                    else bv[u].zero();
+                }
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) {
+                    if (pos + u < end) {
+                        if (pos + u == nb) {
+                            red_vec<T, V>(C + (long long)row * N + kcol, acc);
+                            nwb += V;
+                            acc.zero();
+                            do {
+                                ++row;
+                                nb = __ldg(rp + row + 1);
+                            } while (pos + u == nb);
+                        }
+                        fma_vec<T, V>(acc, vv[u], bv[u]);
+                    }
+                }
+            }
+            red_vec<T, V>(C + (long long)row * N + kcol, acc);
+            nwb += V;
+        }
+    }
+    flush_count(wb, nwb);
+}
+
+// The verification product of runner.verify_point (runner.py:193-194): the
+// dense reference C = A@B in float64, per (i,k) ascending-p order with the
+// multiply and the add rounded separately (no FMA contraction) -- the same
+// arithmetic as matrices.dense_spmm_oracle (matrices.py:241-254), evaluated on
+// the device so the check needs no host SpMM.  One lane per (i, k); lanes of a
+// warp run along k, so every B-row read is coalesced.
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_reference_f64(const int *__restrict__ rp, const int *__restrict__ ci,
+                const T *__restrict__ av, const T *__restrict__ B, double *__restrict__ C,
+                int M, int N) {
+    const long long cells = (long long)M * N;
+    for (long long h = (long long)blockIdx.x * blockDim.x + threadIdx.x; h < cells;
+         h += (long long)gridDim.x * blockDim.x) {
+        const long long i = h / N;
+        const long long k = h - i * N;
+        double acc = 0.0;
+        const int end = __ldg(rp + i + 1);
+        for (int p = __ldg(rp + i); p < end; ++p) {
+            const double prod = __dmul_rn((double)__ldg(av + p),
+                                          (double)__ldg(B + (long long)__ldg(ci + p) * N + k));
+            acc = __dadd_rn(acc, prod);
+        }
+        C[h] = acc;
+    }
+}
+
+// lowering.compute_block_starts (lowering.py:119-128) on the device.
+__global__ void k_block_starts(const int *__restrict__ rp, long long M, long long chunk,
+                               long long nb, int *__restrict__ out) {
+    const long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b > nb) return;
+    const long long t = b * chunk;
+    long long lo = 0, hi = M + 1;
+    while (lo < hi) {
+        const long long mid = lo + ((hi - lo) >> 1);
+        if ((long long)__ldg(rp + mid) <= t) lo = mid + 1; else hi = mid;
+    }
+    out[b] = (int)(lo - 1);
+}
+
+// ===========================================================================
+// The simulator's group macros over explicit lane vectors (sim.py:112-165),
+// running the same seg_lanes / seg_scan / group_sum code as the kernels.
+// ===========================================================================
+template <typename T, int R>
+__global__ void __launch_bounds__(256)
+k_seg_reduce_prim(const long long *__restrict__ idx, const T *__restrict__ val,
+                  const unsigned char *__restrict__ active, long long lanes, T *out,
+                  long long out_len, unsigned long long *wb, long long *fault) {
+    const long long items = (lanes + 31) >> 5;
+    unsigned long long nwb = 0;
+    SGAP_WARP_LOOP(item, items) {
+        const long long L = item * 32 + lane_id();
+        const bool act = L < lanes && (active == nullptr || active[L] != 0);
+        const long long key = act ? idx[L] : 0;
+        const T v = act ? val[L] : T(0);
+        const SegLanes s = seg_lanes<R, long long>(key, act);
+        if (s.decreasing) atomicMin(fault, L);
+        const T sum = seg_scan<R, T>(v, s.dist);
+        if (s.tail) {
+            if (key < 0 || key >= out_len) atomicMin(fault, L);
+            else atomicAdd(out + key, sum);
+            ++nwb;
+        }
+    }
+    flush_count(wb, nwb);
+}
+
+template <typename T, int R>
+__global__ void __launch_bounds__(256)
+k_atomic_add_prim(const long long *__restrict__ idx, const T *__restrict__ val,
+                  const unsigned char *__restrict__ active, long long lanes, T *out,
+                  long long out_len, unsigned long long *wb, long long *fault) {
+    const long long items = (lanes + 31) >> 5;
+    unsigned long long nwb = 0;
+    const unsigned lane = lane_id();
+    SGAP_WARP_LOOP(item, items) {
+        const long long L = item * 32 + lane;
+        const bool act = L < lanes && (active == nullptr || active[L] != 0);
+        const long long key = act ? idx[L] : 0;
+        T v = act ? val[L] : T(0);
+        long long lo = act ? key : LLONG_MAX, hi = act ? key : LLONG_MIN;
+#pragma unroll
+        for (int off = R / 2; off > 0; off >>= 1) {
+            lo = min(lo, __shfl_xor_sync(kFull, lo, off, R));
+            hi = max(hi, __shfl_xor_sync(kFull, hi, off, R));
+        }
+        v = group_sum<R, T>(v);
+        const unsigned gbase = lane & ~(unsigned)(R - 1);
+        const unsigned gmask = (R >= 32) ? kFull : (((1u << R) - 1u) << gbase);
+        const unsigned act_mask = __ballot_sync(kFull, act) & gmask;
+        const bool leader = act_mask != 0u && (int)lane == __ffs(act_mask) - 1;
+        if (leader) {
+            if (lo != hi || key < 0 || key >= out_len) atomicMin(fault, L);
+            else atomicAdd(out + key, v);
+            ++nwb;
+        }
+    }
+    flush_count(wb, nwb);
+}
+
+}  // namespace sgap

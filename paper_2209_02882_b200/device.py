@@ -1,0 +1,168 @@
+"""Device-resident operands and the stream-ordered SpMM call.
+
+PyTorch is used here only as plumbing -- device allocation, streams, events
+and host<->device copies.  Every FLOP of the SpMM runs in ``libsgap.so``
+(``include/sgap.h``), reached through ctypes with raw device pointers.
+
+Device layout: ``row_ptr`` int32[M+1],
+``col_idx`` int32[nnz], ``vals`` float32|float64[nnz]; B row-major [K, N];
+C row-major [M, N]; all 64-bit element offsets inside the kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native
+from .lowering import LoweredKernel
+
+__all__ = ["DeviceCsr", "kernel_struct", "device_block_starts", "spmm", "reference_spmm_f64",
+           "torch_dtype", "native_dtype", "require_cuda"]
+
+_INT32_MAX = 2**31 - 1
+
+
+def require_cuda(device=None) -> torch.device:
+    """The product path runs on a CUDA device only -- fail loudly otherwise."""
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2209_02882_b200 needs a CUDA (sm_100a) device; none is visible")
+    _native.lib()
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if dev.type != "cuda":
+        raise ValueError(f"device must be a CUDA device, got {dev}")
+    return dev
+
+
+def torch_dtype(precision: str) -> torch.dtype:
+    if precision == "single":
+        return torch.float32
+    if precision == "double":
+        return torch.float64
+    raise ValueError(f"unknown precision {precision!r}")
+
+
+def native_dtype(t: torch.dtype) -> int:
+    if t == torch.float32:
+        return _native.F32
+    if t == torch.float64:
+        return _native.F64
+    raise ValueError(f"unsupported value dtype {t}")
+
+
+@dataclass
+class DeviceCsr:
+    """CSR operand resident in HBM (int32 indices)."""
+
+    num_rows: int
+    num_cols: int
+    row_ptr: torch.Tensor
+    col_idx: torch.Tensor
+    vals: torch.Tensor
+
+    @property
+    def nnz(self) -> int:
+        return int(self.col_idx.numel())
+
+    @property
+    def device(self) -> torch.device:
+        return self.row_ptr.device
+
+    @classmethod
+    def from_host(cls, a, *, dtype=torch.float32, device=None, non_blocking=False) -> "DeviceCsr":
+        """Upload any CSR with num_rows/num_cols/row_ptr/col_idx/vals (ours
+        or the reference's CsrMatrix)."""
+        dev = require_cuda(device)
+        rp = np.asarray(a.row_ptr)
+        if rp[-1] > _INT32_MAX or a.num_rows >= _INT32_MAX:
+            raise ValueError("nnz and num_rows must fit int32 on the device")
+        ci = np.asarray(a.col_idx)
+        vals = np.asarray(a.vals)
+        np_dt = np.float32 if dtype == torch.float32 else np.float64
+
+        def up(x, dt):
+            t = torch.from_numpy(np.ascontiguousarray(x, dtype=dt))
+            if non_blocking:
+                t = t.pin_memory()
+            return t.to(dev, non_blocking=non_blocking)
+
+        return cls(int(a.num_rows), int(a.num_cols), up(rp, np.int32), up(ci, np.int32),
+                   up(vals, np_dt))
+
+    def view(self) -> _native.Csr:
+        return _native.Csr(self.num_rows, self.num_cols, self.nnz, self.row_ptr.data_ptr(),
+                           self.col_idx.data_ptr(), self.vals.data_ptr())
+
+    def nbytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in (self.row_ptr, self.col_idx, self.vals))
+
+    def slice_rows(self, lo: int, hi: int) -> "DeviceCsr":
+        """Rows [lo, hi) as a rebased CSR (device copy of the row_ptr slice;
+        col/val are views).  Used by the row-shard partitioner."""
+        rp = self.row_ptr[lo:hi + 1]
+        base = int(rp[0].item())
+        end = int(rp[-1].item())
+        return DeviceCsr(hi - lo, self.num_cols, (rp - base).contiguous(), self.col_idx[base:end],
+                         self.vals[base:end])
+
+
+def kernel_struct(k: LoweredKernel, *, hw_block: int = 0) -> _native.Kernel:
+    fam = _native.FAMILY_IDS[k.family]
+    return _native.Kernel(fam, k.n, k.p, k.g, k.c, k.r, k.chunk, k.grid_size, k.block_size,
+                          1 if k.family in ("nnz-one", "nnz-multiple") else 0, hw_block)
+
+
+def _stream_handle(stream) -> ctypes.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def device_block_starts(a: DeviceCsr, chunk: int, num_blocks: int, *, stream=None) -> torch.Tensor:
+    """lowering.compute_block_starts on the device (int32[num_blocks + 1])."""
+    out = torch.empty(num_blocks + 1, dtype=torch.int32, device=a.device)
+    _native.check(_native.lib().sgap_block_starts(a.row_ptr.data_ptr(), a.num_rows, chunk,
+                                                  num_blocks, out.data_ptr(), _stream_handle(stream)),
+                  "sgap_block_starts")
+    return out
+
+
+def spmm(k: LoweredKernel, a: DeviceCsr, b: torch.Tensor, c: torch.Tensor, *,
+         accumulate: bool = False, starts: torch.Tensor | None = None,
+         writebacks: torch.Tensor | None = None, hw_block: int = 0, stream=None) -> None:
+    """C (+)= A @ B with kernel ``k``, stream-ordered, no host synchronisation.
+
+    ``b``: [num_cols, n] and ``c``: [num_rows, n] contiguous tensors of the
+    value dtype of ``a``; ``starts`` from ``device_block_starts`` (computed
+    here when omitted); ``writebacks``: optional int64[1] counter.
+    """
+    if b.dtype != a.vals.dtype or c.dtype != a.vals.dtype:
+        raise ValueError("A, B and C must share one value dtype")
+    if tuple(b.shape) != (a.num_cols, k.n) or tuple(c.shape) != (a.num_rows, k.n):
+        raise ValueError(
+            f"shape mismatch: A is {a.num_rows}x{a.num_cols}, B {tuple(b.shape)}, C {tuple(c.shape)}, n={k.n}")
+    if not (b.is_contiguous() and c.is_contiguous()):
+        raise ValueError("B and C must be contiguous row-major")
+    if k.family in ("nnz-one", "nnz-multiple") and starts is None and k.grid_size > 0:
+        starts = device_block_starts(a, k.chunk, k.grid_size, stream=stream)
+    ks = kernel_struct(k, hw_block=hw_block)
+    view = a.view()
+    st = _native.lib().sgap_run(
+        ctypes.byref(ks), ctypes.byref(view), b.data_ptr(), c.data_ptr(),
+        native_dtype(a.vals.dtype), 1 if accumulate else 0,
+        starts.data_ptr() if starts is not None else None,
+        writebacks.data_ptr() if writebacks is not None else None, _stream_handle(stream))
+    _native.check(st, "sgap_run")
+
+
+def reference_spmm_f64(a: DeviceCsr, b: torch.Tensor, n: int, *, stream=None) -> torch.Tensor:
+    """The verify_point reference product in float64 on the device."""
+    out = torch.empty((a.num_rows, n), dtype=torch.float64, device=a.device)
+    view = a.view()
+    st = _native.lib().sgap_reference_spmm_f64(ctypes.byref(view), b.data_ptr(), n,
+                                               native_dtype(a.vals.dtype), out.data_ptr(),
+                                               _stream_handle(stream))
+    _native.check(st, "sgap_reference_spmm_f64")
+    return out

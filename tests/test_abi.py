@@ -1,0 +1,71 @@
+"""The C ABI boundary: libsgap.so loads without a GPU, exports exactly what
+include/sgap.h declares, and host-only entry points validate arguments.
+No compute call is made here (no GPU in the CPU suite)."""
+
+import ctypes
+import re
+import subprocess
+from pathlib import Path
+
+import pytest
+
+from paper_2209_02882_b200 import _native
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def declared_symbols():
+    text = (ROOT / "include" / "sgap.h").read_text()
+    return sorted(set(re.findall(r"^\s*(?:int|const char \*)\s*(sgap_\w+)\(", text, re.M)))
+
+
+def test_header_and_binding_agree():
+    assert declared_symbols() == sorted(_native.EXPORTED)
+
+
+def test_library_exports_every_declared_symbol():
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_native.LIB_PATH)],
+                         capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r"\sT\s(sgap_\w+)", out))
+    missing = set(declared_symbols()) - exported
+    assert not missing, missing
+    L = _native.lib()
+    for name in declared_symbols():
+        assert hasattr(L, name)
+
+
+def test_abi_version_and_status_strings():
+    L = _native.lib()
+    assert L.sgap_abi_version() == 1
+    assert _native.status_string(_native.ERR_NO_TEMPLATE) == "no template covers the point"
+    assert _native.status_string(99) == "unknown status"
+
+
+def test_library_is_sm100a_only():
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_native.LIB_PATH)],
+                         capture_output=True, text=True, check=True).stdout
+    arches = set(re.findall(r"sm_\d+a?", out))
+    assert arches == {"sm_100a"}, arches
+
+
+def test_argument_validation_without_device():
+    L = _native.lib()
+    k = _native.Kernel()
+    assert L.sgap_run(None, None, None, None, 0, 0, None, None, None) == _native.ERR_ARG
+    k.n, k.c = 4, 1
+    a = _native.Csr()
+    assert L.sgap_run(ctypes.byref(k), ctypes.byref(a), None, None, 7, 0, None, None,
+                      None) == _native.ERR_PRECISION
+    # zero-sized output: nothing to do, no device touched
+    assert L.sgap_run(ctypes.byref(k), ctypes.byref(a), None, None, 0, 0, None, None,
+                      None) == _native.OK
+    assert L.sgap_block_starts(None, 4, 0, 1, None, None) == _native.ERR_ARG
+    assert L.sgap_seg_reduce_group(None, None, None, 5, 4, None, 0, 0, None, None, None) == _native.ERR_ARG
+    assert L.sgap_atomic_add_group(None, None, None, 8, 3, None, 0, 0, None, None, None) == _native.ERR_ARG
+
+
+def test_missing_library_fails_loudly(monkeypatch, tmp_path):
+    monkeypatch.setattr(_native, "LIB_PATH", tmp_path / "nope.so")
+    monkeypatch.setattr(_native, "_lib", None)
+    with pytest.raises(_native.NativeLibraryError):
+        _native.lib()
