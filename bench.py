@@ -1,0 +1,415 @@
+#!/usr/bin/env python
+"""Benchmark: CSR SpMM GFLOP/s (2*nnz*N/t) and HBM GB/s vs roofline on B200.
+
+    python bench.py [--gpus N --steps K --warmup W] [--config 2] [--point P --p 256]
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port P bench.py --gpus N ...
+    python bench.py --impl reference ...   # the reference's CPU path (oracle port)
+
+Workload (BASELINE.json configs):
+  --config 2 (default): R-MAT scale 20+log2(N), edge factor 16, Graph500
+    (0.57,0.19,0.19,0.05), seeded vertex permutation, duplicates summed,
+    N=128 dense columns, fp32.  At N=1 GPU this is exactly config 2 (1M rows,
+    16.09M nnz); at N GPUs the matrix grows N-fold and is cut into N
+    nnz-balanced row shards (B replicated, C row-disjoint, no collective):
+    per-GPU work stays ~config 2, i.e. weak scaling.
+  --config 1/3/4/5 select the other BASELINE shapes (5 = R-MAT scale 24 at
+    any N: strong scaling of one matrix).
+
+One step = one full SpMM over the resident operands: C zero-fill (atomic
+families) + the sm_100a kernel.  A+B+C exceed the 126 MB L2, so no flush is
+needed between steps.  ``value`` is total GFLOP/s over all ranks with the
+max-over-ranks device time; ``e2e`` repeats the step through the host-buffer
+path (pinned H2D of A and B, kernel, D2H of C) inside the timed region.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "SpMM GFLOP/s (2*nnz*N/t)"
+UNIT = "GFLOP/s"
+FALLBACK_HBM_GBS = 6650.0
+
+
+# --------------------------------------------------------------------------- setup
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--n", type=int, default=0, help="dense width override")
+    ap.add_argument("--point", default="", help="schedule point (default: selector)")
+    ap.add_argument("--p", type=int, default=256)
+    ap.add_argument("--hw-block", type=int, default=0)
+    ap.add_argument("--sweep", default="", help="write the full candidate sweep (JSON) here")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--seed", type=int, default=1)
+    return ap.parse_args()
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def default_n(cfg: int) -> int:
+    return {1: 32, 2: 128, 3: 64, 4: 128, 5: 128}[cfg]
+
+
+def build_workload(cfg: int, world: int, seed: int, device):
+    from paper_2209_02882_b200 import generators as G
+    if cfg == 2:
+        scale = 20 + int(round(math.log2(world)))
+        g = G.rmat(scale, 16, seed=seed, device=device)
+        desc = f"config 2: R-MAT scale {scale}, edge factor 16, permuted" + \
+            (f" ({world}x config 2, {world} nnz-balanced row shards)" if world > 1 else "")
+        return g, desc, "weak"
+    g = G.config_matrix(cfg, device=device, seed=seed)
+    return g, f"config {cfg}: {g.label}", "strong"
+
+
+def dense_b(num_rows: int, n: int, seed: int, device) -> torch.Tensor:
+    gen = torch.Generator(device=device)
+    gen.manual_seed(seed + 1)
+    return (torch.rand((num_rows, n), generator=gen, dtype=torch.float32, device=device) * 2.0 - 1.0)
+
+
+class ClockSampler:
+    """NVML clock/throttle sampling in a thread during the timed region."""
+
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+        "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+        "hw_power_brake_slowdown": 0x80, "display_clocks": 0x100,
+    }
+
+    def __init__(self, index: int, period_s: float = 0.002):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        self.period = period_s
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # pragma: no cover - NVML unavailable
+            self.nv = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def summary(self) -> dict:
+        names = [k for k, bit in self.REASONS.items() if self.reasons & bit and k != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
+
+
+def measured_peak_hbm() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return FALLBACK_HBM_GBS, "fallback"
+
+
+def algorithmic_bytes(m: int, nnz: int, n: int, touched: int, esz: int = 4) -> int:
+    """A streamed once (row_ptr + int32 col + fp32 val), each
+    touched B row read once, C written once."""
+    return 4 * (m + 1) + 8 * nnz + esz * n * touched + esz * m * n
+
+
+def ncu_traffic(workload: str, point: str):
+    """dram read+write bytes per launch of the timed kernel from the committed
+    ncu --set full capture, when one exists for this exact workload."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None
+    try:
+        rec = json.loads(p.read_text())
+        for r in rec.get("entries", []):
+            if r.get("workload") == workload and r.get("point") == point:
+                return r.get("dram_bytes")
+    except Exception:
+        return None
+    return None
+
+
+# --------------------------------------------------------------------------- reference arm
+
+def run_reference(args, rank, world):
+    """The reference's CPU path on this host's cores: the oracle port of
+    dense_spmm_oracle (oracle/, C, bit-identical f64), on a bounded sample."""
+    if rank != 0:
+        return
+    import oracle
+    cfg = args.config
+    n = args.n or default_n(cfg)
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    g, desc, scaling = build_workload(cfg, world, args.seed, dev)
+    rp = g.row_ptr.cpu().numpy()
+    ci = g.col_idx.cpu().numpy().astype(np.int32)
+    vals = g.vals.cpu().numpy().astype(np.float32)
+    b = dense_b(g.num_cols, n, args.seed, dev).cpu().numpy()
+    threads = oracle.max_threads()
+    # bounded sample: leading rows holding ~sample_nnz nonzeros per step
+    sample_nnz = min(g.nnz, 4_000_000)
+    r_end = int(np.searchsorted(rp, sample_nnz, side="left"))
+    r_end = max(1, min(r_end, g.num_rows))
+    srp = rp[: r_end + 1].astype(np.int32)
+    s_nnz = int(srp[-1])
+    for _ in range(args.warmup):
+        oracle.spmm_f64(srp, ci[:s_nnz], vals[:s_nnz], b, n, threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.spmm_f64(srp, ci[:s_nnz], vals[:s_nnz], b, n, threads=threads)
+    dt = (time.perf_counter() - t0) / args.steps
+    value = 2.0 * s_nnz * n / dt / 1e9
+    sample = f"rows [0, {r_end}) of the workload: {s_nnz} nnz x N={n} per step"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": desc, "rows": g.num_rows, "nnz": g.nnz, "n": n},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- our arm
+
+def main():
+    args = parse_args()
+    rank, world, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    from paper_2209_02882_b200.device import DeviceCsr, prepare_aux, spmm
+    from paper_2209_02882_b200.partition import plan_shards, shard_csr
+    from paper_2209_02882_b200.selector import (Candidate, autotune, candidates, heuristic,
+                                                matrix_stats, plan_for)
+    import torch.distributed as dist
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    cfg = args.config
+    n = args.n or default_n(cfg)
+    g, desc, scaling = build_workload(cfg, world, args.seed, dev)
+    total_nnz = g.nnz
+    plan = plan_shards(g.row_ptr.cpu().numpy(), world)
+    rp, ci, vals = shard_csr(g.row_ptr, g.col_idx, g.vals, plan, rank)
+    lo, hi = plan.rows(rank)
+    a = DeviceCsr(hi - lo, g.num_cols, rp.to(torch.int32).contiguous(),
+                  ci.to(torch.int32).contiguous(), vals.to(torch.float32).contiguous())
+    touched = int(torch.unique(a.col_idx).numel()) if a.nnz else 0
+    rp_host = a.row_ptr.cpu().numpy().astype(np.int64)
+    b = dense_b(g.num_cols, n, args.seed, dev)
+    c = torch.empty((a.num_rows, n), dtype=torch.float32, device=dev)
+    del g
+    torch.cuda.empty_cache()
+    stream = torch.cuda.current_stream()
+    stats = matrix_stats(rp_host, a.num_cols)
+
+    # ---- schedule choice (untimed)
+    sweep_rows = []
+    if args.point:
+        choice = Candidate(args.point, args.p, args.hw_block)
+    else:
+        choice = None
+        if rank == 0:
+            ranked = autotune(a, b, c, n, candidates(n), reps=2, row_ptr_host=rp_host,
+                              stream=stream, max_ms=50.0)
+            sweep_rows = [{"point": cd.point, "p": cd.p, "ms": ms,
+                           "gflops": 2.0 * a.nnz * n / (ms * 1e6)} for cd, ms in ranked]
+            choice = ranked[0][0]
+        if world > 1:
+            obj = [choice]
+            dist.broadcast_object_list(obj, src=0)
+            choice = obj[0]
+    heur = heuristic(stats, n)
+    k = plan_for(choice, n, a.num_rows, a.num_cols, rp_host)
+    eb = k.family in ("nnz-one", "nnz-multiple")
+    aux = prepare_aux(k, a, stream=stream)
+
+    def step(ev=None):
+        if eb:
+            c.zero_()
+        if ev is not None:
+            ev.record(stream)
+        spmm(k, a, b, c, accumulate=eb, aux=aux, hw_block=choice.hw_block, stream=stream)
+
+    for _ in range(max(args.warmup, 3 if args.warmup >= 3 else args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        t_start.record(stream)
+        for i in range(args.steps):
+            step(mids[i])
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    total_ms = t_start.elapsed_time(ends[-1])
+    kernel_ms = statistics.mean(mids[i].elapsed_time(ends[i]) for i in range(args.steps))
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = 2.0 * total_nnz * n / (ms_per_step * 1e6)
+
+    # ---- roofline of the dominant kernel (this rank's shard)
+    peak, peak_kind = measured_peak_hbm()
+    abytes = algorithmic_bytes(a.num_rows, a.nnz, n, touched)
+    achieved = abytes / (kernel_ms * 1e-3) / 1e9
+    workload_key = f"cfg{cfg}:world{world}:n{n}"
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": ncu_traffic(workload_key, choice.point),
+            "peak_source": peak_kind, "algorithmic_bytes": abytes, "kernel_ms": kernel_ms,
+            "kernel_share": kernel_ms / ms_per_step}
+
+    # ---- end to end through host buffers
+    e2e = None
+    if not args.no_e2e:
+        h_rp = a.row_ptr.cpu().pin_memory()
+        h_ci = a.col_idx.cpu().pin_memory()
+        h_v = a.vals.cpu().pin_memory()
+        h_b = b.cpu().pin_memory()
+        h_c = torch.empty(c.shape, dtype=c.dtype).pin_memory()
+        d_rp, d_ci, d_v, d_b = (torch.empty_like(x) for x in (a.row_ptr, a.col_idx, a.vals, b))
+        ea = DeviceCsr(a.num_rows, a.num_cols, d_rp, d_ci, d_v)
+
+        def e2e_step():
+            d_rp.copy_(h_rp, non_blocking=True)
+            d_ci.copy_(h_ci, non_blocking=True)
+            d_v.copy_(h_v, non_blocking=True)
+            d_b.copy_(h_b, non_blocking=True)
+            e_aux = prepare_aux(k, ea, stream=stream)
+            spmm(k, ea, d_b, c, accumulate=False, aux=e_aux, hw_block=choice.hw_block, stream=stream)
+            h_c.copy_(c, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        e_steps = max(3, min(args.steps, 10))
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e_steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1) / e_steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        h2d = sum(x.numel() * x.element_size() for x in (h_rp, h_ci, h_v, h_b))
+        e2e = {"value": 2.0 * total_nnz * n / (float(te.item()) * 1e6), "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": h_c.numel() * h_c.element_size(),
+               "ms_per_step": float(te.item()), "steps": e_steps,
+               "path": "pinned host A,B -> H2D -> block starts + SpMM -> D2H C"}
+
+    # ---- CPU baseline (rank 0, single GPU only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        import oracle
+        threads = oracle.max_threads()
+        h_rp32 = rp_host.astype(np.int32)
+        h_ci32 = a.col_idx.cpu().numpy()
+        h_v32 = a.vals.cpu().numpy()
+        h_b32 = b.cpu().numpy()
+        sample_nnz = min(a.nnz, 4_000_000)
+        r_end = max(1, min(int(np.searchsorted(h_rp32, sample_nnz, side="left")), a.num_rows))
+        srp = h_rp32[: r_end + 1]
+        s_nnz = int(srp[-1])
+        oracle.spmm_f64(srp, h_ci32[:s_nnz], h_v32[:s_nnz], h_b32, n, threads=threads)
+        reps = 3
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            oracle.spmm_f64(srp, h_ci32[:s_nnz], h_v32[:s_nnz], h_b32, n, threads=threads)
+        dt = (time.perf_counter() - t0) / reps
+        cpu = {"value": 2.0 * s_nnz * n / dt / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"oracle (C fp64 port of dense_spmm_oracle) on rows [0, {r_end}): "
+                         f"{s_nnz} nnz x N={n}, {reps} reps"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {
+                "workload": desc, "rows": int(plan.starts[-1]), "nnz": total_nnz, "n": n,
+                "shard_rows": a.num_rows, "shard_nnz": a.nnz, "touched_b_rows": touched,
+                "schedule": choice.point, "p": choice.p, "family": k.family,
+                "heuristic_choice": heur.label(), "selector": "given" if args.point else "autotune",
+                "parallelism": f"row-shard{world}" if world > 1 else "single",
+                "l2": "inputs > L2 (A+B+C far above 126 MB): no flush needed",
+                "stats": stats.as_dict(),
+            },
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+        if args.sweep and sweep_rows:
+            Path(args.sweep).parent.mkdir(parents=True, exist_ok=True)
+            Path(args.sweep).write_text(json.dumps({"workload": desc, "n": n, "rows": sweep_rows,
+                                                    "heuristic": heur.label()}, indent=1))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

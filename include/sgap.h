@@ -17,6 +17,7 @@
  *                          + grid/block geometry)         lowering.py:218-243,649-696)
  *   sgap_block_starts     lowering.compute_block_starts  lowering.py:119-128
  *   sgap_run              sim.run                        sim.py:431-487
+ *   sgap_prepare_long_rows (engine-side numerics, no reference counterpart)
  *   sgap_seg_reduce_group sim.exec_seg_reduce_group      sim.py:139-165
  *   sgap_atomic_add_group sim.exec_atomic_add_group      sim.py:112-136
  *
@@ -91,7 +92,8 @@ typedef struct {
     int64_t grid_size;      /* == LoweredKernel.grid_size                    */
     int64_t block_size;     /* == LoweredKernel.block_size                   */
     int32_t has_block_starts; /* == (LoweredKernel.block_starts is not None) */
-    int32_t hw_block;       /* hardware CTA size chosen for sm_100a (0=auto) */
+    int32_t hw_block;       /* CTA size override: 0 = auto (256), else a warp
+                               multiple in [32, 256]                        */
 } sgap_kernel_t;
 
 /* CSR operand on the device (matrices.py:38-86 with int32 indices). */
@@ -123,19 +125,51 @@ int sgap_build_kernel(const sgap_point_t *point, int32_t n, int32_t p,
 int sgap_block_starts(const int32_t *d_row_ptr, int64_t num_rows, int64_t chunk,
                       int64_t num_blocks, int32_t *d_starts, void *stream);
 
+/* Per-matrix side data of a kernel (what the reference's LoweredKernel
+ * carries beyond its integers, plus the long-row table of this engine).  All
+ * device memory is owned by the caller.
+ *   d_block_starts: [grid_size + 1] from sgap_block_starts; required for the
+ *     nnz families (LoweredKernel.block_starts, lowering.py:683-696).
+ *   Long rows (float32 only, nnz families): rows with more than
+ *   long_threshold nonzeros receive so many separate atomic flushes that a
+ *   float32 running sum in C would exceed the 1e-5 accuracy bound; their
+ *   flushes go to a float64 table d_long_acc [long_capacity x n] that
+ *   sgap_run folds into C (and clears) after the kernel.  d_long_rows holds
+ *   the sorted ids of those rows and d_long_count their number, both filled
+ *   by sgap_prepare_long_rows.  long_threshold < 0 disables the table.       */
+typedef struct {
+    const int32_t *d_block_starts;
+    int32_t *d_long_rows;
+    int32_t *d_long_count;
+    double *d_long_acc;
+    int64_t long_capacity;
+    int64_t long_threshold;
+} sgap_aux_t;
+
+/* Threshold the engine uses for a kernel (-1: no table needed: row families
+ * keep float64 running sums, float64 values accumulate in float64).        */
+int64_t sgap_long_row_threshold(const sgap_kernel_t *kernel, int32_t dtype);
+/* Upper bound on the number of long rows (each holds > threshold nonzeros). */
+int64_t sgap_long_row_capacity(int64_t nnz, int64_t threshold);
+/* Scratch for the ordered compaction in sgap_prepare_long_rows. */
+size_t sgap_long_rows_tmp_bytes(int64_t num_rows);
+/* Fill aux->d_long_rows / d_long_count for aux->long_threshold and zero
+ * aux->d_long_acc (long_capacity x n). */
+int sgap_prepare_long_rows(const int32_t *d_row_ptr, int64_t num_rows, int32_t n,
+                           sgap_aux_t *aux, void *d_tmp, size_t tmp_bytes,
+                           void *stream);
+
 /* sim.run: C (+)= A @ B on the device.
  *   d_b: [a->num_cols x kernel->n] row-major, d_c: [a->num_rows x n] row-major.
  *   accumulate = 1: C += A@B (c0 already in d_c, sim.py:439-441);
  *   accumulate = 0: C = A@B (d_c is overwritten; zero-fill included).
- *   d_block_starts: [grid_size + 1] from sgap_block_starts; required when
- *   kernel->has_block_starts.
+ *   aux: side data (required for the nnz families; NULL allowed otherwise).
  *   d_writebacks: optional (NULL = off) device counter, incremented by the
  *   number of output writebacks (== SimMetrics.atomic_ops of the reference
  *   simulator for the same kernel; 0 for row-multiple).                      */
 int sgap_run(const sgap_kernel_t *kernel, const sgap_csr_t *a, const void *d_b,
-             void *d_c, int32_t dtype, int32_t accumulate,
-             const int32_t *d_block_starts, unsigned long long *d_writebacks,
-             void *stream);
+             void *d_c, int32_t dtype, int32_t accumulate, const sgap_aux_t *aux,
+             unsigned long long *d_writebacks, void *stream);
 
 /* The dense reference product that runner.verify_point checks against
  * (runner.py:193-194 -> matrices.dense_spmm_oracle, matrices.py:241-254),

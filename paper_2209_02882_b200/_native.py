@@ -41,6 +41,10 @@ EXPORTED = (
     "sgap_legality_rule",
     "sgap_build_kernel",
     "sgap_block_starts",
+    "sgap_long_row_threshold",
+    "sgap_long_row_capacity",
+    "sgap_long_rows_tmp_bytes",
+    "sgap_prepare_long_rows",
     "sgap_run",
     "sgap_reference_spmm_f64",
     "sgap_seg_reduce_group",
@@ -96,6 +100,17 @@ class Csr(ctypes.Structure):
     ]
 
 
+class Aux(ctypes.Structure):
+    _fields_ = [
+        ("d_block_starts", ctypes.c_void_p),
+        ("d_long_rows", ctypes.c_void_p),
+        ("d_long_count", ctypes.c_void_p),
+        ("d_long_acc", ctypes.c_void_p),
+        ("long_capacity", ctypes.c_int64),
+        ("long_threshold", ctypes.c_int64),
+    ]
+
+
 _lib = None
 
 
@@ -123,8 +138,16 @@ def lib():
     L.sgap_build_kernel.restype = ctypes.c_int
     L.sgap_block_starts.argtypes = [vp, i64, i64, i64, vp, vp]
     L.sgap_block_starts.restype = ctypes.c_int
+    L.sgap_long_row_threshold.argtypes = [ctypes.POINTER(Kernel), i32]
+    L.sgap_long_row_threshold.restype = i64
+    L.sgap_long_row_capacity.argtypes = [i64, i64]
+    L.sgap_long_row_capacity.restype = i64
+    L.sgap_long_rows_tmp_bytes.argtypes = [i64]
+    L.sgap_long_rows_tmp_bytes.restype = ctypes.c_size_t
+    L.sgap_prepare_long_rows.argtypes = [vp, i64, i32, ctypes.POINTER(Aux), vp, ctypes.c_size_t, vp]
+    L.sgap_prepare_long_rows.restype = ctypes.c_int
     L.sgap_run.argtypes = [ctypes.POINTER(Kernel), ctypes.POINTER(Csr), vp, vp, i32, i32,
-                           vp, vp, vp]
+                           ctypes.POINTER(Aux), vp, vp]
     L.sgap_run.restype = ctypes.c_int
     L.sgap_reference_spmm_f64.argtypes = [ctypes.POINTER(Csr), vp, i32, i32, vp, vp]
     L.sgap_reference_spmm_f64.restype = ctypes.c_int

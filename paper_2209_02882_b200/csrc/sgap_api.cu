@@ -5,7 +5,9 @@
 #include <cstdint>
 #include <cstring>
 
+#include <cub/device/device_select.cuh>
 #include <cuda_runtime.h>
+#include <thrust/iterator/counting_iterator.h>
 
 #include "../../include/sgap.h"
 #include "sgap_kernels.cuh"
@@ -90,7 +92,7 @@ int run_row_reciprocal(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, 
 
 template <typename T, int V, int R>
 int run_nnz_one_r(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
-                  const int *starts, unsigned long long *wb, cudaStream_t st) {
+                  const int *starts, const LongRows &lr, unsigned long long *wb, cudaStream_t st) {
     const int NT = k.n / V;
     const int TW = pow2_floor(NT < 32 / R ? NT : 32 / R);
     const int Q = 32 / TW;
@@ -99,62 +101,82 @@ int run_nnz_one_r(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
     const int blk = k.hw_block > 0 ? k.hw_block : kHwBlock;
     k_nnz_one<T, V, R><<<grid_for(items, blk), blk, 0, st>>>(
         a.d_row_ptr, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, starts,
-        (int)a.num_rows, k.n, a.nnz, k.chunk, k.grid_size, TW, wb);
+        (int)a.num_rows, k.n, a.nnz, k.chunk, k.grid_size, TW, lr, wb);
     return launch_status();
 }
 
 template <typename T, int V>
 int run_nnz_one(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
-                const int *starts, unsigned long long *wb, cudaStream_t st) {
+                const int *starts, const LongRows &lr, unsigned long long *wb, cudaStream_t st) {
     switch (k.r) {
-        case 1: return run_nnz_one_r<T, V, 1>(k, a, B, C, starts, wb, st);
-        case 2: return run_nnz_one_r<T, V, 2>(k, a, B, C, starts, wb, st);
-        case 4: return run_nnz_one_r<T, V, 4>(k, a, B, C, starts, wb, st);
-        case 8: return run_nnz_one_r<T, V, 8>(k, a, B, C, starts, wb, st);
-        case 16: return run_nnz_one_r<T, V, 16>(k, a, B, C, starts, wb, st);
-        case 32: return run_nnz_one_r<T, V, 32>(k, a, B, C, starts, wb, st);
+        case 1: return run_nnz_one_r<T, V, 1>(k, a, B, C, starts, lr, wb, st);
+        case 2: return run_nnz_one_r<T, V, 2>(k, a, B, C, starts, lr, wb, st);
+        case 4: return run_nnz_one_r<T, V, 4>(k, a, B, C, starts, lr, wb, st);
+        case 8: return run_nnz_one_r<T, V, 8>(k, a, B, C, starts, lr, wb, st);
+        case 16: return run_nnz_one_r<T, V, 16>(k, a, B, C, starts, lr, wb, st);
+        case 32: return run_nnz_one_r<T, V, 32>(k, a, B, C, starts, lr, wb, st);
         default: return SGAP_ERR_NO_TEMPLATE;
     }
 }
 
-template <typename T, int V>
-int run_nnz_multiple(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
-                     const int *starts, unsigned long long *wb, cudaStream_t st) {
-    const int NT = k.n / V;
-    const int TW = pow2_floor(NT);
-    const int SG = 32 / TW;
+template <typename T, int V, int W>
+int run_nnz_multiple_w(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
+                       const int *starts, const LongRows &lr, unsigned long long *wb,
+                       cudaStream_t st) {
     const long long chunks = k.grid_size * (k.chunk / k.g);
-    const long long items = ceil_div(chunks, SG);
+    const long long items = ceil_div(chunks, 32 / W);
     const int blk = k.hw_block > 0 ? k.hw_block : kHwBlock;
-    k_nnz_multiple<T, V><<<grid_for(items, blk), blk, 0, st>>>(
+    k_nnz_multiple<T, V, W><<<grid_for(items, blk), blk, 0, st>>>(
         a.d_row_ptr, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, starts,
-        (int)a.num_rows, k.n, a.nnz, k.g, k.chunk, k.grid_size, TW, wb);
+        (int)a.num_rows, k.n, a.nnz, k.g, k.chunk, k.grid_size, lr, wb);
     return launch_status();
 }
 
 template <typename T, int V>
+int run_nnz_multiple(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
+                     const int *starts, const LongRows &lr, unsigned long long *wb,
+                     cudaStream_t st) {
+    switch (pow2_floor(k.n / V)) {
+        case 1: return run_nnz_multiple_w<T, V, 1>(k, a, B, C, starts, lr, wb, st);
+        case 2: return run_nnz_multiple_w<T, V, 2>(k, a, B, C, starts, lr, wb, st);
+        case 4: return run_nnz_multiple_w<T, V, 4>(k, a, B, C, starts, lr, wb, st);
+        case 8: return run_nnz_multiple_w<T, V, 8>(k, a, B, C, starts, lr, wb, st);
+        case 16: return run_nnz_multiple_w<T, V, 16>(k, a, B, C, starts, lr, wb, st);
+        default: return run_nnz_multiple_w<T, V, 32>(k, a, B, C, starts, lr, wb, st);
+    }
+}
+
+template <typename T, int V>
 int run_family(const sgap_kernel_t &k, const sgap_csr_t &a, const void *b, void *c, int acc,
-               const int *starts, unsigned long long *wb, cudaStream_t st) {
+               const int *starts, const LongRows &lr, unsigned long long *wb, cudaStream_t st) {
     const T *B = static_cast<const T *>(b);
     T *C = static_cast<T *>(c);
     switch (k.family) {
         case SGAP_ROW_MULTIPLE: return run_row_multiple<T, V>(k, a, B, C, acc, st);
         case SGAP_ROW_RECIPROCAL: return run_row_reciprocal<T, V>(k, a, B, C, acc, wb, st);
-        case SGAP_NNZ_ONE: return run_nnz_one<T, V>(k, a, B, C, starts, wb, st);
-        case SGAP_NNZ_MULTIPLE: return run_nnz_multiple<T, V>(k, a, B, C, starts, wb, st);
+        case SGAP_NNZ_ONE: return run_nnz_one<T, V>(k, a, B, C, starts, lr, wb, st);
+        case SGAP_NNZ_MULTIPLE: return run_nnz_multiple<T, V>(k, a, B, C, starts, lr, wb, st);
         default: return SGAP_ERR_ARG;
     }
 }
 
 template <typename T>
 int run_typed(const sgap_kernel_t &k, const sgap_csr_t &a, const void *b, void *c, int acc,
-              const int *starts, unsigned long long *wb, cudaStream_t st) {
+              const int *starts, const LongRows &lr, unsigned long long *wb, cudaStream_t st) {
+    int status;
     switch (k.c) {
-        case 1: return run_family<T, 1>(k, a, b, c, acc, starts, wb, st);
-        case 2: return run_family<T, 2>(k, a, b, c, acc, starts, wb, st);
-        case 4: return run_family<T, 4>(k, a, b, c, acc, starts, wb, st);
+        case 1: status = run_family<T, 1>(k, a, b, c, acc, starts, lr, wb, st); break;
+        case 2: status = run_family<T, 2>(k, a, b, c, acc, starts, lr, wb, st); break;
+        case 4: status = run_family<T, 4>(k, a, b, c, acc, starts, lr, wb, st); break;
         default: return SGAP_ERR_NO_TEMPLATE;
     }
+    if (status != SGAP_OK || lr.threshold < 0) return status;
+    // fold the float64 side table of long rows into C (and clear it for the next call)
+    long long cap_cells = (long long)k.n * 65536;
+    unsigned blocks = (unsigned)ceil_div(cap_cells, kHwBlock);
+    if (blocks > 4096) blocks = 4096;
+    k_long_rows_fold<T><<<blocks, kHwBlock, 0, st>>>(static_cast<T *>(c), k.n, lr);
+    return launch_status();
 }
 
 template <typename T>
@@ -313,12 +335,63 @@ int sgap_block_starts(const int32_t *d_row_ptr, int64_t num_rows, int64_t chunk,
     return launch_status();
 }
 
+int64_t sgap_long_row_threshold(const sgap_kernel_t *k, int32_t dtype) {
+    if (k == nullptr || dtype != SGAP_F32) return -1;
+    long long unit;
+    if (k->family == SGAP_NNZ_MULTIPLE) unit = k->g;
+    else if (k->family == SGAP_NNZ_ONE) unit = k->r;
+    else return -1;  // row families own their rows: float64 running sums suffice
+    const long long t = 64 * unit;
+    return t < 128 ? 128 : t;
+}
+
+int64_t sgap_long_row_capacity(int64_t nnz, int64_t threshold) {
+    if (threshold < 0) return 0;
+    return nnz / (threshold + 1) + 1;
+}
+
+size_t sgap_long_rows_tmp_bytes(int64_t num_rows) {
+    size_t bytes = 0;
+    LongRowPred pred{nullptr, 0};
+    cub::DeviceSelect::If(nullptr, bytes, thrust::counting_iterator<int>(0), (int *)nullptr,
+                          (int *)nullptr, (int)(num_rows > 0 ? num_rows : 1), pred);
+    return bytes;
+}
+
+int sgap_prepare_long_rows(const int32_t *d_row_ptr, int64_t num_rows, int32_t n,
+                           sgap_aux_t *aux, void *d_tmp, size_t tmp_bytes, void *stream) {
+    if (aux == nullptr || d_row_ptr == nullptr || n < 1) return SGAP_ERR_ARG;
+    if (aux->long_threshold < 0) return SGAP_OK;
+    if (aux->d_long_rows == nullptr || aux->d_long_count == nullptr || aux->d_long_acc == nullptr)
+        return SGAP_ERR_ARG;
+    if (num_rows > INT_MAX - 1) return SGAP_ERR_SHAPE;
+    cudaStream_t st = as_stream(stream);
+    if (num_rows == 0) {
+        return cudaMemsetAsync(aux->d_long_count, 0, sizeof(int32_t), st) == cudaSuccess
+                   ? SGAP_OK : SGAP_ERR_CUDA;
+    }
+    size_t need = sgap_long_rows_tmp_bytes(num_rows);
+    if (d_tmp == nullptr || tmp_bytes < need) return SGAP_ERR_ARG;
+    LongRowPred pred{d_row_ptr, aux->long_threshold};
+    if (cub::DeviceSelect::If(d_tmp, tmp_bytes, thrust::counting_iterator<int>(0),
+                              aux->d_long_rows, aux->d_long_count, (int)num_rows, pred, st) !=
+        cudaSuccess)
+        return SGAP_ERR_CUDA;
+    const size_t acc_bytes = (size_t)aux->long_capacity * (size_t)n * sizeof(double);
+    if (acc_bytes && cudaMemsetAsync(aux->d_long_acc, 0, acc_bytes, st) != cudaSuccess)
+        return SGAP_ERR_CUDA;
+    return launch_status();
+}
+
 int sgap_run(const sgap_kernel_t *k, const sgap_csr_t *a, const void *d_b, void *d_c,
-             int32_t dtype, int32_t accumulate, const int32_t *d_block_starts,
+             int32_t dtype, int32_t accumulate, const sgap_aux_t *aux,
              unsigned long long *d_writebacks, void *stream) {
     if (k == nullptr || a == nullptr) return SGAP_ERR_ARG;
     if (dtype != SGAP_F32 && dtype != SGAP_F64) return SGAP_ERR_PRECISION;
     if (k->n < 1 || k->c < 1 || k->n % k->c) return SGAP_ERR_CONFIG;
+    // kernels are compiled with __launch_bounds__(256)
+    if (k->hw_block != 0 && (k->hw_block < 32 || k->hw_block > 256 || k->hw_block % 32))
+        return SGAP_ERR_ARG;
     if (a->num_rows < 0 || a->num_cols < 0 || a->nnz < 0) return SGAP_ERR_SHAPE;
     if (a->num_rows > INT_MAX - 1 || a->nnz > INT_MAX) return SGAP_ERR_SHAPE;
     const size_t esz = dtype == SGAP_F32 ? 4 : 8;
@@ -331,8 +404,15 @@ int sgap_run(const sgap_kernel_t *k, const sgap_csr_t *a, const void *d_b, void 
     const size_t vec_bytes = esz * (size_t)(k->c == 4 && esz == 8 ? 2 : k->c);
     if ((d_b && !aligned(d_b, vec_bytes)) || !aligned(d_c, vec_bytes)) return SGAP_ERR_ARG;
     const bool eb = k->family == SGAP_NNZ_ONE || k->family == SGAP_NNZ_MULTIPLE;
-    if (eb && k->grid_size > 0 && d_block_starts == nullptr) return SGAP_ERR_ARG;
+    const int32_t *starts = aux ? aux->d_block_starts : nullptr;
+    if (eb && k->grid_size > 0 && starts == nullptr) return SGAP_ERR_ARG;
     if (k->family == SGAP_NNZ_MULTIPLE && (k->g < 1 || k->chunk % k->g)) return SGAP_ERR_CONFIG;
+    LongRows lr{nullptr, nullptr, nullptr, -1};
+    if (eb && aux && aux->long_threshold >= 0 && dtype == SGAP_F32) {
+        if (aux->d_long_rows == nullptr || aux->d_long_count == nullptr || aux->d_long_acc == nullptr)
+            return SGAP_ERR_ARG;
+        lr = LongRows{aux->d_long_rows, aux->d_long_count, aux->d_long_acc, aux->long_threshold};
+    }
     if (eb && !accumulate) {
         // atomic-writeback families accumulate into C: zero-fill (counts as
         // part of the SpMM).
@@ -341,8 +421,8 @@ int sgap_run(const sgap_kernel_t *k, const sgap_csr_t *a, const void *d_b, void 
     }
     if (eb && k->grid_size == 0) return SGAP_OK;
     if (dtype == SGAP_F32)
-        return run_typed<float>(*k, *a, d_b, d_c, accumulate, d_block_starts, d_writebacks, st);
-    return run_typed<double>(*k, *a, d_b, d_c, accumulate, d_block_starts, d_writebacks, st);
+        return run_typed<float>(*k, *a, d_b, d_c, accumulate, starts, lr, d_writebacks, st);
+    return run_typed<double>(*k, *a, d_b, d_c, accumulate, starts, lr, d_writebacks, st);
 }
 
 int sgap_reference_spmm_f64(const sgap_csr_t *a, const void *d_b, int32_t n, int32_t dtype,

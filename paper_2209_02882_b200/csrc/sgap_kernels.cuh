@@ -32,7 +32,8 @@ constexpr int kBatch = 4;  // independent gathers kept in flight per lane
 // (cuda_row_multiple.cu:37-43).  Hardware: L = N/c lanes per row group; when
 // L divides 32 (or is a multiple of 32) the lanes sharing a row stage that
 // row's (col, val) pairs with one coalesced load and shuffle them, which also
-// lets kBatch B-row gathers issue back to back.
+// lets kBatch B-row gathers issue back to back.  Partial sums of each staged
+// round (<= 32 terms) fold into a float64 running sum.
 // ===========================================================================
 template <typename T, int V>
 __global__ void __launch_bounds__(256)
@@ -58,10 +59,13 @@ k_row_multiple(const int *__restrict__ rp, const int *__restrict__ ci,
             Vec<T, V> acc[kBatch];
 #pragma unroll
             for (int u = 0; u < kBatch; ++u) acc[u].zero();
+            Vec<double, V> tot;
+            tot.zero();
             if (S > 0) {
                 // Staged: S lanes (aligned) share the row; warp-uniform trip count.
                 const int maxlen = __reduce_max_sync(kFull, len);
                 const int sl = (int)(lane & (unsigned)(S - 1));
+                const int round = S < 32 ? 32 : S;  // positions per fold
                 for (int base = 0; base < maxlen; base += S) {
                     int my_c = 0;
                     T my_v = T(0);
@@ -91,35 +95,44 @@ k_row_multiple(const int *__restrict__ rp, const int *__restrict__ ci,
 #pragma unroll
                         for (int u = 0; u < kBatch; ++u) fma_vec<T, V>(acc[u], vv[u], bv[u]);
                     }
+                    if ((base + S) % round == 0 || base + S >= maxlen) {
+#pragma unroll
+                        for (int u = 0; u < kBatch; ++u) fold<T, V>(tot, acc[u]);
+                    }
                 }
             } else {
                 // Direct: row lanes straddle warps; each lane walks the row.
-                int p = beg;
                 const int end = beg + len;
-                for (; p + kBatch <= end; p += kBatch) {
-                    int cc[kBatch];
-                    T vv[kBatch];
-                    Vec<T, V> bv[kBatch];
+                for (int p0 = beg; p0 < end; p0 += 32) {
+                    const int e = min(p0 + 32, end);
+                    int p = p0;
+                    for (; p + kBatch <= e; p += kBatch) {
+                        int cc[kBatch];
+                        T vv[kBatch];
+                        Vec<T, V> bv[kBatch];
 #pragma unroll
-                    for (int u = 0; u < kBatch; ++u) {
-                        cc[u] = __ldg(ci + p + u);
-                        vv[u] = __ldg(av + p + u);
+                        for (int u = 0; u < kBatch; ++u) {
+                            cc[u] = __ldg(ci + p + u);
+                            vv[u] = __ldg(av + p + u);
+                        }
+#pragma unroll
+                        for (int u = 0; u < kBatch; ++u)
+                            ldg_vec<T, V>(bv[u], B + (long long)cc[u] * N + kcol);
+#pragma unroll
+                        for (int u = 0; u < kBatch; ++u) fma_vec<T, V>(acc[u], vv[u], bv[u]);
+                    }
+                    for (; p < e; ++p) {
+                        Vec<T, V> bv;
+                        ldg_vec<T, V>(bv, B + (long long)__ldg(ci + p) * N + kcol);
+                        fma_vec<T, V>(acc[0], __ldg(av + p), bv);
                     }
 #pragma unroll
-                    for (int u = 0; u < kBatch; ++u)
-                        ldg_vec<T, V>(bv[u], B + (long long)cc[u] * N + kcol);
-#pragma unroll
-                    for (int u = 0; u < kBatch; ++u) fma_vec<T, V>(acc[u], vv[u], bv[u]);
-                }
-                for (; p < end; ++p) {
-                    Vec<T, V> bv;
-                    ldg_vec<T, V>(bv, B + (long long)__ldg(ci + p) * N + kcol);
-                    fma_vec<T, V>(acc[0], __ldg(av + p), bv);
+                    for (int u = 0; u < kBatch; ++u) fold<T, V>(tot, acc[u]);
                 }
             }
 #pragma unroll
-            for (int u = 1; u < kBatch; ++u) add_vec<T, V>(acc[0], acc[u]);
-            if (row_ok) store_vec<T, V>(C + i * N + kcol, acc[0], accumulate != 0);
+            for (int u = 0; u < kBatch; ++u) fold<T, V>(tot, acc[u]);
+            if (row_ok) store_vec<T, V>(C + i * N + kcol, narrow<T, V>(tot), accumulate != 0);
         }
     }
 }
@@ -130,6 +143,7 @@ k_row_multiple(const int *__restrict__ rp, const int *__restrict__ ci,
 // columns); lane j accumulates positions begin+j, begin+j+G, ...
 // (cuda_row_reciprocal.cu:39-46), then the AtomicAddGroup becomes an
 // xor-shuffle tree and a single exclusive store by the group's lane 0.
+// Each lane folds its partial into float64 every 32 strided terms.
 // ===========================================================================
 template <typename T, int V, int G>
 __global__ void __launch_bounds__(256)
@@ -155,31 +169,37 @@ k_row_reciprocal(const int *__restrict__ rp, const int *__restrict__ ci,
         Vec<T, V> acc[kBatch];
 #pragma unroll
         for (int u = 0; u < kBatch; ++u) acc[u].zero();
-        int p = beg + j;
-        for (; p + (kBatch - 1) * G < end; p += kBatch * G) {
-            int cc[kBatch];
-            T vv[kBatch];
-            Vec<T, V> bv[kBatch];
+        Vec<double, V> tot;
+        tot.zero();
+        for (int seg = beg + j; seg < end; seg += 32 * G) {
+            const int seg_end = min(seg + 32 * G, end);
+            int p = seg;
+            for (; p + (kBatch - 1) * G < seg_end; p += kBatch * G) {
+                int cc[kBatch];
+                T vv[kBatch];
+                Vec<T, V> bv[kBatch];
 #pragma unroll
-            for (int u = 0; u < kBatch; ++u) {
-                cc[u] = __ldg(ci + p + u * G);
-                vv[u] = __ldg(av + p + u * G);
+                for (int u = 0; u < kBatch; ++u) {
+                    cc[u] = __ldg(ci + p + u * G);
+                    vv[u] = __ldg(av + p + u * G);
+                }
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) ldg_vec<T, V>(bv[u], B + (long long)cc[u] * N + k0);
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) fma_vec<T, V>(acc[u], vv[u], bv[u]);
+            }
+            for (; p < seg_end; p += G) {
+                Vec<T, V> bv;
+                ldg_vec<T, V>(bv, B + (long long)__ldg(ci + p) * N + k0);
+                fma_vec<T, V>(acc[0], __ldg(av + p), bv);
             }
 #pragma unroll
-            for (int u = 0; u < kBatch; ++u) ldg_vec<T, V>(bv[u], B + (long long)cc[u] * N + k0);
-#pragma unroll
-            for (int u = 0; u < kBatch; ++u) fma_vec<T, V>(acc[u], vv[u], bv[u]);
+            for (int u = 0; u < kBatch; ++u) fold<T, V>(tot, acc[u]);
         }
-        for (; p < end; p += G) {
-            Vec<T, V> bv;
-            ldg_vec<T, V>(bv, B + (long long)__ldg(ci + p) * N + k0);
-            fma_vec<T, V>(acc[0], __ldg(av + p), bv);
-        }
-#pragma unroll
-        for (int u = 1; u < kBatch; ++u) add_vec<T, V>(acc[0], acc[u]);
-        group_sum_vec<G, T, V>(acc[0]);
+        Vec<T, V> part = narrow<T, V>(tot);
+        group_sum_vec<G, T, V>(part);
         if (ok && j == 0) {
-            store_vec<T, V>(C + i * N + k0, acc[0], accumulate != 0);
+            store_vec<T, V>(C + i * N + k0, part, accumulate != 0);
             nwb += V;
         }
     }
@@ -202,7 +222,7 @@ __global__ void __launch_bounds__(256)
 k_nnz_one(const int *__restrict__ rp, const int *__restrict__ ci, const T *__restrict__ av,
           const T *__restrict__ B, T *__restrict__ C, const int *__restrict__ starts,
           int M, int N, long long nnz, long long npb, long long grid, int TW,
-          unsigned long long *wb) {
+          LongRows lr, unsigned long long *wb) {
     const int NT = N / V;
     const int Q = 32 / TW;
     const long long total_pos = grid * npb;
@@ -222,29 +242,31 @@ k_nnz_one(const int *__restrict__ rp, const int *__restrict__ ci, const T *__res
         SegLanes sl{};
         if constexpr (R > 1) sl = seg_lanes<R, int>(row, in_grid);
         const T *brow = B + (long long)col * N;
-        T *crow = C + (long long)row * N;
         for (int tt = 0; tt < NT; tt += TW) {
             const int tile = tt + tl;
             const bool tok = tile < NT;
+            const long long kcol = (long long)tile * V;
             Vec<T, V> prod;
             prod.zero();
             if (in_nnz && tok) {
                 Vec<T, V> bv;
-                ldg_vec<T, V>(bv, brow + (long long)tile * V);
+                ldg_vec<T, V>(bv, brow + kcol);
 #pragma unroll
                 for (int x = 0; x < V; ++x) prod.v[x] = a * bv.v[x];
             }
+            bool writer;
             if constexpr (R == 1) {
-                if (in_nnz && tok) {
-                    red_vec<T, V>(crow + (long long)tile * V, prod);
-                    nwb += V;
-                }
+                writer = in_nnz && tok;
             } else {
                 seg_scan_vec<R, T, V>(prod, sl.dist);
-                if (sl.tail && tok) {
-                    red_vec<T, V>(crow + (long long)tile * V, prod);
-                    nwb += V;
-                }
+                writer = sl.tail && tok;
+            }
+            if (writer) {
+                Vec<double, V> tot;
+#pragma unroll
+                for (int x = 0; x < V; ++x) tot.v[x] = (double)prod.v[x];
+                flush_tile<T, V>(C, N, row, kcol, tot, rp, lr);
+                nwb += V;
             }
         }
     }
@@ -254,26 +276,29 @@ k_nnz_one(const int *__restrict__ rp, const int *__restrict__ ci, const T *__res
 // ===========================================================================
 // EB + serial reduction: nnz:g,col:c,r:1 (nnz-multiple, the TACO nnz split).
 // Logical work = one aligned chunk of g positions x one column; the walk
-// tracks its row with the block-window search plus forward advance, flushing
-// an atomic at every row change and once at the end -- also for chunks past
-// nnz (cuda_nnz_multiple.cu:33-53).  Hardware: TW lanes x c columns per chunk,
-// 32/TW chunks per warp; kBatch positions' (col, val) and B rows are fetched
-// before the serial flush logic consumes them.
+// tracks its row (block-window search, then forward advance) and flushes an
+// atomic at every row change plus once at the end -- also for chunks past nnz
+// (cuda_nnz_multiple.cu:33-53).
+// Hardware: W lanes (c columns each) share a chunk, 32/W chunks per warp.
+// The lanes of a chunk read each position's (col, val) as a broadcast load,
+// kBatch B-row gathers go out back to back before the serial flush logic
+// consumes them, and the chunk's next row start is kept in a register so the
+// walk only touches row_ptr at a row change.
 // ===========================================================================
-template <typename T, int V>
+template <typename T, int V, int W>
 __global__ void __launch_bounds__(256)
 k_nnz_multiple(const int *__restrict__ rp, const int *__restrict__ ci,
                const T *__restrict__ av, const T *__restrict__ B, T *__restrict__ C,
                const int *__restrict__ starts, int M, int N, long long nnz, int g,
-               long long chunk, long long grid, int TW, unsigned long long *wb) {
+               long long chunk, long long grid, LongRows lr, unsigned long long *wb) {
     const int NT = N / V;
-    const int SG = 32 / TW;
+    constexpr int SG = 32 / W;
     const long long cpb = chunk / g;
     const long long total_chunks = grid * cpb;
     const long long items = (total_chunks + SG - 1) / SG;
     const unsigned lane = lane_id();
-    const int sg = (int)(lane / (unsigned)TW);
-    const int tl = (int)(lane & (unsigned)(TW - 1));
+    const int sg = (int)(lane / (unsigned)W);
+    const int sl = (int)(lane & (unsigned)(W - 1));
     unsigned long long nwb = 0;
     SGAP_WARP_LOOP(item, items) {
         const long long ch = item * SG + sg;
@@ -283,14 +308,16 @@ k_nnz_multiple(const int *__restrict__ rp, const int *__restrict__ ci,
         int hi = __ldg(starts + ch / cpb + 1) + 1;
         hi = hi < M ? hi : M;
         const int row0 = search_before(rp, __ldg(starts + ch / cpb), hi, base);
-        for (int tile = tl; tile < NT; tile += TW) {
+        for (int tile = sl; tile < NT; tile += W) {
             const long long kcol = (long long)tile * V;
             int row = row0;
             long long nb = __ldg(rp + row + 1);
             Vec<T, V> acc;
             acc.zero();
-            long long pos = base;
-            for (; pos < end; pos += kBatch) {
+            Vec<double, V> tot;
+            tot.zero();
+            int since_fold = 0;
+            for (long long pos = base; pos < end; pos += kBatch) {
                 int cc[kBatch];
                 T vv[kBatch];
                 Vec<T, V> bv[kBatch];
@@ -309,9 +336,11 @@ k_nnz_multiple(const int *__restrict__ rp, const int *__restrict__ ci,
                 for (int u = 0; u < kBatch; ++u) {
                     if (pos + u < end) {
                         if (pos + u == nb) {
-                            red_vec<T, V>(C + (long long)row * N + kcol, acc);
+                            fold<T, V>(tot, acc);
+                            flush_tile<T, V>(C, N, row, kcol, tot, rp, lr);
                             nwb += V;
-                            acc.zero();
+                            tot.zero();
+                            since_fold = 0;
                             do {
                                 ++row;
                                 nb = __ldg(rp + row + 1);
@@ -320,13 +349,42 @@ k_nnz_multiple(const int *__restrict__ rp, const int *__restrict__ ci,
                         fma_vec<T, V>(acc, vv[u], bv[u]);
                     }
                 }
+                since_fold += kBatch;
+                if (since_fold >= 32) {
+                    fold<T, V>(tot, acc);
+                    since_fold = 0;
+                }
             }
-            red_vec<T, V>(C + (long long)row * N + kcol, acc);
+            fold<T, V>(tot, acc);
+            flush_tile<T, V>(C, N, row, kcol, tot, rp, lr);
             nwb += V;
         }
     }
     flush_count(wb, nwb);
 }
+
+// Adds the float64 side table of long rows into C (after the SpMM kernel).
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_long_rows_fold(T *__restrict__ C, int N, LongRows lr) {
+    const long long total = (long long)(*lr.count) * N;
+    for (long long h = (long long)blockIdx.x * blockDim.x + threadIdx.x; h < total;
+         h += (long long)gridDim.x * blockDim.x) {
+        const long long slot = h / N;
+        const long long k = h - slot * N;
+        const long long off = (long long)__ldg(lr.rows + slot) * N + k;
+        C[off] = (T)((double)C[off] + lr.acc[h]);
+    }
+}
+
+// Marks rows longer than `threshold` (input to the ordered compaction).
+struct LongRowPred {
+    const int *rp;
+    long long threshold;
+    __host__ __device__ __forceinline__ bool operator()(const int &r) const {
+        return (long long)(rp[r + 1] - rp[r]) > threshold;
+    }
+};
 
 // The verification product of runner.verify_point (runner.py:193-194): the
 // dense reference C = A@B in float64, per (i,k) ascending-p order with the

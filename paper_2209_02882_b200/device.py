@@ -20,8 +20,8 @@ import torch
 from . import _native
 from .lowering import LoweredKernel
 
-__all__ = ["DeviceCsr", "kernel_struct", "device_block_starts", "spmm", "reference_spmm_f64",
-           "torch_dtype", "native_dtype", "require_cuda"]
+__all__ = ["DeviceCsr", "KernelAux", "kernel_struct", "device_block_starts", "prepare_aux", "spmm",
+           "reference_spmm_f64", "torch_dtype", "native_dtype", "require_cuda"]
 
 _INT32_MAX = 2**31 - 1
 
@@ -129,14 +129,68 @@ def device_block_starts(a: DeviceCsr, chunk: int, num_blocks: int, *, stream=Non
     return out
 
 
+@dataclass
+class KernelAux:
+    """Per-(kernel, matrix) device side data: the block-start table
+    (LoweredKernel.block_starts) and the float64 long-row table.  Built once
+    by ``prepare_aux`` and reused across calls on the same matrix."""
+
+    starts: torch.Tensor | None
+    long_rows: torch.Tensor | None = None
+    long_count: torch.Tensor | None = None
+    long_acc: torch.Tensor | None = None
+    long_capacity: int = 0
+    long_threshold: int = -1
+
+    def view(self) -> _native.Aux:
+        ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+        return _native.Aux(ptr(self.starts), ptr(self.long_rows), ptr(self.long_count),
+                           ptr(self.long_acc), self.long_capacity, self.long_threshold)
+
+    def nbytes(self) -> int:
+        ts = (self.starts, self.long_rows, self.long_count, self.long_acc)
+        return sum(t.numel() * t.element_size() for t in ts if t is not None)
+
+
+def prepare_aux(k: LoweredKernel, a: DeviceCsr, *, stream=None, long_rows: bool = True) -> KernelAux:
+    """Block starts (nnz families) and, for float32 values, the long-row
+    table (include/sgap.h, sgap_prepare_long_rows)."""
+    starts = None
+    if k.family in ("nnz-one", "nnz-multiple") and k.grid_size > 0:
+        starts = device_block_starts(a, k.chunk, k.grid_size, stream=stream)
+    aux = KernelAux(starts)
+    if not long_rows:
+        return aux
+    L = _native.lib()
+    ks = kernel_struct(k)
+    thr = int(L.sgap_long_row_threshold(ctypes.byref(ks), native_dtype(a.vals.dtype)))
+    if thr < 0:
+        return aux
+    cap = int(L.sgap_long_row_capacity(a.nnz, thr))
+    dev = a.device
+    aux.long_threshold = thr
+    aux.long_capacity = cap
+    aux.long_rows = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+    aux.long_count = torch.zeros(1, dtype=torch.int32, device=dev)
+    aux.long_acc = torch.empty(max(cap, 1) * k.n, dtype=torch.float64, device=dev)
+    tmp_bytes = int(L.sgap_long_rows_tmp_bytes(a.num_rows))
+    tmp = torch.empty(max(tmp_bytes, 1), dtype=torch.uint8, device=dev)
+    v = aux.view()
+    _native.check(L.sgap_prepare_long_rows(a.row_ptr.data_ptr(), a.num_rows, k.n, ctypes.byref(v),
+                                           tmp.data_ptr(), tmp_bytes, _stream_handle(stream)),
+                  "sgap_prepare_long_rows")
+    return aux
+
+
 def spmm(k: LoweredKernel, a: DeviceCsr, b: torch.Tensor, c: torch.Tensor, *,
-         accumulate: bool = False, starts: torch.Tensor | None = None,
+         accumulate: bool = False, aux: KernelAux | None = None,
          writebacks: torch.Tensor | None = None, hw_block: int = 0, stream=None) -> None:
     """C (+)= A @ B with kernel ``k``, stream-ordered, no host synchronisation.
 
     ``b``: [num_cols, n] and ``c``: [num_rows, n] contiguous tensors of the
-    value dtype of ``a``; ``starts`` from ``device_block_starts`` (computed
-    here when omitted); ``writebacks``: optional int64[1] counter.
+    value dtype of ``a``; ``aux`` from ``prepare_aux`` (built here when
+    omitted -- pass it in to keep the call launch-only); ``writebacks``:
+    optional int64[1] counter.
     """
     if b.dtype != a.vals.dtype or c.dtype != a.vals.dtype:
         raise ValueError("A, B and C must share one value dtype")
@@ -145,14 +199,14 @@ def spmm(k: LoweredKernel, a: DeviceCsr, b: torch.Tensor, c: torch.Tensor, *,
             f"shape mismatch: A is {a.num_rows}x{a.num_cols}, B {tuple(b.shape)}, C {tuple(c.shape)}, n={k.n}")
     if not (b.is_contiguous() and c.is_contiguous()):
         raise ValueError("B and C must be contiguous row-major")
-    if k.family in ("nnz-one", "nnz-multiple") and starts is None and k.grid_size > 0:
-        starts = device_block_starts(a, k.chunk, k.grid_size, stream=stream)
+    if aux is None:
+        aux = prepare_aux(k, a, stream=stream)
     ks = kernel_struct(k, hw_block=hw_block)
     view = a.view()
+    av = aux.view()
     st = _native.lib().sgap_run(
         ctypes.byref(ks), ctypes.byref(view), b.data_ptr(), c.data_ptr(),
-        native_dtype(a.vals.dtype), 1 if accumulate else 0,
-        starts.data_ptr() if starts is not None else None,
+        native_dtype(a.vals.dtype), 1 if accumulate else 0, ctypes.byref(av),
         writebacks.data_ptr() if writebacks is not None else None, _stream_handle(stream))
     _native.check(st, "sgap_run")
 

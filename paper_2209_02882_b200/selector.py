@@ -1,0 +1,153 @@
+"""Schedule selection: pick (split, reduction strategy, r, c, p, CTA size).
+
+The reference only enumerates the space (space.py:232-348) and leaves
+DA-SpMM's decision tree out of scope; SURVEY 8(a) a20 asks
+for a selector driven by nnz/row statistics and N, validated as regret
+against an exhaustive sweep.  Two layers:
+
+* ``heuristic(stats, n)`` -- a closed-form rule over the row-length
+  statistics (no device work);
+* ``autotune(...)`` -- measures candidate kernels on the device operands and
+  returns them ranked (the exhaustive sweep when given every candidate).
+
+``tests/test_selector.py`` and ``bench.py --sweep`` report the heuristic's
+regret against the sweep.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .device import DeviceCsr, prepare_aux, spmm
+from .lowering import KernelConfig, LoweredKernel, lower
+from .space import enumerate_space, parse_point
+from .templates import algorithm_template
+
+__all__ = ["MatrixStats", "matrix_stats", "Candidate", "candidates", "heuristic", "autotune",
+           "plan_for"]
+
+
+@dataclass(frozen=True)
+class MatrixStats:
+    num_rows: int
+    num_cols: int
+    nnz: int
+    mean_row: float
+    cv_row: float
+    max_row: int
+    empty_frac: float
+
+    def as_dict(self) -> dict:
+        return dict(self.__dict__)
+
+
+def matrix_stats(row_ptr, num_cols: int) -> MatrixStats:
+    rp = np.asarray(row_ptr.cpu() if isinstance(row_ptr, torch.Tensor) else row_ptr, dtype=np.int64)
+    lens = np.diff(rp)
+    m = lens.shape[0]
+    mean = float(lens.mean()) if m else 0.0
+    cv = float(lens.std() / mean) if mean > 0 else 0.0
+    return MatrixStats(m, int(num_cols), int(rp[-1]), mean, cv, int(lens.max()) if m else 0,
+                       float((lens == 0).mean()) if m else 0.0)
+
+
+@dataclass(frozen=True)
+class Candidate:
+    point: str
+    p: int
+    hw_block: int = 0
+
+    def label(self) -> str:
+        return f"{self.point}@p{self.p}" + (f"/b{self.hw_block}" if self.hw_block else "")
+
+
+class _RowPtrOnly:
+    """Minimal matrix view for host planning (row_ptr + dims)."""
+
+    def __init__(self, num_rows, num_cols, row_ptr):
+        self.num_rows, self.num_cols, self.row_ptr = num_rows, num_cols, row_ptr
+
+
+def plan_for(cand: Candidate, n: int, num_rows: int, num_cols: int, row_ptr_host) -> LoweredKernel | None:
+    tpl = algorithm_template(parse_point(cand.point), KernelConfig(n=n, p=cand.p))
+    if tpl is None:
+        return None
+    return lower(tpl, _RowPtrOnly(num_rows, num_cols, row_ptr_host), compute_starts=False)
+
+
+def candidates(n: int, p_values=(256, 1024)) -> list[Candidate]:
+    """Every templated point at dense width n for each p (deduplicated by
+    the kernel it lowers to)."""
+    out, seen = [], set()
+    for p in p_values:
+        cfg = KernelConfig(n=n, p=p)
+        for pt in enumerate_space().legal:
+            tpl = algorithm_template(pt, cfg)
+            if tpl is None:
+                continue
+            key = (tpl.family, tpl.g, tpl.c, tpl.r, tpl.chunk)
+            if key in seen:
+                continue
+            seen.add(key)
+            out.append(Candidate(str(pt), p))
+    return out
+
+
+def heuristic(stats: MatrixStats, n: int) -> Candidate:
+    """Closed-form choice from row statistics and n.
+
+    * c = widest vector dividing n (16-byte B-row gathers when n % 4 == 0);
+    * short, regular rows (cv < 1, max row <= 8 * mean): row split, one row
+      per lane group (RB + serial, no atomics, no zero-fill);
+    * skewed rows (power-law, hub rows): nnz split with a serial walk over
+      g = 32 positions (EB + serial: load balanced, atomics only at chunk
+      boundaries);
+    * very narrow n (< 8) with skew: segment groups of r = 8 over single
+      nonzeros (the Sgap schedule the paper recommends for small N).
+    """
+    c = 4 if n % 4 == 0 else (2 if n % 2 == 0 else 1)
+    regular = stats.cv_row < 1.0 and stats.max_row <= 8 * max(stats.mean_row, 1.0)
+    if regular:
+        return Candidate(f"row:1,col:{c},r:1" if c > 1 else "row:1,col:1,r:1", 256)
+    if n < 8:
+        for r in (8, 4, 2):
+            pt = f"nnz:1,col:{c},r:{r}" if c > 1 else f"nnz:1,col:1,r:{r}"
+            if algorithm_template(parse_point(pt), KernelConfig(n=n, p=256)) is not None:
+                return Candidate(pt, 256)
+    for p in (256, 1024):
+        pt = f"nnz:32,col:{c},r:1" if c > 1 else "nnz:32,col:1,r:1"
+        if algorithm_template(parse_point(pt), KernelConfig(n=n, p=p)) is not None:
+            return Candidate(pt, p)
+    return Candidate(f"row:1,col:{c},r:1" if c > 1 else "row:1,col:1,r:1", 256)
+
+
+def autotune(a: DeviceCsr, b: torch.Tensor, c: torch.Tensor, n: int, cands, *, reps: int = 3,
+             row_ptr_host=None, stream=None, max_ms: float | None = None) -> list[tuple[Candidate, float]]:
+    """Time each candidate (zero-fill included for atomic families); returns
+    [(candidate, best ms)] fastest first.  Candidates slower than ``max_ms``
+    on their first run are not repeated."""
+    rp = row_ptr_host if row_ptr_host is not None else a.row_ptr.cpu().numpy()
+    stream = stream or torch.cuda.current_stream()
+    results = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for cand in cands:
+        k = plan_for(cand, n, a.num_rows, a.num_cols, rp)
+        if k is None:
+            continue
+        aux = prepare_aux(k, a, stream=stream)
+        spmm(k, a, b, c, aux=aux, hw_block=cand.hw_block, stream=stream)  # warm
+        best = float("inf")
+        for i in range(reps):
+            e0.record(stream)
+            spmm(k, a, b, c, aux=aux, hw_block=cand.hw_block, stream=stream)
+            e1.record(stream)
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+            if max_ms is not None and best > max_ms:
+                break
+        results.append((cand, best))
+    results.sort(key=lambda t: t[1])
+    return results

@@ -30,8 +30,7 @@ import numpy as np
 import torch
 
 from . import _native
-from .device import (DeviceCsr, device_block_starts, native_dtype, require_cuda, spmm,
-                     torch_dtype)
+from .device import DeviceCsr, native_dtype, prepare_aux, require_cuda, spmm, torch_dtype
 from .lowering import LoweredKernel
 from .matrices import DenseMatrix
 from .space import parse_point
@@ -120,13 +119,11 @@ def run(kernel, a, b, c0=None, *, precision: str = "double", device=None,
         dc = torch.from_numpy(np.asarray(c0.vals, dtype=np_dt).reshape(a.num_rows, n).copy()).to(dev)
     wb = torch.zeros(1, dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream(dev)
-    starts = None
-    if k.family in ("nnz-one", "nnz-multiple") and k.grid_size > 0:
-        starts = device_block_starts(da, k.chunk, k.grid_size, stream=stream)
+    aux = prepare_aux(k, da, stream=stream)
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
-    spmm(k, da, db, dc, accumulate=c0 is not None, starts=starts, writebacks=wb,
+    spmm(k, da, db, dc, accumulate=c0 is not None, aux=aux, writebacks=wb,
          hw_block=hw_block, stream=stream)
     t1.record(stream)
     t1.synchronize()

@@ -16,7 +16,7 @@ ROOT = Path(__file__).resolve().parents[1]
 
 def declared_symbols():
     text = (ROOT / "include" / "sgap.h").read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|const char \*)\s*(sgap_\w+)\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|size_t|const char \*)\s*(sgap_\w+)\(", text, re.M)))
 
 
 def test_header_and_binding_agree():
@@ -52,6 +52,10 @@ def test_argument_validation_without_device():
     L = _native.lib()
     k = _native.Kernel()
     assert L.sgap_run(None, None, None, None, 0, 0, None, None, None) == _native.ERR_ARG
+    assert L.sgap_long_row_threshold(None, 0) == -1
+    assert L.sgap_long_row_capacity(1000, -1) == 0
+    assert L.sgap_long_row_capacity(1000, 99) == 11
+    L.sgap_long_rows_tmp_bytes(1 << 20)  # needs a device to size CUB scratch; must not crash
     k.n, k.c = 4, 1
     a = _native.Csr()
     assert L.sgap_run(ctypes.byref(k), ctypes.byref(a), None, None, 7, 0, None, None,

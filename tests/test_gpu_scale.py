@@ -1,0 +1,81 @@
+"""Parity at BASELINE sizes: config 2 (R-MAT scale 20, 16.09M nnz, N=128)
+and a 27-point stencil, every family, against the CPU oracle.
+
+Power-law hub rows (up to ~40k nonzeros) are where float32 accumulation
+breaks the 1e-5 bound unless long sums are carried in float64 -- this is the
+test that pins the engine's numerics policy."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2209_02882_b200 import generators as G
+from paper_2209_02882_b200.device import DeviceCsr, prepare_aux, spmm
+from paper_2209_02882_b200.lowering import KernelConfig, lower
+from paper_2209_02882_b200.space import parse_point
+from paper_2209_02882_b200.templates import algorithm_template
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+POINTS_N128 = [
+    ("nnz:32,col:4,r:1", 256), ("nnz:8,col:2,r:1", 1024), ("nnz:32,col:1,r:1", 4096),
+    ("nnz:1,col:4,r:8", 1024), ("nnz:1,col:4,r:32", 1024), ("nnz:1,col:4,r:1", 256),
+    ("row:1,col:4,r:1", 256), ("row:4,col:1,r:1", 256),
+    ("row:1/4,col:4,r:4", 256), ("row:1/32,col:4,r:32", 256),
+]
+
+
+class _Rp:
+    def __init__(self, m, k, rp):
+        self.num_rows, self.num_cols, self.row_ptr = m, k, rp
+
+
+def _device(g):
+    return DeviceCsr(g.num_rows, g.num_cols, g.row_ptr.to(torch.int32), g.col_idx.to(torch.int32),
+                     g.vals.to(torch.float32))
+
+
+def _check(g, n, points):
+    dev = torch.device("cuda", 0)
+    a = _device(g)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(2)
+    b = torch.rand((g.num_cols, n), generator=gen, device=dev) * 2 - 1
+    rp = a.row_ptr.cpu().numpy()
+    want = oracle.spmm_f64(rp, a.col_idx.cpu().numpy(), a.vals.cpu().numpy(), b.cpu().numpy(), n)
+    c = torch.empty((a.num_rows, n), dtype=torch.float32, device=dev)
+    worst = {}
+    for text, p in points:
+        tpl = algorithm_template(parse_point(text), KernelConfig(n=n, p=p))
+        assert tpl is not None, text
+        k = lower(tpl, _Rp(a.num_rows, a.num_cols, rp.astype(np.int64)), compute_starts=False)
+        c.fill_(float("nan"))
+        spmm(k, a, b, c, aux=prepare_aux(k, a))
+        err = oracle.max_rel_error(c.cpu().numpy(), want)
+        worst[text] = err
+        assert err <= TOL, (text, p, err)
+    return worst
+
+
+def test_config2_rmat_every_family():
+    g = G.rmat(20, 16, seed=1, device="cuda")
+    assert g.nnz > 16_000_000
+    print(_check(g, 128, POINTS_N128))
+
+
+def test_stencil_small_n():
+    g = G.stencil27(48, device="cuda")
+    assert g.nnz == (3 * 48 - 2) ** 3
+    pts = [("nnz:1,col:1,r:8", 256), ("nnz:1,col:4,r:4", 256), ("nnz:32,col:4,r:1", 256),
+           ("row:1,col:4,r:1", 256), ("row:1/8,col:1,r:8", 256), ("row:1/4,col:4,r:4", 256)]
+    print(_check(g, 4, pts))
+
+
+def test_unpermuted_rmat_small_n():
+    g = G.rmat(16, 16, seed=3, permute=False, device="cuda")
+    pts = [("nnz:1,col:4,r:32", 1024), ("nnz:1,col:1,r:1", 256), ("nnz:16,col:4,r:1", 256),
+           ("row:1,col:4,r:1", 256), ("row:1/32,col:1,r:32", 256)]
+    print(_check(g, 8, pts))
