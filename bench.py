@@ -59,6 +59,7 @@ def parse_args():
     ap.add_argument("--point", default="", help="schedule point (default: selector)")
     ap.add_argument("--p", type=int, default=256)
     ap.add_argument("--hw-block", type=int, default=0)
+    ap.add_argument("--hw-variant", type=int, default=0)
     ap.add_argument("--sweep", default="", help="write the full candidate sweep (JSON) here")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -261,7 +262,7 @@ def main():
     # ---- schedule choice (untimed)
     sweep_rows = []
     if args.point:
-        choice = Candidate(args.point, args.p, args.hw_block)
+        choice = Candidate(args.point, args.p, args.hw_block, args.hw_variant)
     else:
         choice = None
         if rank == 0:
@@ -284,7 +285,8 @@ def main():
             c.zero_()
         if ev is not None:
             ev.record(stream)
-        spmm(k, a, b, c, accumulate=eb, aux=aux, hw_block=choice.hw_block, stream=stream)
+        spmm(k, a, b, c, accumulate=eb, aux=aux, hw_block=choice.hw_block,
+             hw_variant=choice.hw_variant, stream=stream)
 
     for _ in range(max(args.warmup, 3 if args.warmup >= 3 else args.warmup)):
         step()
@@ -339,7 +341,8 @@ def main():
             d_v.copy_(h_v, non_blocking=True)
             d_b.copy_(h_b, non_blocking=True)
             e_aux = prepare_aux(k, ea, stream=stream)
-            spmm(k, ea, d_b, c, accumulate=False, aux=e_aux, hw_block=choice.hw_block, stream=stream)
+            spmm(k, ea, d_b, c, accumulate=False, aux=e_aux, hw_block=choice.hw_block,
+                 hw_variant=choice.hw_variant, stream=stream)
             h_c.copy_(c, non_blocking=True)
 
         e2e_step()

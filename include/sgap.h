@@ -94,6 +94,8 @@ typedef struct {
     int32_t has_block_starts; /* == (LoweredKernel.block_starts is not None) */
     int32_t hw_block;       /* CTA size override: 0 = auto (256), else a warp
                                multiple in [32, 256]                        */
+    int32_t hw_variant;     /* nnz-multiple walk: 0 auto, 1 register-staged,
+                               2 TMA-staged (cp.async.bulk + mbarrier ring)  */
 } sgap_kernel_t;
 
 /* CSR operand on the device (matrices.py:38-86 with int32 indices). */
@@ -128,8 +130,11 @@ int sgap_block_starts(const int32_t *d_row_ptr, int64_t num_rows, int64_t chunk,
 /* Per-matrix side data of a kernel (what the reference's LoweredKernel
  * carries beyond its integers, plus the long-row table of this engine).  All
  * device memory is owned by the caller.
- *   d_block_starts: [grid_size + 1] from sgap_block_starts; required for the
- *     nnz families (LoweredKernel.block_starts, lowering.py:683-696).
+ *   d_block_starts: [grid_size + 1] from sgap_block_starts
+ *     (LoweredKernel.block_starts, lowering.py:683-696); informational: the
+ *     kernels use d_rowid instead of per-lane searches in its windows.
+ *   d_rowid: [nnz] row owning each position (from sgap_row_ids), bit 31 set
+ *     for rows of the long-row table; required for the nnz families.
  *   Long rows (float32 only, nnz families): rows with more than
  *   long_threshold nonzeros receive so many separate atomic flushes that a
  *   float32 running sum in C would exceed the 1e-5 accuracy bound; their
@@ -139,12 +144,20 @@ int sgap_block_starts(const int32_t *d_row_ptr, int64_t num_rows, int64_t chunk,
  *   by sgap_prepare_long_rows.  long_threshold < 0 disables the table.       */
 typedef struct {
     const int32_t *d_block_starts;
+    const int32_t *d_rowid;
     int32_t *d_long_rows;
     int32_t *d_long_count;
     double *d_long_acc;
     int64_t long_capacity;
     int64_t long_threshold;
 } sgap_aux_t;
+
+/* Per-position row ids (what the reference lowering recovers per lane with
+ * binary_search_before over the block window plus a forward advance,
+ * lowering.py:459-500), expanded once per matrix; bit 31 marks rows longer
+ * than long_threshold (pass -1 for none).                                  */
+int sgap_row_ids(const int32_t *d_row_ptr, int64_t num_rows, int64_t nnz,
+                 int64_t long_threshold, int32_t *d_rowid, void *stream);
 
 /* Threshold the engine uses for a kernel (-1: no table needed: row families
  * keep float64 running sums, float64 values accumulate in float64).        */

@@ -41,6 +41,7 @@ EXPORTED = (
     "sgap_legality_rule",
     "sgap_build_kernel",
     "sgap_block_starts",
+    "sgap_row_ids",
     "sgap_long_row_threshold",
     "sgap_long_row_capacity",
     "sgap_long_rows_tmp_bytes",
@@ -86,6 +87,7 @@ class Kernel(ctypes.Structure):
         ("block_size", ctypes.c_int64),
         ("has_block_starts", ctypes.c_int32),
         ("hw_block", ctypes.c_int32),
+        ("hw_variant", ctypes.c_int32),
     ]
 
 
@@ -103,6 +105,7 @@ class Csr(ctypes.Structure):
 class Aux(ctypes.Structure):
     _fields_ = [
         ("d_block_starts", ctypes.c_void_p),
+        ("d_rowid", ctypes.c_void_p),
         ("d_long_rows", ctypes.c_void_p),
         ("d_long_count", ctypes.c_void_p),
         ("d_long_acc", ctypes.c_void_p),
@@ -138,6 +141,8 @@ def lib():
     L.sgap_build_kernel.restype = ctypes.c_int
     L.sgap_block_starts.argtypes = [vp, i64, i64, i64, vp, vp]
     L.sgap_block_starts.restype = ctypes.c_int
+    L.sgap_row_ids.argtypes = [vp, i64, i64, i64, vp, vp]
+    L.sgap_row_ids.restype = ctypes.c_int
     L.sgap_long_row_threshold.argtypes = [ctypes.POINTER(Kernel), i32]
     L.sgap_long_row_threshold.restype = i64
     L.sgap_long_row_capacity.argtypes = [i64, i64]

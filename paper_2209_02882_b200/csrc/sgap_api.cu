@@ -92,7 +92,7 @@ int run_row_reciprocal(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, 
 
 template <typename T, int V, int R>
 int run_nnz_one_r(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
-                  const int *starts, const LongRows &lr, unsigned long long *wb, cudaStream_t st) {
+                  const int *rowid, const LongRows &lr, unsigned long long *wb, cudaStream_t st) {
     const int NT = k.n / V;
     const int TW = pow2_floor(NT < 32 / R ? NT : 32 / R);
     const int Q = 32 / TW;
@@ -100,74 +100,107 @@ int run_nnz_one_r(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
     const long long items = ceil_div(total_pos, Q);
     const int blk = k.hw_block > 0 ? k.hw_block : kHwBlock;
     k_nnz_one<T, V, R><<<grid_for(items, blk), blk, 0, st>>>(
-        a.d_row_ptr, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, starts,
-        (int)a.num_rows, k.n, a.nnz, k.chunk, k.grid_size, TW, lr, wb);
+        rowid, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, (int)a.num_rows, k.n, a.nnz,
+        total_pos, TW, lr, wb);
     return launch_status();
 }
 
 template <typename T, int V>
 int run_nnz_one(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
-                const int *starts, const LongRows &lr, unsigned long long *wb, cudaStream_t st) {
+                const int *rowid, const LongRows &lr, unsigned long long *wb, cudaStream_t st) {
     switch (k.r) {
-        case 1: return run_nnz_one_r<T, V, 1>(k, a, B, C, starts, lr, wb, st);
-        case 2: return run_nnz_one_r<T, V, 2>(k, a, B, C, starts, lr, wb, st);
-        case 4: return run_nnz_one_r<T, V, 4>(k, a, B, C, starts, lr, wb, st);
-        case 8: return run_nnz_one_r<T, V, 8>(k, a, B, C, starts, lr, wb, st);
-        case 16: return run_nnz_one_r<T, V, 16>(k, a, B, C, starts, lr, wb, st);
-        case 32: return run_nnz_one_r<T, V, 32>(k, a, B, C, starts, lr, wb, st);
+        case 1: return run_nnz_one_r<T, V, 1>(k, a, B, C, rowid, lr, wb, st);
+        case 2: return run_nnz_one_r<T, V, 2>(k, a, B, C, rowid, lr, wb, st);
+        case 4: return run_nnz_one_r<T, V, 4>(k, a, B, C, rowid, lr, wb, st);
+        case 8: return run_nnz_one_r<T, V, 8>(k, a, B, C, rowid, lr, wb, st);
+        case 16: return run_nnz_one_r<T, V, 16>(k, a, B, C, rowid, lr, wb, st);
+        case 32: return run_nnz_one_r<T, V, 32>(k, a, B, C, rowid, lr, wb, st);
         default: return SGAP_ERR_NO_TEMPLATE;
     }
 }
 
+// TMA tile: the largest multiple of lcm(g, 4) that fits a stage (so tiles
+// start on chunk boundaries and on 16-byte boundaries); 0 when none does.
+inline int tma_tile_for(int g) {
+    long long l = g;
+    while (l % 4) l += g;
+    if (l > kTmaTile) return 0;
+    return (int)((kTmaTile / l) * l);
+}
+
 template <typename T, int V, int W>
 int run_nnz_multiple_w(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
-                       const int *starts, const LongRows &lr, unsigned long long *wb,
+                       const int *rowid, const LongRows &lr, unsigned long long *wb,
                        cudaStream_t st) {
-    const long long chunks = k.grid_size * (k.chunk / k.g);
-    const long long items = ceil_div(chunks, 32 / W);
+    const long long total_pos = k.grid_size * k.chunk;
+    const int tile = tma_tile_for(k.g);
+    const bool tma_ok = tile > 0 && aligned(rowid, 16) && aligned(a.d_col_idx, 16) &&
+                        aligned(a.d_vals, 16);
+    const int variant = k.hw_variant == 0 ? (tma_ok ? 2 : 1) : k.hw_variant;
+    if (variant == 2) {
+        if (!tma_ok) return SGAP_ERR_ARG;
+        const size_t smem = tma_smem_bytes<T>();
+        auto kern = k_nnz_multiple_tma<T, V, W>;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
+            return SGAP_ERR_CUDA;
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTmaThreads, smem);
+        const long long ntiles = ceil_div(total_pos, tile);
+        long long ctas = (long long)sms * (per_sm > 0 ? per_sm : 1);
+        if (ctas > ntiles) ctas = ntiles;
+        if (ctas < 1) ctas = 1;
+        kern<<<(unsigned)ctas, kTmaThreads, smem, st>>>(
+            rowid, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, (int)a.num_rows, k.n,
+            a.nnz, k.g, total_pos, tile, lr, wb);
+        return launch_status();
+    }
+    const long long items = ceil_div(total_pos / k.g, 32 / W);
     const int blk = k.hw_block > 0 ? k.hw_block : kHwBlock;
     k_nnz_multiple<T, V, W><<<grid_for(items, blk), blk, 0, st>>>(
-        a.d_row_ptr, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, starts,
-        (int)a.num_rows, k.n, a.nnz, k.g, k.chunk, k.grid_size, lr, wb);
+        rowid, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, (int)a.num_rows, k.n,
+        a.nnz, k.g, total_pos, lr, wb);
     return launch_status();
 }
 
 template <typename T, int V>
 int run_nnz_multiple(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
-                     const int *starts, const LongRows &lr, unsigned long long *wb,
+                     const int *rowid, const LongRows &lr, unsigned long long *wb,
                      cudaStream_t st) {
     switch (pow2_floor(k.n / V)) {
-        case 1: return run_nnz_multiple_w<T, V, 1>(k, a, B, C, starts, lr, wb, st);
-        case 2: return run_nnz_multiple_w<T, V, 2>(k, a, B, C, starts, lr, wb, st);
-        case 4: return run_nnz_multiple_w<T, V, 4>(k, a, B, C, starts, lr, wb, st);
-        case 8: return run_nnz_multiple_w<T, V, 8>(k, a, B, C, starts, lr, wb, st);
-        case 16: return run_nnz_multiple_w<T, V, 16>(k, a, B, C, starts, lr, wb, st);
-        default: return run_nnz_multiple_w<T, V, 32>(k, a, B, C, starts, lr, wb, st);
+        case 1: return run_nnz_multiple_w<T, V, 1>(k, a, B, C, rowid, lr, wb, st);
+        case 2: return run_nnz_multiple_w<T, V, 2>(k, a, B, C, rowid, lr, wb, st);
+        case 4: return run_nnz_multiple_w<T, V, 4>(k, a, B, C, rowid, lr, wb, st);
+        case 8: return run_nnz_multiple_w<T, V, 8>(k, a, B, C, rowid, lr, wb, st);
+        case 16: return run_nnz_multiple_w<T, V, 16>(k, a, B, C, rowid, lr, wb, st);
+        default: return run_nnz_multiple_w<T, V, 32>(k, a, B, C, rowid, lr, wb, st);
     }
 }
 
 template <typename T, int V>
 int run_family(const sgap_kernel_t &k, const sgap_csr_t &a, const void *b, void *c, int acc,
-               const int *starts, const LongRows &lr, unsigned long long *wb, cudaStream_t st) {
+               const int *rowid, const LongRows &lr, unsigned long long *wb, cudaStream_t st) {
     const T *B = static_cast<const T *>(b);
     T *C = static_cast<T *>(c);
     switch (k.family) {
         case SGAP_ROW_MULTIPLE: return run_row_multiple<T, V>(k, a, B, C, acc, st);
         case SGAP_ROW_RECIPROCAL: return run_row_reciprocal<T, V>(k, a, B, C, acc, wb, st);
-        case SGAP_NNZ_ONE: return run_nnz_one<T, V>(k, a, B, C, starts, lr, wb, st);
-        case SGAP_NNZ_MULTIPLE: return run_nnz_multiple<T, V>(k, a, B, C, starts, lr, wb, st);
+        case SGAP_NNZ_ONE: return run_nnz_one<T, V>(k, a, B, C, rowid, lr, wb, st);
+        case SGAP_NNZ_MULTIPLE: return run_nnz_multiple<T, V>(k, a, B, C, rowid, lr, wb, st);
         default: return SGAP_ERR_ARG;
     }
 }
 
 template <typename T>
 int run_typed(const sgap_kernel_t &k, const sgap_csr_t &a, const void *b, void *c, int acc,
-              const int *starts, const LongRows &lr, unsigned long long *wb, cudaStream_t st) {
+              const int *rowid, const LongRows &lr, unsigned long long *wb, cudaStream_t st) {
     int status;
     switch (k.c) {
-        case 1: status = run_family<T, 1>(k, a, b, c, acc, starts, lr, wb, st); break;
-        case 2: status = run_family<T, 2>(k, a, b, c, acc, starts, lr, wb, st); break;
-        case 4: status = run_family<T, 4>(k, a, b, c, acc, starts, lr, wb, st); break;
+        case 1: status = run_family<T, 1>(k, a, b, c, acc, rowid, lr, wb, st); break;
+        case 2: status = run_family<T, 2>(k, a, b, c, acc, rowid, lr, wb, st); break;
+        case 4: status = run_family<T, 4>(k, a, b, c, acc, rowid, lr, wb, st); break;
         default: return SGAP_ERR_NO_TEMPLATE;
     }
     if (status != SGAP_OK || lr.threshold < 0) return status;
@@ -383,6 +416,17 @@ int sgap_prepare_long_rows(const int32_t *d_row_ptr, int64_t num_rows, int32_t n
     return launch_status();
 }
 
+int sgap_row_ids(const int32_t *d_row_ptr, int64_t num_rows, int64_t nnz,
+                 int64_t long_threshold, int32_t *d_rowid, void *stream) {
+    if (num_rows < 0 || nnz < 0 || num_rows > INT_MAX - 1 || nnz > INT_MAX) return SGAP_ERR_SHAPE;
+    if (nnz == 0) return SGAP_OK;
+    if (d_row_ptr == nullptr || d_rowid == nullptr || num_rows == 0) return SGAP_ERR_ARG;
+    const long long items = ceil_div(nnz, 1024);
+    k_row_ids<<<grid_for(items, kHwBlock), kHwBlock, 0, as_stream(stream)>>>(
+        d_row_ptr, (int)num_rows, nnz, long_threshold, d_rowid);
+    return launch_status();
+}
+
 int sgap_run(const sgap_kernel_t *k, const sgap_csr_t *a, const void *d_b, void *d_c,
              int32_t dtype, int32_t accumulate, const sgap_aux_t *aux,
              unsigned long long *d_writebacks, void *stream) {
@@ -404,8 +448,8 @@ int sgap_run(const sgap_kernel_t *k, const sgap_csr_t *a, const void *d_b, void 
     const size_t vec_bytes = esz * (size_t)(k->c == 4 && esz == 8 ? 2 : k->c);
     if ((d_b && !aligned(d_b, vec_bytes)) || !aligned(d_c, vec_bytes)) return SGAP_ERR_ARG;
     const bool eb = k->family == SGAP_NNZ_ONE || k->family == SGAP_NNZ_MULTIPLE;
-    const int32_t *starts = aux ? aux->d_block_starts : nullptr;
-    if (eb && k->grid_size > 0 && starts == nullptr) return SGAP_ERR_ARG;
+    const int32_t *rowid = aux ? aux->d_rowid : nullptr;
+    if (eb && k->grid_size > 0 && a->nnz > 0 && rowid == nullptr) return SGAP_ERR_ARG;
     if (k->family == SGAP_NNZ_MULTIPLE && (k->g < 1 || k->chunk % k->g)) return SGAP_ERR_CONFIG;
     LongRows lr{nullptr, nullptr, nullptr, -1};
     if (eb && aux && aux->long_threshold >= 0 && dtype == SGAP_F32) {
@@ -421,8 +465,8 @@ int sgap_run(const sgap_kernel_t *k, const sgap_csr_t *a, const void *d_b, void 
     }
     if (eb && k->grid_size == 0) return SGAP_OK;
     if (dtype == SGAP_F32)
-        return run_typed<float>(*k, *a, d_b, d_c, accumulate, starts, lr, d_writebacks, st);
-    return run_typed<double>(*k, *a, d_b, d_c, accumulate, starts, lr, d_writebacks, st);
+        return run_typed<float>(*k, *a, d_b, d_c, accumulate, rowid, lr, d_writebacks, st);
+    return run_typed<double>(*k, *a, d_b, d_c, accumulate, rowid, lr, d_writebacks, st);
 }
 
 int sgap_reference_spmm_f64(const sgap_csr_t *a, const void *d_b, int32_t n, int32_t dtype,

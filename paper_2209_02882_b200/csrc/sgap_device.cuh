@@ -147,26 +147,23 @@ struct LongRows {
     long long threshold;  // < 0: side table disabled (float64 values, RB families)
 };
 
-__device__ __forceinline__ int long_slot(const int *__restrict__ rp, const LongRows &lr, int row) {
-    if (lr.threshold < 0) return -1;
-    const int len = __ldg(rp + row + 1) - __ldg(rp + row);
-    if (len <= lr.threshold) return -1;
-    int lo = 0, hi = *lr.count;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (__ldg(lr.rows + mid) < row) lo = mid + 1; else hi = mid;
-    }
-    return lo;
-}
+// Row ids carry bit 31 when the row belongs to the long-row table.
+constexpr int kLongFlag = (int)0x80000000u;
+constexpr int kRowMask = 0x7fffffff;
 
-// One atomic writeback of a (row, column tile) partial.
+// One atomic writeback of a (row, column tile) partial; `rid` is a row id
+// (possibly flagged long).
 template <typename T, int V>
-__device__ __forceinline__ void flush_tile(T *__restrict__ C, int N, int row, long long kcol,
-                                           const Vec<double, V> &tot,
-                                           const int *__restrict__ rp, const LongRows &lr) {
-    const int slot = long_slot(rp, lr, row);
-    if (slot >= 0) {
-        double *p = lr.acc + (long long)slot * N + kcol;
+__device__ __forceinline__ void flush_row(T *__restrict__ C, int N, int rid, long long kcol,
+                                          const Vec<double, V> &tot, const LongRows &lr) {
+    const int row = rid & kRowMask;
+    if (rid < 0 && lr.threshold >= 0) {
+        int lo = 0, hi = *lr.count;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (__ldg(lr.rows + mid) < row) lo = mid + 1; else hi = mid;
+        }
+        double *p = lr.acc + (long long)lo * N + kcol;
 #pragma unroll
         for (int x = 0; x < V; ++x) atomicAdd(p + x, tot.v[x]);
     } else {
@@ -286,6 +283,56 @@ __device__ __forceinline__ void flush_count(unsigned long long *counter, unsigne
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) mine += __shfl_xor_sync(kFull, mine, off);
     if (lane_id() == 0 && mine) atomicAdd(counter, mine);
+}
+
+}  // namespace sgap
+
+namespace sgap {
+
+// ---------------------------------------------------------------------------
+// Bulk async copies (TMA engine, cp.async.bulk) + mbarrier pipeline helpers.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// 1-D global -> shared bulk copy completing on `bar` (bytes % 16 == 0, both
+// addresses 16-byte aligned).
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes,
+                                         unsigned long long *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
 }
 
 }  // namespace sgap

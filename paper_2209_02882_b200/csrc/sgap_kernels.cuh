@@ -23,7 +23,8 @@ namespace sgap {
     for (long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;     \
          item < (items); item += ((long long)gridDim.x * blockDim.x) >> 5)
 
-constexpr int kBatch = 4;  // independent gathers kept in flight per lane
+constexpr int kBatch = 4;     // independent gathers kept in flight per lane
+constexpr int kBatchTma = 8;  // ... in the TMA-staged walk
 
 // ===========================================================================
 // RB + serial reduction: row:g,col:c,r:1 (row-multiple).
@@ -219,13 +220,11 @@ k_row_reciprocal(const int *__restrict__ rp, const int *__restrict__ ci,
 // ===========================================================================
 template <typename T, int V, int R>
 __global__ void __launch_bounds__(256)
-k_nnz_one(const int *__restrict__ rp, const int *__restrict__ ci, const T *__restrict__ av,
-          const T *__restrict__ B, T *__restrict__ C, const int *__restrict__ starts,
-          int M, int N, long long nnz, long long npb, long long grid, int TW,
-          LongRows lr, unsigned long long *wb) {
+k_nnz_one(const int *__restrict__ rowid, const int *__restrict__ ci, const T *__restrict__ av,
+          const T *__restrict__ B, T *__restrict__ C, int M, int N, long long nnz,
+          long long total_pos, int TW, LongRows lr, unsigned long long *wb) {
     const int NT = N / V;
     const int Q = 32 / TW;
-    const long long total_pos = grid * npb;
     const long long items = (total_pos + Q - 1) / Q;
     const unsigned lane = lane_id();
     const int ql = (int)(lane & (unsigned)(Q - 1));
@@ -235,8 +234,11 @@ k_nnz_one(const int *__restrict__ rp, const int *__restrict__ ci, const T *__res
         const long long pos = item * Q + ql;
         const bool in_grid = pos < total_pos;
         const bool in_nnz = pos < nnz;
-        int row = 0;
-        if (in_grid) row = lane_row(rp, starts, pos / npb, pos, nnz, M);
+        // row owning the position; zero-extended lanes past nnz keep the
+        // clamped search row M-1 (lowering.py:476-488 with the window of the
+        // last block)
+        const int rid = in_nnz ? __ldg(rowid + pos) : (M - 1);
+        const int row = rid & kRowMask;
         const int col = in_nnz ? __ldg(ci + pos) : 0;
         const T a = in_nnz ? __ldg(av + pos) : T(0);
         SegLanes sl{};
@@ -265,7 +267,7 @@ k_nnz_one(const int *__restrict__ rp, const int *__restrict__ ci, const T *__res
                 Vec<double, V> tot;
 #pragma unroll
                 for (int x = 0; x < V; ++x) tot.v[x] = (double)prod.v[x];
-                flush_tile<T, V>(C, N, row, kcol, tot, rp, lr);
+                flush_row<T, V>(C, N, rid, kcol, tot, lr);
                 nwb += V;
             }
         }
@@ -287,14 +289,13 @@ k_nnz_one(const int *__restrict__ rp, const int *__restrict__ ci, const T *__res
 // ===========================================================================
 template <typename T, int V, int W>
 __global__ void __launch_bounds__(256)
-k_nnz_multiple(const int *__restrict__ rp, const int *__restrict__ ci,
+k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
                const T *__restrict__ av, const T *__restrict__ B, T *__restrict__ C,
-               const int *__restrict__ starts, int M, int N, long long nnz, int g,
-               long long chunk, long long grid, LongRows lr, unsigned long long *wb) {
+               int M, int N, long long nnz, int g, long long total_pos, LongRows lr,
+               unsigned long long *wb) {
     const int NT = N / V;
     constexpr int SG = 32 / W;
-    const long long cpb = chunk / g;
-    const long long total_chunks = grid * cpb;
+    const long long total_chunks = total_pos / g;
     const long long items = (total_chunks + SG - 1) / SG;
     const unsigned lane = lane_id();
     const int sg = (int)(lane / (unsigned)W);
@@ -305,20 +306,20 @@ k_nnz_multiple(const int *__restrict__ rp, const int *__restrict__ ci,
         if (ch >= total_chunks) continue;
         const long long base = ch * g;
         const long long end = min(base + (long long)g, nnz);
-        int hi = __ldg(starts + ch / cpb + 1) + 1;
-        hi = hi < M ? hi : M;
-        const int row0 = search_before(rp, __ldg(starts + ch / cpb), hi, base);
         for (int tile = sl; tile < NT; tile += W) {
             const long long kcol = (long long)tile * V;
-            int row = row0;
-            long long nb = __ldg(rp + row + 1);
+            if (base >= end) {  // chunk past nnz: the reference flushes 0 into row M-1
+                nwb += V;
+                continue;
+            }
+            int cur = __ldg(rowid + base);
             Vec<T, V> acc;
             acc.zero();
             Vec<double, V> tot;
             tot.zero();
             int since_fold = 0;
             for (long long pos = base; pos < end; pos += kBatch) {
-                int cc[kBatch];
+                int cc[kBatch], rr[kBatch];
                 T vv[kBatch];
                 Vec<T, V> bv[kBatch];
 #pragma unroll
@@ -326,6 +327,7 @@ k_nnz_multiple(const int *__restrict__ rp, const int *__restrict__ ci,
                     const bool ok = pos + u < end;
                     cc[u] = ok ? __ldg(ci + pos + u) : 0;
                     vv[u] = ok ? __ldg(av + pos + u) : T(0);
+                    rr[u] = ok ? __ldg(rowid + pos + u) : cur;
                 }
 #pragma unroll
                 for (int u = 0; u < kBatch; ++u) {
@@ -334,20 +336,15 @@ k_nnz_multiple(const int *__restrict__ rp, const int *__restrict__ ci,
                 }
 #pragma unroll
                 for (int u = 0; u < kBatch; ++u) {
-                    if (pos + u < end) {
-                        if (pos + u == nb) {
-                            fold<T, V>(tot, acc);
-                            flush_tile<T, V>(C, N, row, kcol, tot, rp, lr);
-                            nwb += V;
-                            tot.zero();
-                            since_fold = 0;
-                            do {
-                                ++row;
-                                nb = __ldg(rp + row + 1);
-                            } while (pos + u == nb);
-                        }
-                        fma_vec<T, V>(acc, vv[u], bv[u]);
+                    if (pos + u < end && rr[u] != cur) {
+                        fold<T, V>(tot, acc);
+                        flush_row<T, V>(C, N, cur, kcol, tot, lr);
+                        nwb += V;
+                        tot.zero();
+                        since_fold = 0;
+                        cur = rr[u];
                     }
+                    fma_vec<T, V>(acc, vv[u], bv[u]);
                 }
                 since_fold += kBatch;
                 if (since_fold >= 32) {
@@ -356,11 +353,194 @@ k_nnz_multiple(const int *__restrict__ rp, const int *__restrict__ ci,
                 }
             }
             fold<T, V>(tot, acc);
-            flush_tile<T, V>(C, N, row, kcol, tot, rp, lr);
+            flush_row<T, V>(C, N, cur, kcol, tot, lr);
             nwb += V;
         }
     }
     flush_count(wb, nwb);
+}
+
+// ---------------------------------------------------------------------------
+// The same family, TMA-staged: a persistent CTA walks tiles of `tile`
+// positions (a multiple of g, so chunks stay globally aligned).  One producer
+// warp streams each tile's (col, val, row id) arrays into a shared-memory
+// ring with cp.async.bulk, completion tracked by mbarriers; 8 consumer warps
+// take the tile's chunks and only ever touch global memory for the B-row
+// gathers and the C flushes.  This takes the A stream (and its DRAM latency)
+// off the gather's critical path.
+// ---------------------------------------------------------------------------
+constexpr int kTmaConsumerWarps = 8;
+constexpr int kTmaStages = 3;
+constexpr int kTmaTile = 2048;  // positions per stage (capacity)
+constexpr int kTmaThreads = (kTmaConsumerWarps + 1) * 32;
+
+template <typename T>
+constexpr size_t tma_smem_bytes() {
+    return (size_t)kTmaStages * kTmaTile * (2 * sizeof(int) + sizeof(T)) +
+           2 * kTmaStages * sizeof(unsigned long long);
+}
+
+template <typename T, int V, int W>
+__global__ void __launch_bounds__(kTmaThreads)
+k_nnz_multiple_tma(const int *__restrict__ rowid, const int *__restrict__ ci,
+                   const T *__restrict__ av, const T *__restrict__ B, T *__restrict__ C,
+                   int M, int N, long long nnz, int g, long long total_pos, int tile,
+                   LongRows lr, unsigned long long *wb) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    int *s_col = reinterpret_cast<int *>(smem);
+    int *s_row = s_col + kTmaStages * kTmaTile;
+    T *s_val = reinterpret_cast<T *>(s_row + kTmaStages * kTmaTile);
+    unsigned long long *full = reinterpret_cast<unsigned long long *>(s_val + kTmaStages * kTmaTile);
+    unsigned long long *empty = full + kTmaStages;
+    const int warp = threadIdx.x >> 5;
+    const unsigned lane = lane_id();
+    const long long ntiles = (total_pos + tile - 1) / tile;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kTmaStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kTmaConsumerWarps);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    unsigned long long nwb = 0;
+    if (warp == kTmaConsumerWarps) {
+        // ---------------- producer: one elected lane issues the bulk copies
+        if (lane == 0) {
+            int i = 0;
+            for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+                const int s = i % kTmaStages;
+                mbar_wait(&empty[s], ((i / kTmaStages) & 1) ^ 1);
+                const long long p0 = t * tile;
+                long long left = nnz - p0;
+                const int n_in = left <= 0 ? 0 : (left >= tile ? tile : (int)left);
+                const int n_bulk = n_in & ~3;  // 16-byte granules
+                int *dc = s_col + s * kTmaTile;
+                int *dr = s_row + s * kTmaTile;
+                T *dv = s_val + s * kTmaTile;
+                for (int q = n_bulk; q < n_in; ++q) {  // <= 3 tail elements
+                    dc[q] = __ldg(ci + p0 + q);
+                    dr[q] = __ldg(rowid + p0 + q);
+                    dv[q] = __ldg(av + p0 + q);
+                }
+                const unsigned tx = (unsigned)n_bulk * (unsigned)(2 * sizeof(int) + sizeof(T));
+                mbar_arrive_expect_tx(&full[s], tx);
+                if (n_bulk) {
+                    bulk_g2s(dc, ci + p0, (unsigned)n_bulk * sizeof(int), &full[s]);
+                    bulk_g2s(dr, rowid + p0, (unsigned)n_bulk * sizeof(int), &full[s]);
+                    bulk_g2s(dv, av + p0, (unsigned)n_bulk * sizeof(T), &full[s]);
+                }
+            }
+        }
+    } else {
+        // ---------------- consumers
+        constexpr int SG = 32 / W;
+        const int NT = N / V;
+        const int sg = (int)(lane / (unsigned)W);
+        const int sl = (int)(lane & (unsigned)(W - 1));
+        int i = 0;
+        for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+            const int s = i % kTmaStages;
+            mbar_wait(&full[s], (i / kTmaStages) & 1);
+            const long long p0 = t * tile;
+            const long long left = nnz - p0;
+            const int n_in = left <= 0 ? 0 : (left >= tile ? tile : (int)left);
+            const long long span = total_pos - p0;
+            const int chunks = (int)((span >= tile ? tile : span) / g);
+            const int *sc = s_col + s * kTmaTile;
+            const int *sr = s_row + s * kTmaTile;
+            const T *sv = s_val + s * kTmaTile;
+            for (int cj = warp * SG + sg; cj < chunks; cj += kTmaConsumerWarps * SG) {
+                const int q0 = cj * g;
+                const int qend = min(q0 + g, n_in);
+                for (int tc = sl; tc < NT; tc += W) {
+                    const long long kcol = (long long)tc * V;
+                    if (q0 >= qend) {  // chunk past nnz: a zero flush into row M-1
+                        nwb += V;
+                        continue;
+                    }
+                    int cur = sr[q0];
+                    Vec<T, V> acc;
+                    acc.zero();
+                    Vec<double, V> tot;
+                    tot.zero();
+                    int since_fold = 0;
+                    for (int q = q0; q < qend; q += kBatchTma) {
+                        int cc[kBatchTma], rr[kBatchTma];
+                        T vv[kBatchTma];
+                        Vec<T, V> bv[kBatchTma];
+#pragma unroll
+                        for (int u = 0; u < kBatchTma; ++u) {
+                            const bool ok = q + u < qend;
+                            cc[u] = ok ? sc[q + u] : 0;
+                            vv[u] = ok ? sv[q + u] : T(0);
+                            rr[u] = ok ? sr[q + u] : cur;
+                        }
+#pragma unroll
+                        for (int u = 0; u < kBatchTma; ++u) {
+                            if (q + u < qend) ldg_vec<T, V>(bv[u], B + (long long)cc[u] * N + kcol);
+                            else bv[u].zero();
+                        }
+#pragma unroll
+                        for (int u = 0; u < kBatchTma; ++u) {
+                            if (q + u < qend && rr[u] != cur) {
+                                fold<T, V>(tot, acc);
+                                flush_row<T, V>(C, N, cur, kcol, tot, lr);
+                                nwb += V;
+                                tot.zero();
+                                since_fold = 0;
+                                cur = rr[u];
+                            }
+                            fma_vec<T, V>(acc, vv[u], bv[u]);
+                        }
+                        since_fold += kBatchTma;
+                        if (since_fold >= 32) {
+                            fold<T, V>(tot, acc);
+                            since_fold = 0;
+                        }
+                    }
+                    fold<T, V>(tot, acc);
+                    flush_row<T, V>(C, N, cur, kcol, tot, lr);
+                    nwb += V;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+    }
+    flush_count(wb, nwb);
+}
+
+// Per-position row ids (the row owning each nonzero, lowering.py:459-500),
+// expanded once per matrix: a warp covers 1024 positions, each lane does one
+// binary search and then walks forward; bit 31 flags rows of the long-row
+// table (length > thr).
+__global__ void __launch_bounds__(256)
+k_row_ids(const int *__restrict__ rp, int M, long long nnz, long long thr, int *__restrict__ out) {
+    const long long items = (nnz + 1023) >> 10;
+    const unsigned lane = lane_id();
+    SGAP_WARP_LOOP(item, items) {
+        const long long base = item * 1024 + lane;
+        if (base >= nnz) continue;
+        int lo = 0, hi = M;  // last r in [0, M) with rp[r] <= base
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if ((long long)__ldg(rp + mid) <= base) lo = mid; else hi = mid;
+        }
+        int r = lo;
+        long long start = __ldg(rp + r), next = __ldg(rp + r + 1);
+        for (int j = 0; j < 32; ++j) {
+            const long long p = base + 32LL * j;
+            if (p >= nnz) break;
+            while (next <= p) {
+                ++r;
+                start = next;
+                next = __ldg(rp + r + 1);
+            }
+            const bool is_long = thr >= 0 && next - start > thr;
+            out[p] = r | (is_long ? kLongFlag : 0);
+        }
+    }
 }
 
 // Adds the float64 side table of long rows into C (after the SpMM kernel).

@@ -109,10 +109,10 @@ class DeviceCsr:
                          self.vals[base:end])
 
 
-def kernel_struct(k: LoweredKernel, *, hw_block: int = 0) -> _native.Kernel:
+def kernel_struct(k: LoweredKernel, *, hw_block: int = 0, hw_variant: int = 0) -> _native.Kernel:
     fam = _native.FAMILY_IDS[k.family]
     return _native.Kernel(fam, k.n, k.p, k.g, k.c, k.r, k.chunk, k.grid_size, k.block_size,
-                          1 if k.family in ("nnz-one", "nnz-multiple") else 0, hw_block)
+                          1 if k.family in ("nnz-one", "nnz-multiple") else 0, hw_block, hw_variant)
 
 
 def _stream_handle(stream) -> ctypes.c_void_p:
@@ -136,6 +136,7 @@ class KernelAux:
     by ``prepare_aux`` and reused across calls on the same matrix."""
 
     starts: torch.Tensor | None
+    rowid: torch.Tensor | None = None
     long_rows: torch.Tensor | None = None
     long_count: torch.Tensor | None = None
     long_acc: torch.Tensor | None = None
@@ -144,30 +145,41 @@ class KernelAux:
 
     def view(self) -> _native.Aux:
         ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
-        return _native.Aux(ptr(self.starts), ptr(self.long_rows), ptr(self.long_count),
-                           ptr(self.long_acc), self.long_capacity, self.long_threshold)
+        return _native.Aux(ptr(self.starts), ptr(self.rowid), ptr(self.long_rows),
+                           ptr(self.long_count), ptr(self.long_acc), self.long_capacity,
+                           self.long_threshold)
 
     def nbytes(self) -> int:
-        ts = (self.starts, self.long_rows, self.long_count, self.long_acc)
+        ts = (self.starts, self.rowid, self.long_rows, self.long_count, self.long_acc)
         return sum(t.numel() * t.element_size() for t in ts if t is not None)
 
 
-def prepare_aux(k: LoweredKernel, a: DeviceCsr, *, stream=None, long_rows: bool = True) -> KernelAux:
-    """Block starts (nnz families) and, for float32 values, the long-row
-    table (include/sgap.h, sgap_prepare_long_rows)."""
+def prepare_aux(k: LoweredKernel, a: DeviceCsr, *, stream=None, long_rows: bool = True,
+                long_threshold: int | None = None, block_starts: bool = True) -> KernelAux:
+    """Per-matrix side data of kernel ``k``: block starts and per-position row
+    ids (nnz families) and, for float32 values, the long-row table
+    (include/sgap.h: sgap_block_starts, sgap_row_ids, sgap_prepare_long_rows)."""
+    eb = k.family in ("nnz-one", "nnz-multiple")
     starts = None
-    if k.family in ("nnz-one", "nnz-multiple") and k.grid_size > 0:
+    if eb and k.grid_size > 0 and block_starts:
         starts = device_block_starts(a, k.chunk, k.grid_size, stream=stream)
     aux = KernelAux(starts)
-    if not long_rows:
+    if not eb:
         return aux
     L = _native.lib()
-    ks = kernel_struct(k)
-    thr = int(L.sgap_long_row_threshold(ctypes.byref(ks), native_dtype(a.vals.dtype)))
+    dev = a.device
+    thr = -1
+    if long_rows:
+        ks = kernel_struct(k)
+        thr = int(L.sgap_long_row_threshold(ctypes.byref(ks), native_dtype(a.vals.dtype)))
+        if long_threshold is not None and thr >= 0:
+            thr = int(long_threshold)
+    aux.rowid = torch.empty(max(a.nnz, 4), dtype=torch.int32, device=dev)
+    _native.check(L.sgap_row_ids(a.row_ptr.data_ptr(), a.num_rows, a.nnz, thr,
+                                 aux.rowid.data_ptr(), _stream_handle(stream)), "sgap_row_ids")
     if thr < 0:
         return aux
     cap = int(L.sgap_long_row_capacity(a.nnz, thr))
-    dev = a.device
     aux.long_threshold = thr
     aux.long_capacity = cap
     aux.long_rows = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
@@ -184,7 +196,8 @@ def prepare_aux(k: LoweredKernel, a: DeviceCsr, *, stream=None, long_rows: bool 
 
 def spmm(k: LoweredKernel, a: DeviceCsr, b: torch.Tensor, c: torch.Tensor, *,
          accumulate: bool = False, aux: KernelAux | None = None,
-         writebacks: torch.Tensor | None = None, hw_block: int = 0, stream=None) -> None:
+         writebacks: torch.Tensor | None = None, hw_block: int = 0, hw_variant: int = 0,
+         stream=None) -> None:
     """C (+)= A @ B with kernel ``k``, stream-ordered, no host synchronisation.
 
     ``b``: [num_cols, n] and ``c``: [num_rows, n] contiguous tensors of the
@@ -201,7 +214,7 @@ def spmm(k: LoweredKernel, a: DeviceCsr, b: torch.Tensor, c: torch.Tensor, *,
         raise ValueError("B and C must be contiguous row-major")
     if aux is None:
         aux = prepare_aux(k, a, stream=stream)
-    ks = kernel_struct(k, hw_block=hw_block)
+    ks = kernel_struct(k, hw_block=hw_block, hw_variant=hw_variant)
     view = a.view()
     av = aux.view()
     st = _native.lib().sgap_run(

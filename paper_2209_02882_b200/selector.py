@@ -59,9 +59,11 @@ class Candidate:
     point: str
     p: int
     hw_block: int = 0
+    hw_variant: int = 0  # nnz-multiple walk: 0 auto, 1 register-staged, 2 TMA-staged
 
     def label(self) -> str:
-        return f"{self.point}@p{self.p}" + (f"/b{self.hw_block}" if self.hw_block else "")
+        return (f"{self.point}@p{self.p}" + (f"/b{self.hw_block}" if self.hw_block else "")
+                + (f"/v{self.hw_variant}" if self.hw_variant else ""))
 
 
 class _RowPtrOnly:
@@ -138,11 +140,13 @@ def autotune(a: DeviceCsr, b: torch.Tensor, c: torch.Tensor, n: int, cands, *, r
         if k is None:
             continue
         aux = prepare_aux(k, a, stream=stream)
-        spmm(k, a, b, c, aux=aux, hw_block=cand.hw_block, stream=stream)  # warm
+        spmm(k, a, b, c, aux=aux, hw_block=cand.hw_block, hw_variant=cand.hw_variant,
+             stream=stream)  # warm
         best = float("inf")
         for i in range(reps):
             e0.record(stream)
-            spmm(k, a, b, c, aux=aux, hw_block=cand.hw_block, stream=stream)
+            spmm(k, a, b, c, aux=aux, hw_block=cand.hw_block, hw_variant=cand.hw_variant,
+                 stream=stream)
             e1.record(stream)
             e1.synchronize()
             best = min(best, e0.elapsed_time(e1))

@@ -96,7 +96,7 @@ def resolve_kernel(kernel, n: int, matrix) -> LoweredKernel:
 
 
 def run(kernel, a, b, c0=None, *, precision: str = "double", device=None,
-        hw_block: int = 0) -> tuple[DenseMatrix, GpuMetrics]:
+        hw_block: int = 0, hw_variant: int = 0) -> tuple[DenseMatrix, GpuMetrics]:
     """Execute ``kernel`` for C = c0 + A @ B on the GPU."""
     dt = torch_dtype(precision)  # ValueError on unknown precision, as in sim.py:444-445
     if a.num_cols != b.num_rows:
@@ -124,7 +124,7 @@ def run(kernel, a, b, c0=None, *, precision: str = "double", device=None,
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
     spmm(k, da, db, dc, accumulate=c0 is not None, aux=aux, writebacks=wb,
-         hw_block=hw_block, stream=stream)
+         hw_block=hw_block, hw_variant=hw_variant, stream=stream)
     t1.record(stream)
     t1.synchronize()
     out = DenseMatrix(a.num_rows, n, dc.double().cpu().numpy().reshape(-1))

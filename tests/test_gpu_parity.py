@@ -209,3 +209,34 @@ def test_device_group_macros_reference_gate_and_faults():
     out = np.zeros(8)
     assert exec_seg_reduce_group(np.array([5, 5, 5, 5]), np.ones(4), out, group_size=2) == 2
     assert out[5] == 4.0
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+def test_nnz_multiple_walk_variants(zoo, variant):
+    """Both nnz-multiple walks (register-staged, TMA-staged) on the zoo and
+    config 1, including g that does not divide the TMA tile evenly."""
+    sim = {(r["matrix"], r["n"], r["point"]): r for r in
+           json.loads((GOLDEN / "sim_metrics.json").read_text())}
+    for n in (4, 8):
+        cfg = KernelConfig(n=n, p=256)
+        pts = [pt for pt in templated(n, 256) if str(pt).startswith("nnz:") and
+               not str(pt).startswith("nnz:1,")]
+        assert pts
+        for label, mat, b_seed in zoo:
+            b = random_dense(mat.num_cols, n, seed=b_seed)
+            want = oracle_f32(mat, b, n)
+            for pt in pts:
+                k = build_kernel(pt, cfg, mat)
+                got, m = run(k, mat, b, precision="single", hw_variant=variant)
+                assert oracle.max_rel_error(got.vals, want) <= F32_TOL, (label, str(pt))
+                assert m.atomic_ops == sim[(label, n, str(pt))]["atomic_ops"]
+    a = random_csr(4096, 4096, 0.01, seed=1)
+    b = random_dense(4096, 32, seed=2)
+    want = oracle_f32(a, b, 32)
+    for text, p in (("nnz:32,col:4,r:1", 1024), ("nnz:2,col:4,r:1", 1024), ("nnz:16,col:2,r:1", 1024)):
+        k = build_kernel(parse_point(text), KernelConfig(32, p), a)
+        got, m = run(k, a, b, precision="single", hw_variant=variant)
+        assert oracle.max_rel_error(got.vals, want) <= F32_TOL, text
+        st = oracle.block_starts(a.row_ptr, k.chunk, k.grid_size)
+        assert m.atomic_ops == oracle.writebacks(k.family, a.row_ptr, 32, k.grid_size, starts=st,
+                                                 npb=k.chunk, r=k.r, chunk=k.chunk, g=k.g)

@@ -20,6 +20,7 @@ ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--n", type=int, default=0)
 ap.add_argument("--points", default="nnz:32,col:4,r:1@256")
 ap.add_argument("--blocks", default="0")
+ap.add_argument("--variants", default="0")
 ap.add_argument("--all", action="store_true")
 ap.add_argument("--check", action="store_true")
 ap.add_argument("--reps", type=int, default=5)
@@ -41,7 +42,8 @@ else:
     for item in args.points.split(";"):
         pt, p = item.split("@")
         for hb in args.blocks.split(","):
-            cands.append(Candidate(pt, int(p), int(hb)))
+            for hv in args.variants.split(","):
+                cands.append(Candidate(pt, int(p), int(hb), int(hv)))
 res = autotune(a, b, c, n, cands, reps=args.reps, row_ptr_host=rp, max_ms=100.0)
 abytes = bench.algorithmic_bytes(a.num_rows, a.nnz, n, touched)
 print(desc, "nnz", a.nnz, "n", n, "algorithmic MB", abytes / 1e6)
@@ -59,7 +61,7 @@ if args.check:
                            b.cpu().numpy(), n)
     for cd, ms in res[:8]:
         k = plan_for(cd, n, a.num_rows, a.num_cols, rp)
-        spmm(k, a, b, c, hw_block=cd.hw_block)
+        spmm(k, a, b, c, hw_block=cd.hw_block, hw_variant=cd.hw_variant)
         torch.cuda.synchronize()
         err = oracle.max_rel_error(c.cpu().numpy(), want)
         print(f"check {cd.label():32s} max_rel_error {err:.3e}", "OK" if err <= 1e-5 else "FAIL")
