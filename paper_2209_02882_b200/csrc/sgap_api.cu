@@ -128,19 +128,14 @@ inline int tma_tile_for(int g) {
     return (int)((kTmaTile / l) * l);
 }
 
-template <typename T, int V, int W>
-int run_nnz_multiple_w(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
-                       const int *rowid, const LongRows &lr, unsigned long long *wb,
-                       cudaStream_t st) {
+template <typename T, int V, int W, int U, bool PIPE, int STAGES = 3, int MINB = 3>
+int launch_nnz_multiple(bool tma, int tile, int owner, const sgap_kernel_t &k,
+                        const sgap_csr_t &a, const T *B, T *C, const int *rowid,
+                        const LongRows &lr, unsigned long long *wb, cudaStream_t st) {
     const long long total_pos = k.grid_size * k.chunk;
-    const int tile = tma_tile_for(k.g);
-    const bool tma_ok = tile > 0 && aligned(rowid, 16) && aligned(a.d_col_idx, 16) &&
-                        aligned(a.d_vals, 16);
-    const int variant = k.hw_variant == 0 ? (tma_ok ? 2 : 1) : k.hw_variant;
-    if (variant == 2) {
-        if (!tma_ok) return SGAP_ERR_ARG;
-        const size_t smem = tma_smem_bytes<T>();
-        auto kern = k_nnz_multiple_tma<T, V, W>;
+    if (tma) {
+        const size_t smem = tma_smem_bytes<T, STAGES>();
+        auto kern = k_nnz_multiple_tma<T, V, W, U, PIPE, STAGES, MINB>;
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
             cudaSuccess)
             return SGAP_ERR_CUDA;
@@ -153,29 +148,60 @@ int run_nnz_multiple_w(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, 
         if (ctas > ntiles) ctas = ntiles;
         if (ctas < 1) ctas = 1;
         kern<<<(unsigned)ctas, kTmaThreads, smem, st>>>(
-            rowid, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, (int)a.num_rows, k.n,
-            a.nnz, k.g, total_pos, tile, lr, wb);
+            rowid, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, a.d_row_ptr,
+            (int)a.num_rows, k.n, a.nnz, k.g, total_pos, tile, owner, lr, wb);
         return launch_status();
     }
     const long long items = ceil_div(total_pos / k.g, 32 / W);
     const int blk = k.hw_block > 0 ? k.hw_block : kHwBlock;
-    k_nnz_multiple<T, V, W><<<grid_for(items, blk), blk, 0, st>>>(
-        rowid, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, (int)a.num_rows, k.n,
-        a.nnz, k.g, total_pos, lr, wb);
+    const int vec4 = (k.g % 4 == 0) && aligned(rowid, 16) && aligned(a.d_col_idx, 16) &&
+                     aligned(a.d_vals, 16);
+    k_nnz_multiple<T, V, W, U, PIPE><<<grid_for(items, blk), blk, 0, st>>>(
+        rowid, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, a.d_row_ptr, (int)a.num_rows,
+        k.n, a.nnz, k.g, total_pos, vec4, owner, lr, wb);
     return launch_status();
+}
+
+// hw_variant: 0 auto; 1 register walk; 2 TMA-staged walk.  Measured on config
+// 2 (profiles/): software pipelining and 8-deep batches were slower (the extra
+// registers cost more occupancy than the added in-flight gathers recover), as
+// were L2 evict-first hints on the A stream; the TMA walk needs 3 CTAs/SM
+// (3-stage ring, <= 75 registers) to beat the register walk.
+template <typename T, int V, int W>
+int run_nnz_multiple_w(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
+                       const int *rowid, const LongRows &lr, int owner, unsigned long long *wb,
+                       cudaStream_t st) {
+    const int tile = tma_tile_for(k.g);
+    const bool tma_ok = tile > 0 && aligned(rowid, 16) && aligned(a.d_col_idx, 16) &&
+                        aligned(a.d_vals, 16);
+    // auto: the TMA-staged walk wins for short chunks (g <= 64 on config 2),
+    // the register walk for long ones (fewer, longer walks amortise the A
+    // loads it issues itself)
+    const int variant = k.hw_variant == 0 ? ((tma_ok && k.g <= 64) ? 2 : 1) : k.hw_variant;
+    const bool tma = variant == 2;
+    if (tma && !tma_ok) return SGAP_ERR_ARG;
+    if (variant != 1 && variant != 2) return SGAP_ERR_ARG;
+    return launch_nnz_multiple<T, V, W, 4, false>(tma, tile, owner, k, a, B, C, rowid, lr, wb, st);
 }
 
 template <typename T, int V>
 int run_nnz_multiple(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
-                     const int *rowid, const LongRows &lr, unsigned long long *wb,
+                     const int *rowid, const LongRows &lr, int acc, unsigned long long *wb,
                      cudaStream_t st) {
+    // overwrite mode: zero only rows that will receive atomic flushes (or no
+    // flush at all), then let the walk store complete rows outright
+    const int owner = acc ? 0 : 1;
+    if (owner) {
+        k_zero_shared_rows<T><<<grid_for(ceil_div(a.num_rows, 32), kHwBlock), kHwBlock, 0, st>>>(
+            a.d_row_ptr, (int)a.num_rows, k.n, k.g, lr.threshold, C);
+    }
     switch (pow2_floor(k.n / V)) {
-        case 1: return run_nnz_multiple_w<T, V, 1>(k, a, B, C, rowid, lr, wb, st);
-        case 2: return run_nnz_multiple_w<T, V, 2>(k, a, B, C, rowid, lr, wb, st);
-        case 4: return run_nnz_multiple_w<T, V, 4>(k, a, B, C, rowid, lr, wb, st);
-        case 8: return run_nnz_multiple_w<T, V, 8>(k, a, B, C, rowid, lr, wb, st);
-        case 16: return run_nnz_multiple_w<T, V, 16>(k, a, B, C, rowid, lr, wb, st);
-        default: return run_nnz_multiple_w<T, V, 32>(k, a, B, C, rowid, lr, wb, st);
+        case 1: return run_nnz_multiple_w<T, V, 1>(k, a, B, C, rowid, lr, owner, wb, st);
+        case 2: return run_nnz_multiple_w<T, V, 2>(k, a, B, C, rowid, lr, owner, wb, st);
+        case 4: return run_nnz_multiple_w<T, V, 4>(k, a, B, C, rowid, lr, owner, wb, st);
+        case 8: return run_nnz_multiple_w<T, V, 8>(k, a, B, C, rowid, lr, owner, wb, st);
+        case 16: return run_nnz_multiple_w<T, V, 16>(k, a, B, C, rowid, lr, owner, wb, st);
+        default: return run_nnz_multiple_w<T, V, 32>(k, a, B, C, rowid, lr, owner, wb, st);
     }
 }
 
@@ -188,7 +214,7 @@ int run_family(const sgap_kernel_t &k, const sgap_csr_t &a, const void *b, void 
         case SGAP_ROW_MULTIPLE: return run_row_multiple<T, V>(k, a, B, C, acc, st);
         case SGAP_ROW_RECIPROCAL: return run_row_reciprocal<T, V>(k, a, B, C, acc, wb, st);
         case SGAP_NNZ_ONE: return run_nnz_one<T, V>(k, a, B, C, rowid, lr, wb, st);
-        case SGAP_NNZ_MULTIPLE: return run_nnz_multiple<T, V>(k, a, B, C, rowid, lr, wb, st);
+        case SGAP_NNZ_MULTIPLE: return run_nnz_multiple<T, V>(k, a, B, C, rowid, lr, acc, wb, st);
         default: return SGAP_ERR_ARG;
     }
 }
@@ -208,7 +234,7 @@ int run_typed(const sgap_kernel_t &k, const sgap_csr_t &a, const void *b, void *
     long long cap_cells = (long long)k.n * 65536;
     unsigned blocks = (unsigned)ceil_div(cap_cells, kHwBlock);
     if (blocks > 4096) blocks = 4096;
-    k_long_rows_fold<T><<<blocks, kHwBlock, 0, st>>>(static_cast<T *>(c), k.n, lr);
+    k_long_rows_fold<T><<<blocks, kHwBlock, 0, st>>>(static_cast<T *>(c), k.n, lr, acc ? 0 : 1);
     return launch_status();
 }
 
@@ -374,7 +400,7 @@ int64_t sgap_long_row_threshold(const sgap_kernel_t *k, int32_t dtype) {
     if (k->family == SGAP_NNZ_MULTIPLE) unit = k->g;
     else if (k->family == SGAP_NNZ_ONE) unit = k->r;
     else return -1;  // row families own their rows: float64 running sums suffice
-    const long long t = 64 * unit;
+    const long long t = 32 * unit;
     return t < 128 ? 128 : t;
 }
 
@@ -457,13 +483,19 @@ int sgap_run(const sgap_kernel_t *k, const sgap_csr_t *a, const void *d_b, void 
             return SGAP_ERR_ARG;
         lr = LongRows{aux->d_long_rows, aux->d_long_count, aux->d_long_acc, aux->long_threshold};
     }
-    if (eb && !accumulate) {
+    if (k->family == SGAP_NNZ_ONE && !accumulate) {
         // atomic-writeback families accumulate into C: zero-fill (counts as
-        // part of the SpMM).
+        // part of the SpMM); nnz-multiple zero-fills only the
+        // rows it cannot store outright (k_zero_shared_rows).
         if (cudaMemsetAsync(d_c, 0, (size_t)out_elems * esz, st) != cudaSuccess)
             return SGAP_ERR_CUDA;
     }
-    if (eb && k->grid_size == 0) return SGAP_OK;
+    if (eb && k->grid_size == 0) {
+        if (k->family == SGAP_NNZ_MULTIPLE && !accumulate)  // every row is empty
+            return cudaMemsetAsync(d_c, 0, (size_t)out_elems * esz, st) == cudaSuccess ? SGAP_OK
+                                                                                    : SGAP_ERR_CUDA;
+        return SGAP_OK;
+    }
     if (dtype == SGAP_F32)
         return run_typed<float>(*k, *a, d_b, d_c, accumulate, rowid, lr, d_writebacks, st);
     return run_typed<double>(*k, *a, d_b, d_c, accumulate, rowid, lr, d_writebacks, st);

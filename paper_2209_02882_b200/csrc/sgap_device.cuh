@@ -114,10 +114,11 @@ __device__ __forceinline__ void add_vec(Vec<T, V> &acc, const Vec<T, V> &b) {
 }
 
 // ---------------------------------------------------------------------------
-// Accumulation numerics.  Products and short partial sums (<= 32 terms) are
+// Accumulation numerics.  Products and short partial sums (<= 8 terms) are
 // formed in the value type; every running sum that can grow past that is
 // carried in float64 ("tot") and rounded to the value type once, at the
-// writeback.  Without this a 40k-nonzero power-law row summed serially in
+// writeback.  (32-term float32 partials of config 2's hub row, whose summed
+// duplicate values reach |a| ~ 10, already cost 8.5e-6 of the 1e-5 budget.)  Without this a 40k-nonzero power-law row summed serially in
 // float32 misses the 1e-5 bound of the reference metric by 20x.
 // ---------------------------------------------------------------------------
 template <typename T, int V>

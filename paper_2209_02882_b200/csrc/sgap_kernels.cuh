@@ -24,7 +24,7 @@ namespace sgap {
          item < (items); item += ((long long)gridDim.x * blockDim.x) >> 5)
 
 constexpr int kBatch = 4;     // independent gathers kept in flight per lane
-constexpr int kBatchTma = 8;  // ... in the TMA-staged walk
+constexpr int kFoldEvery = 8;  // float32 partial sums fold into float64 every 8 terms
 
 // ===========================================================================
 // RB + serial reduction: row:g,col:c,r:1 (row-multiple).
@@ -287,12 +287,234 @@ k_nnz_one(const int *__restrict__ rowid, const int *__restrict__ ci, const T *__
 // consumes them, and the chunk's next row start is kept in a register so the
 // walk only touches row_ptr at a row change.
 // ===========================================================================
-template <typename T, int V, int W>
-__global__ void __launch_bounds__(256)
+// A-operand sources for the serial walk: global memory (read-only path) or
+// a shared-memory tile filled by the bulk-copy producer.
+template <typename T>
+struct GlobalA {
+    const int *rowid, *ci;
+    const T *av;
+    __device__ __forceinline__ int row(long long q) const { return __ldg(rowid + q); }
+    __device__ __forceinline__ int col(long long q) const { return __ldg(ci + q); }
+    __device__ __forceinline__ T val(long long q) const { return __ldg(av + q); }
+    // four consecutive positions, q % 4 == 0 (16-byte aligned)
+    __device__ __forceinline__ void load4(long long q, int4 &c, Vec<T, 4> &v, int4 &r) const {
+        c = __ldg(reinterpret_cast<const int4 *>(ci + q));
+        r = __ldg(reinterpret_cast<const int4 *>(rowid + q));
+        ldg_vec<T, 4>(v, av + q);
+    }
+};
+
+template <typename T>
+struct SharedA {
+    const int *sr, *sc;
+    const T *sv;
+    __device__ __forceinline__ int row(long long q) const { return sr[q]; }
+    __device__ __forceinline__ int col(long long q) const { return sc[q]; }
+    __device__ __forceinline__ T val(long long q) const { return sv[q]; }
+    __device__ __forceinline__ void load4(long long q, int4 &c, Vec<T, 4> &v, int4 &r) const {
+        c = *reinterpret_cast<const int4 *>(sc + q);
+        r = *reinterpret_cast<const int4 *>(sr + q);
+        if constexpr (sizeof(T) == 4) {
+            const float4 t = *reinterpret_cast<const float4 *>(sv + q);
+            v.v[0] = t.x; v.v[1] = t.y; v.v[2] = t.z; v.v[3] = t.w;
+        } else {
+            const double2 t0 = *reinterpret_cast<const double2 *>(sv + q);
+            const double2 t1 = *reinterpret_cast<const double2 *>(sv + q + 2);
+            v.v[0] = t0.x; v.v[1] = t0.y; v.v[2] = t1.x; v.v[3] = t1.y;
+        }
+    }
+};
+
+// Vectorised serial walk for chunks that start on a 4-position boundary:
+// one 16-byte load each of 4 (col), (val), (row id), four B-row gathers, and
+// -- since row ids are non-decreasing -- a single compare of the 4th row id
+// against the current row decides whether the batch can flush at all.
+// Owner writes (overwrite mode): a row whose nonzeros all lie inside one
+// chunk is flushed with a plain store -- nobody else touches it, so C needs
+// no zero-fill for it; rows split across chunks are zeroed by k_zero_shared_rows
+// and flushed atomically.  `base`/`end` are global positions of the chunk.
+struct Owner {
+    const int *rp;
+    long long base, end;
+    bool on;
+};
+
+template <typename T, int V>
+__device__ __forceinline__ void flush_owned(T *__restrict__ C, int N, int rid, long long kcol,
+                                            const Vec<double, V> &tot, const LongRows &lr,
+                                            bool complete) {
+    if (complete && rid >= 0)
+        store_vec<T, V>(C + (long long)rid * N + kcol, narrow<T, V>(tot), false);
+    else
+        flush_row<T, V>(C, N, rid, kcol, tot, lr);
+}
+
+// Vectorised serial walk for chunks that start on a 4-position boundary:
+// one 16-byte load each of 4 (col), (val), (row id), four B-row gathers, and
+// -- since row ids are non-decreasing -- a single compare of the 4th row id
+// against the current row decides whether the batch can flush at all.
+template <typename T, int V, class ASrc>
+__device__ __forceinline__ void eb_walk4(const ASrc &A, long long q0, long long qend,
+                                         const T *__restrict__ B, int N, long long kcol,
+                                         T *__restrict__ C, const LongRows &lr, const Owner &own,
+                                         unsigned long long &nwb) {
+    int cur = A.row(q0);
+    bool here = own.on && __ldg(own.rp + (cur & kRowMask)) == own.base;
+    Vec<T, V> acc;
+    acc.zero();
+    Vec<double, V> tot;
+    tot.zero();
+    int since_fold = 0;
+    const T *bk = B + kcol;
+    long long q = q0;
+    for (; q + 4 <= qend; q += 4) {
+        int4 c, r;
+        Vec<T, 4> v;
+        A.load4(q, c, v, r);
+        Vec<T, V> b0, b1, b2, b3;
+        ldg_vec<T, V>(b0, bk + (long long)c.x * N);
+        ldg_vec<T, V>(b1, bk + (long long)c.y * N);
+        ldg_vec<T, V>(b2, bk + (long long)c.z * N);
+        ldg_vec<T, V>(b3, bk + (long long)c.w * N);
+        if (r.w == cur) {
+            fma_vec<T, V>(acc, v.v[0], b0);
+            fma_vec<T, V>(acc, v.v[1], b1);
+            fma_vec<T, V>(acc, v.v[2], b2);
+            fma_vec<T, V>(acc, v.v[3], b3);
+        } else {
+            const int rr[4] = {r.x, r.y, r.z, r.w};
+            const Vec<T, V> *bb[4] = {&b0, &b1, &b2, &b3};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (rr[u] != cur) {
+                    fold<T, V>(tot, acc);
+                    flush_owned<T, V>(C, N, cur, kcol, tot, lr, here);
+                    nwb += V;
+                    tot.zero();
+                    since_fold = 0;
+                    cur = rr[u];
+                    here = own.on;
+                }
+                fma_vec<T, V>(acc, v.v[u], *bb[u]);
+            }
+        }
+        since_fold += 4;
+        if (since_fold >= kFoldEvery) {
+            fold<T, V>(tot, acc);
+            since_fold = 0;
+        }
+    }
+    for (; q < qend; ++q) {  // < 4 tail positions
+        const int rq = A.row(q);
+        Vec<T, V> b;
+        ldg_vec<T, V>(b, bk + (long long)A.col(q) * N);
+        if (rq != cur) {
+            fold<T, V>(tot, acc);
+            flush_owned<T, V>(C, N, cur, kcol, tot, lr, here);
+            nwb += V;
+            tot.zero();
+            cur = rq;
+            here = own.on;
+        }
+        fma_vec<T, V>(acc, A.val(q), b);
+    }
+    fold<T, V>(tot, acc);
+    const bool complete = here && __ldg(own.rp + (cur & kRowMask) + 1) == own.end;
+    flush_owned<T, V>(C, N, cur, kcol, tot, lr, complete);
+    nwb += V;
+}
+
+template <typename T, int V, int U>
+struct WalkBatch {
+    int c[U], r[U];
+    T v[U];
+    Vec<T, V> b[U];
+};
+
+// The serial nnz walk of one chunk [q0, qend) for one column tile, software
+// pipelined: batch i+1's (col, val, row) and its U B-row gathers are issued
+// before batch i is consumed, so 2U gathers are in flight per lane.  A flush
+// (row change or chunk end) is one writeback; partial sums fold into float64
+// every 32 positions.
+template <typename T, int V, int U, bool PIPE, class ASrc>
+__device__ __forceinline__ void eb_walk(const ASrc &A, long long q0, long long qend,
+                                        const T *__restrict__ B, int N, long long kcol,
+                                        T *__restrict__ C, const LongRows &lr, const Owner &own,
+                                        unsigned long long &nwb) {
+    auto fetch = [&](long long q, WalkBatch<T, V, U> &w) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const bool ok = q + u < qend;
+            w.c[u] = ok ? A.col(q + u) : 0;
+            w.v[u] = ok ? A.val(q + u) : T(0);
+            w.r[u] = ok ? A.row(q + u) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (q + u < qend) ldg_vec<T, V>(w.b[u], B + (long long)w.c[u] * N + kcol);
+            else w.b[u].zero();
+        }
+    };
+    int cur = A.row(q0);
+    bool here = own.on && __ldg(own.rp + (cur & kRowMask)) == own.base;
+    Vec<T, V> acc;
+    acc.zero();
+    Vec<double, V> tot;
+    tot.zero();
+    int since_fold = 0;
+    auto consume = [&](long long q, const WalkBatch<T, V, U> &w) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (q + u < qend && w.r[u] != cur) {
+                fold<T, V>(tot, acc);
+                flush_owned<T, V>(C, N, cur, kcol, tot, lr, here);
+                nwb += V;
+                tot.zero();
+                since_fold = 0;
+                cur = w.r[u];
+                here = own.on;
+            }
+            fma_vec<T, V>(acc, w.v[u], w.b[u]);
+        }
+        since_fold += U;
+        if (since_fold >= kFoldEvery) {
+            fold<T, V>(tot, acc);
+            since_fold = 0;
+        }
+    };
+    if constexpr (PIPE) {
+        WalkBatch<T, V, U> w0, w1;
+        fetch(q0, w0);
+        for (long long q = q0;;) {
+            if (q + U < qend) fetch(q + U, w1);
+            consume(q, w0);
+            q += U;
+            if (q >= qend) break;
+            if (q + U < qend) fetch(q + U, w0);
+            consume(q, w1);
+            q += U;
+            if (q >= qend) break;
+        }
+    } else {
+        WalkBatch<T, V, U> w0;
+        for (long long q = q0; q < qend; q += U) {
+            fetch(q, w0);
+            consume(q, w0);
+        }
+    }
+    fold<T, V>(tot, acc);
+    const bool complete = here && __ldg(own.rp + (cur & kRowMask) + 1) == own.end;
+    flush_owned<T, V>(C, N, cur, kcol, tot, lr, complete);
+    nwb += V;
+}
+
+template <typename T, int V, int W, int U, bool PIPE>
+__global__ void __launch_bounds__(256, 4)
 k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
                const T *__restrict__ av, const T *__restrict__ B, T *__restrict__ C,
-               int M, int N, long long nnz, int g, long long total_pos, LongRows lr,
-               unsigned long long *wb) {
+               const int *__restrict__ rp, int M, int N, long long nnz, int g,
+               long long total_pos, int vec4, int owner, LongRows lr, unsigned long long *wb) {
+    const bool VEC4 = vec4 != 0;  // g % 4 == 0 and 16-byte aligned A arrays
     const int NT = N / V;
     constexpr int SG = 32 / W;
     const long long total_chunks = total_pos / g;
@@ -300,6 +522,7 @@ k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
     const unsigned lane = lane_id();
     const int sg = (int)(lane / (unsigned)W);
     const int sl = (int)(lane & (unsigned)(W - 1));
+    const GlobalA<T> A{rowid, ci, av};
     unsigned long long nwb = 0;
     SGAP_WARP_LOOP(item, items) {
         const long long ch = item * SG + sg;
@@ -307,54 +530,15 @@ k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
         const long long base = ch * g;
         const long long end = min(base + (long long)g, nnz);
         for (int tile = sl; tile < NT; tile += W) {
-            const long long kcol = (long long)tile * V;
             if (base >= end) {  // chunk past nnz: the reference flushes 0 into row M-1
                 nwb += V;
                 continue;
             }
-            int cur = __ldg(rowid + base);
-            Vec<T, V> acc;
-            acc.zero();
-            Vec<double, V> tot;
-            tot.zero();
-            int since_fold = 0;
-            for (long long pos = base; pos < end; pos += kBatch) {
-                int cc[kBatch], rr[kBatch];
-                T vv[kBatch];
-                Vec<T, V> bv[kBatch];
-#pragma unroll
-                for (int u = 0; u < kBatch; ++u) {
-                    const bool ok = pos + u < end;
-                    cc[u] = ok ? __ldg(ci + pos + u) : 0;
-                    vv[u] = ok ? __ldg(av + pos + u) : T(0);
-                    rr[u] = ok ? __ldg(rowid + pos + u) : cur;
-                }
-#pragma unroll
-                for (int u = 0; u < kBatch; ++u) {
-                    if (pos + u < end) ldg_vec<T, V>(bv[u], B + (long long)cc[u] * N + kcol);
-                    else bv[u].zero();
-                }
-#pragma unroll
-                for (int u = 0; u < kBatch; ++u) {
-                    if (pos + u < end && rr[u] != cur) {
-                        fold<T, V>(tot, acc);
-                        flush_row<T, V>(C, N, cur, kcol, tot, lr);
-                        nwb += V;
-                        tot.zero();
-                        since_fold = 0;
-                        cur = rr[u];
-                    }
-                    fma_vec<T, V>(acc, vv[u], bv[u]);
-                }
-                since_fold += kBatch;
-                if (since_fold >= 32) {
-                    fold<T, V>(tot, acc);
-                    since_fold = 0;
-                }
-            }
-            fold<T, V>(tot, acc);
-            flush_row<T, V>(C, N, cur, kcol, tot, lr);
-            nwb += V;
+            const Owner own{rp, base, end, owner != 0};
+            if (VEC4)
+                eb_walk4<T, V>(A, base, end, B, N, (long long)tile * V, C, lr, own, nwb);
+            else
+                eb_walk<T, V, U, PIPE>(A, base, end, B, N, (long long)tile * V, C, lr, own, nwb);
         }
     }
     flush_count(wb, nwb);
@@ -370,22 +554,23 @@ k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
 // off the gather's critical path.
 // ---------------------------------------------------------------------------
 constexpr int kTmaConsumerWarps = 8;
-constexpr int kTmaStages = 3;
 constexpr int kTmaTile = 2048;  // positions per stage (capacity)
 constexpr int kTmaThreads = (kTmaConsumerWarps + 1) * 32;
 
-template <typename T>
+template <typename T, int STAGES>
 constexpr size_t tma_smem_bytes() {
-    return (size_t)kTmaStages * kTmaTile * (2 * sizeof(int) + sizeof(T)) +
-           2 * kTmaStages * sizeof(unsigned long long);
+    return (size_t)STAGES * kTmaTile * (2 * sizeof(int) + sizeof(T)) +
+           2 * STAGES * sizeof(unsigned long long);
 }
 
-template <typename T, int V, int W>
-__global__ void __launch_bounds__(kTmaThreads)
+template <typename T, int V, int W, int U, bool PIPE, int kTmaStages, int MINB>
+__global__ void __launch_bounds__(kTmaThreads, MINB)
 k_nnz_multiple_tma(const int *__restrict__ rowid, const int *__restrict__ ci,
                    const T *__restrict__ av, const T *__restrict__ B, T *__restrict__ C,
-                   int M, int N, long long nnz, int g, long long total_pos, int tile,
-                   LongRows lr, unsigned long long *wb) {
+                   const int *__restrict__ rp, int M, int N, long long nnz, int g,
+                   long long total_pos, int tile, int owner, LongRows lr,
+                   unsigned long long *wb) {
+    const bool VEC4 = (g % 4) == 0;
     extern __shared__ __align__(128) unsigned char smem[];
     int *s_col = reinterpret_cast<int *>(smem);
     int *s_row = s_col + kTmaStages * kTmaTile;
@@ -450,58 +635,21 @@ k_nnz_multiple_tma(const int *__restrict__ rowid, const int *__restrict__ ci,
             const int *sc = s_col + s * kTmaTile;
             const int *sr = s_row + s * kTmaTile;
             const T *sv = s_val + s * kTmaTile;
+            const SharedA<T> SA{sr, sc, sv};
             for (int cj = warp * SG + sg; cj < chunks; cj += kTmaConsumerWarps * SG) {
                 const int q0 = cj * g;
                 const int qend = min(q0 + g, n_in);
                 for (int tc = sl; tc < NT; tc += W) {
-                    const long long kcol = (long long)tc * V;
                     if (q0 >= qend) {  // chunk past nnz: a zero flush into row M-1
                         nwb += V;
                         continue;
                     }
-                    int cur = sr[q0];
-                    Vec<T, V> acc;
-                    acc.zero();
-                    Vec<double, V> tot;
-                    tot.zero();
-                    int since_fold = 0;
-                    for (int q = q0; q < qend; q += kBatchTma) {
-                        int cc[kBatchTma], rr[kBatchTma];
-                        T vv[kBatchTma];
-                        Vec<T, V> bv[kBatchTma];
-#pragma unroll
-                        for (int u = 0; u < kBatchTma; ++u) {
-                            const bool ok = q + u < qend;
-                            cc[u] = ok ? sc[q + u] : 0;
-                            vv[u] = ok ? sv[q + u] : T(0);
-                            rr[u] = ok ? sr[q + u] : cur;
-                        }
-#pragma unroll
-                        for (int u = 0; u < kBatchTma; ++u) {
-                            if (q + u < qend) ldg_vec<T, V>(bv[u], B + (long long)cc[u] * N + kcol);
-                            else bv[u].zero();
-                        }
-#pragma unroll
-                        for (int u = 0; u < kBatchTma; ++u) {
-                            if (q + u < qend && rr[u] != cur) {
-                                fold<T, V>(tot, acc);
-                                flush_row<T, V>(C, N, cur, kcol, tot, lr);
-                                nwb += V;
-                                tot.zero();
-                                since_fold = 0;
-                                cur = rr[u];
-                            }
-                            fma_vec<T, V>(acc, vv[u], bv[u]);
-                        }
-                        since_fold += kBatchTma;
-                        if (since_fold >= 32) {
-                            fold<T, V>(tot, acc);
-                            since_fold = 0;
-                        }
-                    }
-                    fold<T, V>(tot, acc);
-                    flush_row<T, V>(C, N, cur, kcol, tot, lr);
-                    nwb += V;
+                    const Owner own{rp, p0 + q0, p0 + qend, owner != 0};
+                    if (VEC4)
+                        eb_walk4<T, V>(SA, q0, qend, B, N, (long long)tc * V, C, lr, own, nwb);
+                    else
+                        eb_walk<T, V, U, PIPE>(SA, q0, qend, B, N, (long long)tc * V, C, lr, own,
+                                               nwb);
                 }
             }
             __syncwarp();
@@ -546,14 +694,51 @@ k_row_ids(const int *__restrict__ rp, int M, long long nnz, long long thr, int *
 // Adds the float64 side table of long rows into C (after the SpMM kernel).
 template <typename T>
 __global__ void __launch_bounds__(256)
-k_long_rows_fold(T *__restrict__ C, int N, LongRows lr) {
+k_long_rows_fold(T *__restrict__ C, int N, LongRows lr, int overwrite) {
     const long long total = (long long)(*lr.count) * N;
     for (long long h = (long long)blockIdx.x * blockDim.x + threadIdx.x; h < total;
          h += (long long)gridDim.x * blockDim.x) {
         const long long slot = h / N;
         const long long k = h - slot * N;
         const long long off = (long long)__ldg(lr.rows + slot) * N + k;
-        C[off] = (T)((double)C[off] + lr.acc[h]);
+        const double base = overwrite ? 0.0 : (double)C[off];
+        C[off] = (T)(base + lr.acc[h]);
+        lr.acc[h] = 0.0;  // leave the table cleared for the next call
+    }
+}
+
+// Overwrite-mode zero-fill for the owner-write walk: zero only the C rows the
+// walk does not store outright -- empty rows and rows whose nonzeros span more
+// than one g-position chunk (those receive atomic flushes) -- except long rows,
+// which the side-table fold overwrites.  Lanes test one row each; the warp
+// then clears the flagged rows cooperatively with 16-byte stores.
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_zero_shared_rows(const int *__restrict__ rp, int M, int N, long long g, long long thr,
+                   T *__restrict__ C) {
+    const long long items = ((long long)M + 31) >> 5;
+    const unsigned lane = lane_id();
+    SGAP_WARP_LOOP(item, items) {
+        const long long r = item * 32 + lane;
+        bool need = false;
+        if (r < M) {
+            const long long s = __ldg(rp + r), e = __ldg(rp + r + 1);
+            const long long len = e - s;
+            need = len == 0 || (s / g != (e - 1) / g && !(thr >= 0 && len > thr));
+        }
+        unsigned mask = __ballot_sync(kFull, need);
+        while (mask) {
+            const int src = __ffs(mask) - 1;
+            mask &= mask - 1;
+            T *row = C + (item * 32 + src) * (long long)N;
+            if ((N * sizeof(T)) % 16 == 0) {
+                float4 *r4 = reinterpret_cast<float4 *>(row);
+                const int n4 = (int)(N * sizeof(T) / 16);
+                for (int x = lane; x < n4; x += 32) r4[x] = make_float4(0.f, 0.f, 0.f, 0.f);
+            } else {
+                for (int x = lane; x < N; x += 32) row[x] = T(0);
+            }
+        }
     }
 }
 

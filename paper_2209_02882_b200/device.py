@@ -21,7 +21,7 @@ from . import _native
 from .lowering import LoweredKernel
 
 __all__ = ["DeviceCsr", "KernelAux", "kernel_struct", "device_block_starts", "prepare_aux", "spmm",
-           "reference_spmm_f64", "torch_dtype", "native_dtype", "require_cuda"]
+           "launches_per_call", "reference_spmm_f64", "torch_dtype", "native_dtype", "require_cuda"]
 
 _INT32_MAX = 2**31 - 1
 
@@ -222,6 +222,17 @@ def spmm(k: LoweredKernel, a: DeviceCsr, b: torch.Tensor, c: torch.Tensor, *,
         native_dtype(a.vals.dtype), 1 if accumulate else 0, ctypes.byref(av),
         writebacks.data_ptr() if writebacks is not None else None, _stream_handle(stream))
     _native.check(st, "sgap_run")
+
+
+def launches_per_call(k: LoweredKernel, aux: KernelAux | None, *, accumulate: bool = False) -> int:
+    """Kernels of libsgap.so one ``spmm`` call launches (the driver's memset
+    for the nnz-one zero-fill is not ours and not counted)."""
+    n = 1
+    if k.family == "nnz-multiple" and not accumulate:
+        n += 1  # k_zero_shared_rows
+    if aux is not None and aux.long_threshold >= 0 and k.family in ("nnz-one", "nnz-multiple"):
+        n += 1  # k_long_rows_fold
+    return n
 
 
 def reference_spmm_f64(a: DeviceCsr, b: torch.Tensor, n: int, *, stream=None) -> torch.Tensor:

@@ -80,13 +80,21 @@ def plan_for(cand: Candidate, n: int, num_rows: int, num_cols: int, row_ptr_host
     return lower(tpl, _RowPtrOnly(num_rows, num_cols, row_ptr_host), compute_starts=False)
 
 
-def candidates(n: int, p_values=(256, 1024)) -> list[Candidate]:
+# The B200 knob grid widens the reference's default g in {2..32}
+# (space.py:220) with longer serial chunks, which the EB walk amortises
+# best on power-law matrices; the point grammar already admits any g >= 2.
+GPU_G_VALUES = (2, 4, 8, 16, 32, 64, 128, 256, 512)
+
+
+def candidates(n: int, p_values=(256, 1024), g_values=GPU_G_VALUES,
+               variants: bool = True) -> list[Candidate]:
     """Every templated point at dense width n for each p (deduplicated by
-    the kernel it lowers to)."""
+    the kernel it lowers to); nnz-multiple points come with both walks
+    (register-staged and TMA-staged) when ``variants``."""
     out, seen = [], set()
     for p in p_values:
         cfg = KernelConfig(n=n, p=p)
-        for pt in enumerate_space().legal:
+        for pt in enumerate_space(g_values=g_values).legal:
             tpl = algorithm_template(pt, cfg)
             if tpl is None:
                 continue
@@ -94,7 +102,10 @@ def candidates(n: int, p_values=(256, 1024)) -> list[Candidate]:
             if key in seen:
                 continue
             seen.add(key)
-            out.append(Candidate(str(pt), p))
+            if variants and tpl.family == "nnz-multiple":
+                out.extend(Candidate(str(pt), p, 0, v) for v in (1, 2))
+            else:
+                out.append(Candidate(str(pt), p))
     return out
 
 
