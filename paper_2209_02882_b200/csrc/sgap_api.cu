@@ -50,18 +50,29 @@ bool aligned(const void *p, size_t bytes) {
 
 // ------------------------------------------------------------------ dispatch
 
+// hw_variant for row-multiple: 0/1 the logical mapping (thread (rg, t) owns
+// rows rg*g .. rg*g+g-1), 2 the interleaved mapping (a CTA's warps on adjacent
+// rows; needs N/c <= CTA size).
 template <typename T, int V>
 int run_row_multiple(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
                      int acc, cudaStream_t st) {
     const int N = k.n, L = N / V;
-    int S = 0;
-    if (L <= 32 && (32 % L) == 0) S = L;
-    else if (L % 32 == 0) S = 32;
-    const long long total = ceil_div(a.num_rows, k.g) * (long long)L;
     const int blk = k.hw_block > 0 ? k.hw_block : kHwBlock;
+    const int vec4 = aligned(a.d_col_idx, 16) && aligned(a.d_vals, 16);
+    if (k.hw_variant == 2) {
+        if (L > blk) return SGAP_ERR_ARG;
+        const long long tile_rows = (long long)(blk / L) * k.g;
+        const long long tiles = ceil_div(a.num_rows, tile_rows);
+        const unsigned ctas = (unsigned)(tiles < (1LL << 30) ? (tiles > 0 ? tiles : 1) : (1LL << 30));
+        k_row_interleaved<T, V><<<ctas, blk, 0, st>>>(a.d_row_ptr, a.d_col_idx,
+                                                      static_cast<const T *>(a.d_vals), B, C,
+                                                      (int)a.num_rows, N, k.g, vec4, acc);
+        return launch_status();
+    }
+    const long long total = ceil_div(a.num_rows, k.g) * (long long)L;
     k_row_multiple<T, V><<<grid_for(ceil_div(total, 32), blk), blk, 0, st>>>(
         a.d_row_ptr, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, (int)a.num_rows, N,
-        k.g, S, acc);
+        k.g, vec4, acc);
     return launch_status();
 }
 
@@ -174,10 +185,11 @@ int run_nnz_multiple_w(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, 
     const int tile = tma_tile_for(k.g);
     const bool tma_ok = tile > 0 && aligned(rowid, 16) && aligned(a.d_col_idx, 16) &&
                         aligned(a.d_vals, 16);
-    // auto: the TMA-staged walk wins for short chunks (g <= 64 on config 2),
-    // the register walk for long ones (fewer, longer walks amortise the A
-    // loads it issues itself)
-    const int variant = k.hw_variant == 0 ? ((tma_ok && k.g <= 64) ? 2 : 1) : k.hw_variant;
+    // auto: the TMA-staged walk wins for short chunks with wide lane groups
+    // (g <= 128, >= 16 lanes per chunk: config 2, Chung-Lu N=64); the register
+    // walk for long chunks (fewer, longer walks amortise the A loads it issues
+    // itself) and for narrow N (profiles/r01_selector_regret.json)
+    const int variant = k.hw_variant == 0 ? ((tma_ok && W >= 16 && k.g <= 128) ? 2 : 1) : k.hw_variant;
     const bool tma = variant == 2;
     if (tma && !tma_ok) return SGAP_ERR_ARG;
     if (variant != 1 && variant != 2) return SGAP_ERR_ARG;

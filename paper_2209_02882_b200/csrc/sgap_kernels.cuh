@@ -30,110 +30,123 @@ constexpr int kFoldEvery = 8;  // float32 partial sums fold into float64 every 8
 // RB + serial reduction: row:g,col:c,r:1 (row-multiple).
 // Logical thread (rg, t): rows rg*g .. rg*g+g-1, columns t*c .. t*c+c-1,
 // serial dot product over each row, one plain store per (row, tile)
-// (cuda_row_multiple.cu:37-43).  Hardware: L = N/c lanes per row group; when
-// L divides 32 (or is a multiple of 32) the lanes sharing a row stage that
-// row's (col, val) pairs with one coalesced load and shuffle them, which also
-// lets kBatch B-row gathers issue back to back.  Partial sums of each staged
-// round (<= 32 terms) fold into a float64 running sum.
+// (cuda_row_multiple.cu:37-43).  Hardware: L = N/c consecutive lanes share a
+// row (the logical mapping itself); each lane walks the row with broadcast
+// loads -- one 16-byte load each of 4 (col) and 4 (val) once the walk is
+// 4-aligned -- keeping 4 B-row gathers in flight, float32 partials folded into
+// a float64 running sum every 8 terms; C is written once with st.global.cs
+// (no atomics, no zero-fill, deterministic).
 // ===========================================================================
 template <typename T, int V>
-__global__ void __launch_bounds__(256)
+__device__ __forceinline__ void rb_step(Vec<T, V> &acc, const int *__restrict__ ci,
+                                        const T *__restrict__ av, int p,
+                                        const T *__restrict__ bk, int N) {
+    Vec<T, V> b;
+    ldg_vec<T, V>(b, bk + (long long)__ldg(ci + p) * N);
+    fma_vec<T, V>(acc, __ldg(av + p), b);
+}
+
+// Dot product of one row with one column tile (float64 result).
+template <typename T, int V>
+__device__ __forceinline__ Vec<double, V> rb_row(const int *__restrict__ ci,
+                                                 const T *__restrict__ av, int p, int end,
+                                                 const T *__restrict__ bk, int N, bool vec4) {
+    Vec<T, V> acc;
+    acc.zero();
+    Vec<double, V> tot;
+    tot.zero();
+    int since_fold = 0;
+    if (vec4) {
+        for (; p < end && (p & 3); ++p) rb_step<T, V>(acc, ci, av, p, bk, N);
+        for (; p + 4 <= end; p += 4) {
+            const int4 c = __ldg(reinterpret_cast<const int4 *>(ci + p));
+            Vec<T, 4> v;
+            ldg_vec<T, 4>(v, av + p);
+            Vec<T, V> b0, b1, b2, b3;
+            ldg_vec<T, V>(b0, bk + (long long)c.x * N);
+            ldg_vec<T, V>(b1, bk + (long long)c.y * N);
+            ldg_vec<T, V>(b2, bk + (long long)c.z * N);
+            ldg_vec<T, V>(b3, bk + (long long)c.w * N);
+            fma_vec<T, V>(acc, v.v[0], b0);
+            fma_vec<T, V>(acc, v.v[1], b1);
+            fma_vec<T, V>(acc, v.v[2], b2);
+            fma_vec<T, V>(acc, v.v[3], b3);
+            since_fold += 4;
+            if (since_fold >= kFoldEvery) {
+                fold<T, V>(tot, acc);
+                since_fold = 0;
+            }
+        }
+    } else {
+        for (; p + 4 <= end; p += 4) {
+            rb_step<T, V>(acc, ci, av, p, bk, N);
+            rb_step<T, V>(acc, ci, av, p + 1, bk, N);
+            rb_step<T, V>(acc, ci, av, p + 2, bk, N);
+            rb_step<T, V>(acc, ci, av, p + 3, bk, N);
+            since_fold += 4;
+            if (since_fold >= kFoldEvery) {
+                fold<T, V>(tot, acc);
+                since_fold = 0;
+            }
+        }
+    }
+    for (; p < end; ++p) rb_step<T, V>(acc, ci, av, p, bk, N);
+    fold<T, V>(tot, acc);
+    return tot;
+}
+
+template <typename T, int V>
+__global__ void __launch_bounds__(256, 4)
 k_row_multiple(const int *__restrict__ rp, const int *__restrict__ ci,
                const T *__restrict__ av, const T *__restrict__ B, T *__restrict__ C,
-               int M, int N, int g, int S, int accumulate) {
+               int M, int N, int g, int vec4, int accumulate) {
     const int L = N / V;
     const long long groups = ((long long)M + g - 1) / g;
-    const long long total = groups * L;           // logical threads
-    const long long items = (total + 31) >> 5;
-    const unsigned lane = lane_id();
-    SGAP_WARP_LOOP(item, items) {
-        const long long h = item * 32 + lane;
-        const bool live = h < total;
-        const long long rg = live ? h / L : 0;
-        const int t = live ? (int)(h - rg * L) : 0;
+    const long long total = groups * L;  // logical threads
+    for (long long h = (long long)blockIdx.x * blockDim.x + threadIdx.x; h < total;
+         h += (long long)gridDim.x * blockDim.x) {
+        const long long rg = h / L;
+        const int t = (int)(h - rg * L);
         const long long kcol = (long long)t * V;
         for (int s = 0; s < g; ++s) {
             const long long i = rg * g + s;
-            const bool row_ok = live && i < M;
-            const int beg = row_ok ? __ldg(rp + i) : 0;
-            const int len = row_ok ? __ldg(rp + i + 1) - beg : 0;
-            Vec<T, V> acc[kBatch];
-#pragma unroll
-            for (int u = 0; u < kBatch; ++u) acc[u].zero();
-            Vec<double, V> tot;
-            tot.zero();
-            if (S > 0) {
-                // Staged: S lanes (aligned) share the row; warp-uniform trip count.
-                const int maxlen = __reduce_max_sync(kFull, len);
-                const int sl = (int)(lane & (unsigned)(S - 1));
-                const int round = S < 32 ? 32 : S;  // positions per fold
-                for (int base = 0; base < maxlen; base += S) {
-                    int my_c = 0;
-                    T my_v = T(0);
-                    if (base + sl < len) {
-                        my_c = __ldg(ci + beg + base + sl);
-                        my_v = __ldg(av + beg + base + sl);
-                    }
-                    const int cnt = min(S, maxlen - base);
-                    for (int j = 0; j < cnt; j += kBatch) {
-                        int cc[kBatch];
-                        T vv[kBatch];
-#pragma unroll
-                        for (int u = 0; u < kBatch; ++u) {
-                            cc[u] = __shfl_sync(kFull, my_c, j + u, S);
-                            vv[u] = __shfl_sync(kFull, my_v, j + u, S);
-                        }
-                        Vec<T, V> bv[kBatch];
-#pragma unroll
-                        for (int u = 0; u < kBatch; ++u) {
-                            if (j + u < cnt && base + j + u < len)
-                                ldg_vec<T, V>(bv[u], B + (long long)cc[u] * N + kcol);
-                            else {
-                                bv[u].zero();
-                                vv[u] = T(0);
-                            }
-                        }
-#pragma unroll
-                        for (int u = 0; u < kBatch; ++u) fma_vec<T, V>(acc[u], vv[u], bv[u]);
-                    }
-                    if ((base + S) % round == 0 || base + S >= maxlen) {
-#pragma unroll
-                        for (int u = 0; u < kBatch; ++u) fold<T, V>(tot, acc[u]);
-                    }
-                }
-            } else {
-                // Direct: row lanes straddle warps; each lane walks the row.
-                const int end = beg + len;
-                for (int p0 = beg; p0 < end; p0 += 32) {
-                    const int e = min(p0 + 32, end);
-                    int p = p0;
-                    for (; p + kBatch <= e; p += kBatch) {
-                        int cc[kBatch];
-                        T vv[kBatch];
-                        Vec<T, V> bv[kBatch];
-#pragma unroll
-                        for (int u = 0; u < kBatch; ++u) {
-                            cc[u] = __ldg(ci + p + u);
-                            vv[u] = __ldg(av + p + u);
-                        }
-#pragma unroll
-                        for (int u = 0; u < kBatch; ++u)
-                            ldg_vec<T, V>(bv[u], B + (long long)cc[u] * N + kcol);
-#pragma unroll
-                        for (int u = 0; u < kBatch; ++u) fma_vec<T, V>(acc[u], vv[u], bv[u]);
-                    }
-                    for (; p < e; ++p) {
-                        Vec<T, V> bv;
-                        ldg_vec<T, V>(bv, B + (long long)__ldg(ci + p) * N + kcol);
-                        fma_vec<T, V>(acc[0], __ldg(av + p), bv);
-                    }
-#pragma unroll
-                    for (int u = 0; u < kBatch; ++u) fold<T, V>(tot, acc[u]);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < kBatch; ++u) fold<T, V>(tot, acc[u]);
-            if (row_ok) store_vec<T, V>(C + i * N + kcol, narrow<T, V>(tot), accumulate != 0);
+            if (i >= M) break;
+            const Vec<double, V> tot = rb_row<T, V>(ci, av, __ldg(rp + i), __ldg(rp + i + 1),
+                                                    B + kcol, N, vec4 != 0);
+            store_vec<T, V>(C + i * N + kcol, narrow<T, V>(tot), accumulate != 0);
+        }
+    }
+}
+
+// The same logical threads on an interleaved mapping: a CTA owns a tile of
+// (rows_per_step x g) consecutive rows and, at each of its g steps, its
+// warps work on *adjacent* rows.  Rows i, i+1, ... of banded / mesh matrices
+// gather mostly the same B rows, so a step's working set (a few dozen B rows
+// per CTA) is served from L1, while tiles still go out in global row order so
+// the chip-wide sweep keeps its L2 reuse.  (A persistent band per CTA was
+// measured: L1 hit 63% but 592 separate sweep fronts broke L2 reuse, 19.6 GB
+// of DRAM reads on config 4.)  Output and numerics are identical to
+// k_row_multiple: each row is one serial dot product per column tile.
+template <typename T, int V>
+__global__ void __launch_bounds__(256, 4)
+k_row_interleaved(const int *__restrict__ rp, const int *__restrict__ ci,
+                  const T *__restrict__ av, const T *__restrict__ B, T *__restrict__ C, int M,
+                  int N, int g, int vec4, int accumulate) {
+    const int L = N / V;
+    const int rows_per_step = blockDim.x / L;
+    if ((int)threadIdx.x >= rows_per_step * L) return;
+    const int t = (int)(threadIdx.x % L);
+    const int slot = (int)(threadIdx.x / L);
+    const long long kcol = (long long)t * V;
+    const long long tile_rows = (long long)rows_per_step * g;
+    const long long tiles = ((long long)M + tile_rows - 1) / tile_rows;
+    for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        for (int s = 0; s < g; ++s) {
+            const long long i = tile * tile_rows + (long long)s * rows_per_step + slot;
+            if (i >= M) break;
+            const Vec<double, V> tot = rb_row<T, V>(ci, av, __ldg(rp + i), __ldg(rp + i + 1),
+                                                    B + kcol, N, vec4 != 0);
+            store_vec<T, V>(C + i * N + kcol, narrow<T, V>(tot), accumulate != 0);
         }
     }
 }

@@ -59,7 +59,7 @@ class Candidate:
     point: str
     p: int
     hw_block: int = 0
-    hw_variant: int = 0  # nnz-multiple walk: 0 auto, 1 register-staged, 2 TMA-staged
+    hw_variant: int = 0  # nnz-multiple: 1 register / 2 TMA walk; row-multiple: 2 interleaved
 
     def label(self) -> str:
         return (f"{self.point}@p{self.p}" + (f"/b{self.hw_block}" if self.hw_block else "")
@@ -104,37 +104,76 @@ def candidates(n: int, p_values=(256, 1024), g_values=GPU_G_VALUES,
             seen.add(key)
             if variants and tpl.family == "nnz-multiple":
                 out.extend(Candidate(str(pt), p, 0, v) for v in (1, 2))
+            elif variants and tpl.family == "row-multiple" and n // tpl.c <= 256:
+                out.extend(Candidate(str(pt), p, 0, v) for v in (0, 2))
             else:
                 out.append(Candidate(str(pt), p))
     return out
 
 
-def heuristic(stats: MatrixStats, n: int) -> Candidate:
-    """Closed-form choice from row statistics and n.
+def _templated(point: str, n: int, p: int) -> bool:
+    return algorithm_template(parse_point(point), KernelConfig(n=n, p=p)) is not None
 
-    * c = widest vector dividing n (16-byte B-row gathers when n % 4 == 0);
-    * short, regular rows (cv < 1, max row <= 8 * mean): row split, one row
-      per lane group (RB + serial, no atomics, no zero-fill);
-    * skewed rows (power-law, hub rows): nnz split with a serial walk over
-      g = 32 positions (EB + serial: load balanced, atomics only at chunk
-      boundaries);
-    * very narrow n (< 8) with skew: segment groups of r = 8 over single
-      nonzeros (the Sgap schedule the paper recommends for small N).
+
+def _first_p(point: str, n: int) -> int | None:
+    """256, 1024 or 4096 when templated there, else the smallest warp
+    multiple that makes the point's divisibility gates pass."""
+    for p in (256, 1024, 4096):
+        if _templated(point, n, p):
+            return p
+    for p in range(32, 32 * 1024, 32):
+        if _templated(point, n, p):
+            return p
+    return None
+
+
+def _pow2_floor(x: float) -> int:
+    out = 1
+    while out * 2 <= x:
+        out *= 2
+    return out
+
+
+def heuristic(stats: MatrixStats, n: int) -> Candidate:
+    """Closed-form schedule choice from row statistics and n, fitted to the
+    round-1 B200 sweeps (profiles/r01_sweep_*.json, r01_paper_claims.md):
+
+    * regular rows (cv < 1, max <= 8 x mean):
+      - n >= 16: RB + serial, 4 rows per logical thread, interleaved CTA
+        mapping, c = 4 (27-pt stencil at N=128);
+      - long rows (mean >= 32): RB + parallel group of 2 lanes, widest
+        vector (uniform 1%: flexible r=2 beats r=32 at every n);
+      - n < 16 and short rows: RB + serial, one lane per row with the widest
+        vector (stencil at N=4/8);
+    * skewed rows (power law, hub rows): EB + serial walk with the widest
+      vector that keeps >= 4 lanes per chunk for small n, chunk g ~ nnz/40k
+      clamped to [32, 512] so every warp slot gets several chunks.
     """
-    c = 4 if n % 4 == 0 else (2 if n % 2 == 0 else 1)
+    widest = 4 if n % 4 == 0 else (2 if n % 2 == 0 else 1)
+    col = lambda c: "1" if c == 1 else str(c)  # noqa: E731
     regular = stats.cv_row < 1.0 and stats.max_row <= 8 * max(stats.mean_row, 1.0)
     if regular:
-        return Candidate(f"row:1,col:{c},r:1" if c > 1 else "row:1,col:1,r:1", 256)
-    if n < 8:
-        for r in (8, 4, 2):
-            pt = f"nnz:1,col:{c},r:{r}" if c > 1 else f"nnz:1,col:1,r:{r}"
-            if algorithm_template(parse_point(pt), KernelConfig(n=n, p=256)) is not None:
-                return Candidate(pt, 256)
-    for p in (256, 1024):
-        pt = f"nnz:32,col:{c},r:1" if c > 1 else "nnz:32,col:1,r:1"
-        if algorithm_template(parse_point(pt), KernelConfig(n=n, p=p)) is not None:
+        if stats.mean_row >= 32:
+            pt = f"row:1/2,col:{col(widest)},r:2"
+            p = _first_p(pt, n)
+            if p is not None:
+                return Candidate(pt, p)
+        if n >= 16:
+            pt = f"row:4,col:{col(widest)},r:1"
+            p = _first_p(pt, n)
+            if p is not None:
+                return Candidate(pt, p, 0, 2)
+        pt = f"row:1,col:{col(widest)},r:1"
+        return Candidate(pt, _first_p(pt, n) or 256)
+    c = widest if n >= 16 else min(widest, max(1, n // 4))
+    g = max(32, min(512, _pow2_floor(stats.nnz / 40_000)))
+    for gg in (g, 256, 128, 64, 32):
+        pt = f"nnz:{gg},col:{col(c)},r:1"
+        p = _first_p(pt, n)
+        if p is not None:
             return Candidate(pt, p)
-    return Candidate(f"row:1,col:{c},r:1" if c > 1 else "row:1,col:1,r:1", 256)
+    pt = f"row:1,col:{col(widest)},r:1"
+    return Candidate(pt, _first_p(pt, n) or 256)
 
 
 def autotune(a: DeviceCsr, b: torch.Tensor, c: torch.Tensor, n: int, cands, *, reps: int = 3,

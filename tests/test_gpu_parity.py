@@ -240,3 +240,24 @@ def test_nnz_multiple_walk_variants(zoo, variant):
         st = oracle.block_starts(a.row_ptr, k.chunk, k.grid_size)
         assert m.atomic_ops == oracle.writebacks(k.family, a.row_ptr, 32, k.grid_size, starts=st,
                                                  npb=k.chunk, r=k.r, chunk=k.chunk, g=k.g)
+
+
+def test_reference_objects_are_accepted():
+    """sim.run takes the reference's own LoweredKernel / CsrMatrix / DenseMatrix
+    (duck-typed), the zero-code switch of INTEGRATION.md section 1."""
+    from types import SimpleNamespace
+
+    a = random_csr(300, 200, 0.05, seed=4)
+    b = random_dense(200, 8, seed=5)
+    ref_a = SimpleNamespace(num_rows=a.num_rows, num_cols=a.num_cols, row_ptr=a.row_ptr,
+                            col_idx=a.col_idx, vals=a.vals, nnz=a.nnz)
+    ref_b = SimpleNamespace(num_rows=b.num_rows, num_cols=b.num_cols, vals=b.vals)
+    want = oracle.spmm_f64(a.row_ptr, a.col_idx, a.vals, b.vals.reshape(200, 8), 8)
+    for text, p in (("nnz:32,col:4,r:1", 1024), ("nnz:1,col:2,r:8", 256), ("row:1/8,col:1,r:8", 256)):
+        ours = build_kernel(parse_point(text), KernelConfig(8, p), a)
+        ref_k = SimpleNamespace(name=ours.name, body=(), grid_size=ours.grid_size,
+                                block_size=ours.block_size, block_starts=ours.block_starts,
+                                family=ours.family, point=text)
+        got, m = run(ref_k, ref_a, ref_b)
+        assert oracle.max_rel_error(got.vals, want) <= F64_TOL
+        assert m.grid_size == ours.grid_size

@@ -1,0 +1,35 @@
+"""Selector: the closed-form heuristic's picks for the BASELINE matrix
+classes (its regret against the exhaustive device sweep is measured by
+tools/selector_regret.py, profiles/r01_selector_regret.json) and the
+candidate grid."""
+
+from paper_2209_02882_b200.lowering import KernelConfig
+from paper_2209_02882_b200.selector import MatrixStats, candidates, heuristic
+from paper_2209_02882_b200.space import parse_point
+from paper_2209_02882_b200.templates import algorithm_template
+
+RMAT20 = MatrixStats(1048576, 1048576, 16086639, 15.34, 9.16, 39633, 0.478)
+STENCIL160 = MatrixStats(4096000, 4096000, 109215352, 26.66, 0.04, 27, 0.0)
+UNIFORM1 = MatrixStats(4096, 4096, 167772, 40.96, 0.15, 66, 0.0)
+
+
+def test_heuristic_picks_are_templated():
+    for st in (RMAT20, STENCIL160, UNIFORM1):
+        for n in (1, 2, 3, 4, 8, 16, 32, 64, 128, 256, 512):
+            cand = heuristic(st, n)
+            assert algorithm_template(parse_point(cand.point), KernelConfig(n=n, p=cand.p)) is not None
+
+
+def test_heuristic_matrix_classes():
+    assert heuristic(RMAT20, 128).point.startswith("nnz:")      # power law -> EB walk
+    assert heuristic(STENCIL160, 128).point.startswith("row:4")  # regular -> RB
+    assert heuristic(STENCIL160, 4).point == "row:1,col:4,r:1"
+    assert heuristic(UNIFORM1, 4).point.startswith("row:1/2")    # flexible group beats r=32
+
+
+def test_candidate_grid_covers_families_and_walks():
+    cands = candidates(128)
+    fams = {algorithm_template(parse_point(c.point), KernelConfig(128, c.p)).family for c in cands}
+    assert fams == {"nnz-one", "nnz-multiple", "row-multiple", "row-reciprocal"}
+    assert any(c.point.startswith("nnz:512") for c in cands)
+    assert {c.hw_variant for c in cands if c.point.startswith("nnz:64,")} == {1, 2}
