@@ -79,3 +79,27 @@ def test_unpermuted_rmat_small_n():
     pts = [("nnz:1,col:4,r:32", 1024), ("nnz:1,col:1,r:1", 256), ("nnz:16,col:4,r:1", 256),
            ("row:1,col:4,r:1", 256), ("row:1/32,col:1,r:32", 256)]
     print(_check(g, 8, pts))
+
+
+def test_pipelined_host_spmm_matches_single_call():
+    from paper_2209_02882_b200.pipeline import HostSpmm
+    from paper_2209_02882_b200.selector import Candidate, plan_for
+
+    g = G.rmat(16, 16, seed=4, device="cuda")
+    a = _device(g)
+    n = 64
+    b = (torch.rand((a.num_cols, n), device="cuda") * 2 - 1)
+    h_rp, h_ci, h_v = (x.cpu().pin_memory() for x in (a.row_ptr, a.col_idx, a.vals))
+    h_b = b.cpu().pin_memory()
+    want = oracle.spmm_f64(h_rp.numpy(), h_ci.numpy(), h_v.numpy(), h_b.numpy(), n)
+    for point, p, blocks in (("nnz:128,col:4,r:1", 256, 5), ("row:1,col:4,r:1", 256, 3),
+                             ("nnz:1,col:4,r:8", 1024, 4)):
+        cand = Candidate(point, p)
+        pipe = HostSpmm(a.num_rows, a.num_cols, n, h_rp,
+                        lambda rows, rp: plan_for(cand, n, rows, a.num_cols, rp), blocks=blocks)
+        for _ in range(3):  # back-to-back calls exercise both buffer sets
+            h_c = torch.full((a.num_rows, n), float("nan")).pin_memory()
+            pipe(h_rp, h_ci, h_v, h_b, h_c)
+            pipe.wait()
+            torch.cuda.synchronize()
+            assert oracle.max_rel_error(h_c.numpy(), want) <= TOL, point
