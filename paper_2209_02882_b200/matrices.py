@@ -20,7 +20,16 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-__all__ = ["CsrMatrix", "DenseMatrix", "coo_to_csr", "random_csr", "random_dense"]
+__all__ = ["CsrMatrix", "DenseMatrix", "MatrixFormatError", "coo_to_csr", "load_matrix_market",
+           "loads_matrix_market", "random_csr", "random_dense"]
+
+
+class MatrixFormatError(ValueError):
+    """Malformed Matrix Market input; ``line`` is 1-based (matrices.py:28-36)."""
+
+    def __init__(self, message: str, line: int | None = None):
+        self.line = line
+        super().__init__(f"line {line}: {message}" if line is not None else message)
 
 
 def _check_csr(num_rows, num_cols, row_ptr, col_idx, vals):
@@ -147,6 +156,99 @@ def coo_to_csr(num_rows: int, num_cols: int, rows, cols, vals, *, check: bool = 
             object.__setattr__(m, name, value)
         return m
     return CsrMatrix(num_rows, num_cols, row_ptr, cols, vals)
+
+
+def _mm_header(lines):
+    """Validate banner + size line; returns (rows, cols, nnz, symmetric, first
+    entry line index) -- matrices.py:144-186 semantics and line numbers."""
+    if not lines:
+        raise MatrixFormatError("empty file", 1)
+    banner = lines[0].split()
+    if len(banner) < 5 or banner[0] != "%%MatrixMarket":
+        raise MatrixFormatError("expected '%%MatrixMarket' banner", 1)
+    obj, fmt, field, sym = (t.lower() for t in banner[1:5])
+    if obj != "matrix" or fmt != "coordinate":
+        raise MatrixFormatError(f"unsupported object/format '{obj} {fmt}'", 1)
+    if field != "real":
+        raise MatrixFormatError(f"unsupported field '{field}' (only real)", 1)
+    if sym not in ("general", "symmetric"):
+        raise MatrixFormatError(f"unsupported symmetry '{sym}'", 1)
+    idx = 1
+    while idx < len(lines) and (not lines[idx].strip() or lines[idx].lstrip().startswith("%")):
+        idx += 1
+    if idx >= len(lines):
+        raise MatrixFormatError("missing size line", idx + 1)
+    parts = lines[idx].split()
+    if len(parts) != 3:
+        raise MatrixFormatError("size line must be 'rows cols nnz'", idx + 1)
+    try:
+        rows, cols, nnz = (int(x) for x in parts)
+    except ValueError:
+        raise MatrixFormatError("size line must contain integers", idx + 1) from None
+    if rows < 0 or cols < 0 or nnz < 0:
+        raise MatrixFormatError("size values must be non-negative", idx + 1)
+    return rows, cols, nnz, sym == "symmetric", idx + 1
+
+
+def _mm_entries_checked(lines, start, rows, cols, nnz):
+    """Line-by-line entry validation, used to report the exact bad line."""
+    r_out, c_out, v_out = [], [], []
+    for ln in range(start, len(lines)):
+        text = lines[ln].strip()
+        if not text or text.startswith("%"):
+            continue
+        parts = text.split()
+        if len(parts) != 3:
+            raise MatrixFormatError("entry must be 'row col value'", ln + 1)
+        try:
+            r, c, v = int(parts[0]), int(parts[1]), float(parts[2])
+        except ValueError:
+            raise MatrixFormatError(f"non-numeric entry {parts!r}", ln + 1) from None
+        if not (1 <= r <= rows and 1 <= c <= cols):
+            raise MatrixFormatError(f"coordinate ({r}, {c}) outside {rows}x{cols}", ln + 1)
+        r_out.append(r - 1)
+        c_out.append(c - 1)
+        v_out.append(v)
+        if len(r_out) > nnz:
+            raise MatrixFormatError("more entries than declared", ln + 1)
+    if len(r_out) != nnz:
+        raise MatrixFormatError(f"declared {nnz} entries but found {len(r_out)}", len(lines) + 1)
+    return np.array(r_out, np.int64), np.array(c_out, np.int64), np.array(v_out, np.float64)
+
+
+def loads_matrix_market(text: str) -> CsrMatrix:
+    """Coordinate Matrix Market (real, general|symmetric) -> CSR, duplicates
+    summed, symmetric off-diagonals mirrored (matrices.py:144-212).  Entry
+    lines are converted with one vectorised numpy pass; any malformed input
+    falls back to the line-by-line check for the exact error line."""
+    lines = text.splitlines()
+    rows, cols, nnz, symmetric, start = _mm_header(lines)
+    body = [ln for ln in lines[start:] if ln.strip() and not ln.lstrip().startswith("%")]
+    try:
+        tok = np.array(" ".join(body).split(), dtype=object)
+        if tok.size != 3 * nnz:
+            raise ValueError
+        tok = tok.reshape(-1, 3)
+        r = tok[:, 0].astype(np.int64) - 1
+        c = tok[:, 1].astype(np.int64) - 1
+        v = tok[:, 2].astype(np.float64)
+        if nnz and (r.min() < 0 or r.max() >= rows or c.min() < 0 or c.max() >= cols):
+            raise ValueError
+    except (ValueError, TypeError):
+        r, c, v = _mm_entries_checked(lines, start, rows, cols, nnz)
+    if symmetric:
+        off = r != c
+        # mirrored entry follows its source, as the reference appends it
+        order = np.argsort(np.concatenate([np.arange(r.size) * 2, np.flatnonzero(off) * 2 + 1]),
+                           kind="stable")
+        r, c, v = (np.concatenate([x, y])[order] for x, y in ((r, c[off]), (c, r[off]), (v, v[off])))
+    return coo_to_csr(rows, cols, r, c, v)
+
+
+def load_matrix_market(path) -> CsrMatrix:
+    from pathlib import Path
+
+    return loads_matrix_market(Path(path).read_text())
 
 
 def random_csr(num_rows: int, num_cols: int, density: float, seed: int) -> CsrMatrix:
