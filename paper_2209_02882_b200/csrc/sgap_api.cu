@@ -176,8 +176,10 @@ int launch_nnz_multiple(bool tma, int tile, int owner, const sgap_kernel_t &k,
 // hw_variant: 0 auto; 1 register walk; 2 TMA-staged walk.  Measured on config
 // 2 (profiles/): software pipelining and 8-deep batches were slower (the extra
 // registers cost more occupancy than the added in-flight gathers recover), as
-// were L2 evict-first hints on the A stream; the TMA walk needs 3 CTAs/SM
-// (3-stage ring, <= 75 registers) to beat the register walk.
+// were L2 evict-first hints on the A stream, L1::no_allocate / evict_last on
+// the B gathers, and per-lane cp.async (LDGSTS) gathers into a 4-stage shared
+// ring (1.21 vs 0.77 ms); the TMA walk needs 3 CTAs/SM (3-stage ring, <= 75
+// registers) to beat the register walk.
 template <typename T, int V, int W>
 int run_nnz_multiple_w(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
                        const int *rowid, const LongRows &lr, int owner, unsigned long long *wb,
