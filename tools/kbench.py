@@ -25,6 +25,7 @@ ap.add_argument("--all", action="store_true")
 ap.add_argument("--check", action="store_true")
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--out", default="")
+ap.add_argument("--cusparse", action="store_true")
 args = ap.parse_args()
 dev = torch.device("cuda", 0)
 n = args.n or bench.default_n(args.config)
@@ -67,3 +68,23 @@ if args.check:
         print(f"check {cd.label():32s} max_rel_error {err:.3e}", "OK" if err <= 1e-5 else "FAIL")
 if args.out:
     Path(args.out).write_text(json.dumps({"workload": desc, "n": n, "rows": rows}, indent=1))
+
+if "--cusparse" in sys.argv[1:] or True:
+    # library sanity check: cuSPARSE SpMM through torch.sparse on
+    # the same device operands -- a reference point, not part of the product
+    try:
+        sp = torch.sparse_csr_tensor(a.row_ptr.to(torch.int64), a.col_idx.to(torch.int64), a.vals,
+                                     size=(a.num_rows, a.num_cols))
+        out = torch.sparse.mm(sp, b)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        best = float("inf")
+        for _ in range(args.reps):
+            e0.record()
+            out = torch.sparse.mm(sp, b)
+            e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        print(f"{'cuSPARSE (torch.sparse.mm, CSR f32)':32s} {best:8.3f} ms {2.0 * a.nnz * n / (best * 1e6):9.1f} GF/s")
+    except Exception as e:  # pragma: no cover
+        print("cuSPARSE comparison unavailable:", e)
