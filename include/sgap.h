@@ -150,6 +150,8 @@ typedef struct {
     double *d_long_acc;
     int64_t long_capacity;
     int64_t long_threshold;
+    int32_t has_exact_rows;   /* any row longer than sgap_exact_row_length()?
+                                 (0 lets sgap_run skip the error-free pass)  */
 } sgap_aux_t;
 
 /* Per-position row ids (what the reference lowering recovers per lane with
@@ -158,6 +160,11 @@ typedef struct {
  * than long_threshold (pass -1 for none).                                  */
 int sgap_row_ids(const int32_t *d_row_ptr, int64_t num_rows, int64_t nnz,
                  int64_t long_threshold, int32_t *d_rowid, void *stream);
+
+/* Rows longer than this (and in the long-row table) are accumulated with an
+ * error-free transform (TwoProduct + TwoSum): float32 product rounding alone
+ * would reach ~1e-5 of the reference metric beyond ~2e5 nonzeros.           */
+int64_t sgap_exact_row_length(void);
 
 /* Threshold the engine uses for a kernel (-1: no table needed: row families
  * keep float64 running sums, float64 values accumulate in float64).        */

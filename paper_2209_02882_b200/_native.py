@@ -42,6 +42,7 @@ EXPORTED = (
     "sgap_build_kernel",
     "sgap_block_starts",
     "sgap_row_ids",
+    "sgap_exact_row_length",
     "sgap_long_row_threshold",
     "sgap_long_row_capacity",
     "sgap_long_rows_tmp_bytes",
@@ -111,6 +112,7 @@ class Aux(ctypes.Structure):
         ("d_long_acc", ctypes.c_void_p),
         ("long_capacity", ctypes.c_int64),
         ("long_threshold", ctypes.c_int64),
+        ("has_exact_rows", ctypes.c_int32),
     ]
 
 
@@ -143,6 +145,8 @@ def lib():
     L.sgap_block_starts.restype = ctypes.c_int
     L.sgap_row_ids.argtypes = [vp, i64, i64, i64, vp, vp]
     L.sgap_row_ids.restype = ctypes.c_int
+    L.sgap_exact_row_length.argtypes = []
+    L.sgap_exact_row_length.restype = i64
     L.sgap_long_row_threshold.argtypes = [ctypes.POINTER(Kernel), i32]
     L.sgap_long_row_threshold.restype = i64
     L.sgap_long_row_capacity.argtypes = [i64, i64]

@@ -14,6 +14,8 @@
 
 using namespace sgap;
 
+extern "C" int64_t sgap_long_row_capacity(int64_t nnz, int64_t threshold);
+
 namespace {
 
 constexpr int kHwBlock = 256;
@@ -182,8 +184,8 @@ int launch_nnz_multiple(bool tma, int tile, int owner, const sgap_kernel_t &k,
 // registers) to beat the register walk.
 template <typename T, int V, int W>
 int run_nnz_multiple_w(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
-                       const int *rowid, const LongRows &lr, int owner, unsigned long long *wb,
-                       cudaStream_t st) {
+                       const int *rowid, const LongRows &lr, int owner, bool has_exact,
+                       unsigned long long *wb, cudaStream_t st) {
     const int tile = tma_tile_for(k.g);
     const bool tma_ok = tile > 0 && aligned(rowid, 16) && aligned(a.d_col_idx, 16) &&
                         aligned(a.d_vals, 16);
@@ -195,13 +197,26 @@ int run_nnz_multiple_w(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, 
     const bool tma = variant == 2;
     if (tma && !tma_ok) return SGAP_ERR_ARG;
     if (variant != 1 && variant != 2) return SGAP_ERR_ARG;
-    return launch_nnz_multiple<T, V, W, 4, false>(tma, tile, owner, k, a, B, C, rowid, lr, wb, st);
+    const int status =
+        launch_nnz_multiple<T, V, W, 4, false>(tma, tile, owner, k, a, B, C, rowid, lr, wb, st);
+    if (status != SGAP_OK || lr.threshold < 0 || sizeof(T) != 4 || !has_exact) return status;
+    // chunks inside long rows: error-free accumulate in their own kernel
+    const long long total_pos = k.grid_size * k.chunk;
+    const int vec4 = (k.g % 4 == 0) && aligned(rowid, 16) && aligned(a.d_col_idx, 16) &&
+                     aligned(a.d_vals, 16);
+    (void)total_pos;
+    const long long cap = sgap_long_row_capacity(a.nnz, lr.threshold);
+    const dim3 grid((unsigned)(cap < 1024 ? (cap > 0 ? cap : 1) : 1024), 64);
+    k_nnz_multiple_exact<T, V><<<grid, kHwBlock, 0, st>>>(
+        rowid, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, a.d_row_ptr, k.n, a.nnz, k.g,
+        vec4, lr);
+    return launch_status();
 }
 
 template <typename T, int V>
 int run_nnz_multiple(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
-                     const int *rowid, const LongRows &lr, int acc, unsigned long long *wb,
-                     cudaStream_t st) {
+                     const int *rowid, const LongRows &lr, int acc, bool has_exact,
+                     unsigned long long *wb, cudaStream_t st) {
     // overwrite mode: zero only rows that will receive atomic flushes (or no
     // flush at all), then let the walk store complete rows outright
     const int owner = acc ? 0 : 1;
@@ -210,37 +225,40 @@ int run_nnz_multiple(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T 
             a.d_row_ptr, (int)a.num_rows, k.n, k.g, lr.threshold, C);
     }
     switch (pow2_floor(k.n / V)) {
-        case 1: return run_nnz_multiple_w<T, V, 1>(k, a, B, C, rowid, lr, owner, wb, st);
-        case 2: return run_nnz_multiple_w<T, V, 2>(k, a, B, C, rowid, lr, owner, wb, st);
-        case 4: return run_nnz_multiple_w<T, V, 4>(k, a, B, C, rowid, lr, owner, wb, st);
-        case 8: return run_nnz_multiple_w<T, V, 8>(k, a, B, C, rowid, lr, owner, wb, st);
-        case 16: return run_nnz_multiple_w<T, V, 16>(k, a, B, C, rowid, lr, owner, wb, st);
-        default: return run_nnz_multiple_w<T, V, 32>(k, a, B, C, rowid, lr, owner, wb, st);
+        case 1: return run_nnz_multiple_w<T, V, 1>(k, a, B, C, rowid, lr, owner, has_exact, wb, st);
+        case 2: return run_nnz_multiple_w<T, V, 2>(k, a, B, C, rowid, lr, owner, has_exact, wb, st);
+        case 4: return run_nnz_multiple_w<T, V, 4>(k, a, B, C, rowid, lr, owner, has_exact, wb, st);
+        case 8: return run_nnz_multiple_w<T, V, 8>(k, a, B, C, rowid, lr, owner, has_exact, wb, st);
+        case 16: return run_nnz_multiple_w<T, V, 16>(k, a, B, C, rowid, lr, owner, has_exact, wb, st);
+        default: return run_nnz_multiple_w<T, V, 32>(k, a, B, C, rowid, lr, owner, has_exact, wb, st);
     }
 }
 
 template <typename T, int V>
 int run_family(const sgap_kernel_t &k, const sgap_csr_t &a, const void *b, void *c, int acc,
-               const int *rowid, const LongRows &lr, unsigned long long *wb, cudaStream_t st) {
+               const int *rowid, const LongRows &lr, bool has_exact, unsigned long long *wb,
+               cudaStream_t st) {
     const T *B = static_cast<const T *>(b);
     T *C = static_cast<T *>(c);
     switch (k.family) {
         case SGAP_ROW_MULTIPLE: return run_row_multiple<T, V>(k, a, B, C, acc, st);
         case SGAP_ROW_RECIPROCAL: return run_row_reciprocal<T, V>(k, a, B, C, acc, wb, st);
         case SGAP_NNZ_ONE: return run_nnz_one<T, V>(k, a, B, C, rowid, lr, wb, st);
-        case SGAP_NNZ_MULTIPLE: return run_nnz_multiple<T, V>(k, a, B, C, rowid, lr, acc, wb, st);
+        case SGAP_NNZ_MULTIPLE:
+            return run_nnz_multiple<T, V>(k, a, B, C, rowid, lr, acc, has_exact, wb, st);
         default: return SGAP_ERR_ARG;
     }
 }
 
 template <typename T>
 int run_typed(const sgap_kernel_t &k, const sgap_csr_t &a, const void *b, void *c, int acc,
-              const int *rowid, const LongRows &lr, unsigned long long *wb, cudaStream_t st) {
+              const int *rowid, const LongRows &lr, bool has_exact, unsigned long long *wb,
+              cudaStream_t st) {
     int status;
     switch (k.c) {
-        case 1: status = run_family<T, 1>(k, a, b, c, acc, rowid, lr, wb, st); break;
-        case 2: status = run_family<T, 2>(k, a, b, c, acc, rowid, lr, wb, st); break;
-        case 4: status = run_family<T, 4>(k, a, b, c, acc, rowid, lr, wb, st); break;
+        case 1: status = run_family<T, 1>(k, a, b, c, acc, rowid, lr, has_exact, wb, st); break;
+        case 2: status = run_family<T, 2>(k, a, b, c, acc, rowid, lr, has_exact, wb, st); break;
+        case 4: status = run_family<T, 4>(k, a, b, c, acc, rowid, lr, has_exact, wb, st); break;
         default: return SGAP_ERR_NO_TEMPLATE;
     }
     if (status != SGAP_OK || lr.threshold < 0) return status;
@@ -418,6 +436,8 @@ int64_t sgap_long_row_threshold(const sgap_kernel_t *k, int32_t dtype) {
     return t < 128 ? 128 : t;
 }
 
+int64_t sgap_exact_row_length(void) { return kExactRow; }
+
 int64_t sgap_long_row_capacity(int64_t nnz, int64_t threshold) {
     if (threshold < 0) return 0;
     return nnz / (threshold + 1) + 1;
@@ -492,6 +512,7 @@ int sgap_run(const sgap_kernel_t *k, const sgap_csr_t *a, const void *d_b, void 
     if (eb && k->grid_size > 0 && a->nnz > 0 && rowid == nullptr) return SGAP_ERR_ARG;
     if (k->family == SGAP_NNZ_MULTIPLE && (k->g < 1 || k->chunk % k->g)) return SGAP_ERR_CONFIG;
     LongRows lr{nullptr, nullptr, nullptr, -1};
+    const bool has_exact = aux != nullptr && aux->has_exact_rows != 0;
     if (eb && aux && aux->long_threshold >= 0 && dtype == SGAP_F32) {
         if (aux->d_long_rows == nullptr || aux->d_long_count == nullptr || aux->d_long_acc == nullptr)
             return SGAP_ERR_ARG;
@@ -511,8 +532,9 @@ int sgap_run(const sgap_kernel_t *k, const sgap_csr_t *a, const void *d_b, void 
         return SGAP_OK;
     }
     if (dtype == SGAP_F32)
-        return run_typed<float>(*k, *a, d_b, d_c, accumulate, rowid, lr, d_writebacks, st);
-    return run_typed<double>(*k, *a, d_b, d_c, accumulate, rowid, lr, d_writebacks, st);
+        return run_typed<float>(*k, *a, d_b, d_c, accumulate, rowid, lr, has_exact, d_writebacks,
+                                st);
+    return run_typed<double>(*k, *a, d_b, d_c, accumulate, rowid, lr, has_exact, d_writebacks, st);
 }
 
 int sgap_reference_spmm_f64(const sgap_csr_t *a, const void *d_b, int32_t n, int32_t dtype,

@@ -130,6 +130,42 @@ __device__ __forceinline__ void fold(Vec<double, V> &tot, Vec<T, V> &acc) {
     }
 }
 
+// Error-free accumulate for rows long enough that float32 product rounding
+// itself would show (config 5's 239k-nonzero hub row: 2^-24 * sqrt(n) * |ab|
+// ~ 1.5e-5 where a column sum cancels to ~0).  TwoProduct (the FMA returns
+// the exact rounding error of a*b) + TwoSum into (hi, lo); the _rn
+// intrinsics keep the compiler from contracting the error terms away.
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+
+template <typename T, int V>
+__device__ __forceinline__ void fma_vec_exact(Vec<T, V> &hi, Vec<T, V> &lo, T a, const Vec<T, V> &b) {
+#pragma unroll
+    for (int x = 0; x < V; ++x) {
+        const T p = mul_rn(a, b.v[x]);
+        const T e = fma(a, b.v[x], -p);  // exact: a*b == p + e
+        const T s = add_rn(hi.v[x], p);
+        const T bb = sub_rn(s, hi.v[x]);
+        const T err = add_rn(sub_rn(hi.v[x], sub_rn(s, bb)), sub_rn(p, bb));
+        hi.v[x] = s;
+        lo.v[x] = add_rn(lo.v[x], add_rn(err, e));
+    }
+}
+
+template <typename T, int V>
+__device__ __forceinline__ void fold2(Vec<double, V> &tot, Vec<T, V> &hi, Vec<T, V> &lo) {
+#pragma unroll
+    for (int x = 0; x < V; ++x) {
+        tot.v[x] += (double)hi.v[x] + (double)lo.v[x];
+        hi.v[x] = T(0);
+        lo.v[x] = T(0);
+    }
+}
+
 template <typename T, int V>
 __device__ __forceinline__ Vec<T, V> narrow(const Vec<double, V> &tot) {
     Vec<T, V> o;
@@ -148,9 +184,14 @@ struct LongRows {
     long long threshold;  // < 0: side table disabled (float64 values, RB families)
 };
 
-// Row ids carry bit 31 when the row belongs to the long-row table.
+// Row ids carry bit 31 when the row belongs to the long-row table and bit 30
+// when it is long enough for float32 product rounding to matter (kExactRow).
 constexpr int kLongFlag = (int)0x80000000u;
-constexpr int kRowMask = 0x7fffffff;
+constexpr int kExactFlag = 0x40000000;
+constexpr int kRowMask = 0x3fffffff;
+// sqrt(n) * rms(a*b) * 2^-24 reaches ~1e-5 near n ~ 2e5 for U[-1,1) data;
+// rows beyond this take the error-free accumulate (TwoProduct + TwoSum).
+constexpr int kExactRow = 65536;
 
 // One atomic writeback of a (row, column tile) partial; `rid` is a row id
 // (possibly flagged long).

@@ -47,17 +47,28 @@ __device__ __forceinline__ void rb_step(Vec<T, V> &acc, const int *__restrict__ 
 }
 
 // Dot product of one row with one column tile (float64 result).
-template <typename T, int V>
-__device__ __forceinline__ Vec<double, V> rb_row(const int *__restrict__ ci,
-                                                 const T *__restrict__ av, int p, int end,
-                                                 const T *__restrict__ bk, int N, bool vec4) {
-    Vec<T, V> acc;
+template <typename T, int V, bool EXACT>
+__device__ __forceinline__ Vec<double, V> rb_row_impl(const int *__restrict__ ci,
+                                                      const T *__restrict__ av, int p, int end,
+                                                      const T *__restrict__ bk, int N,
+                                                      bool vec4) {
+    Vec<T, V> acc, lo;
     acc.zero();
+    lo.zero();
     Vec<double, V> tot;
     tot.zero();
     int since_fold = 0;
+    auto step = [&](T a, const Vec<T, V> &b) {
+        if constexpr (EXACT) fma_vec_exact<T, V>(acc, lo, a, b);
+        else fma_vec<T, V>(acc, a, b);
+    };
+    auto one = [&](int q) {
+        Vec<T, V> b;
+        ldg_vec<T, V>(b, bk + (long long)__ldg(ci + q) * N);
+        step(__ldg(av + q), b);
+    };
     if (vec4) {
-        for (; p < end && (p & 3); ++p) rb_step<T, V>(acc, ci, av, p, bk, N);
+        for (; p < end && (p & 3); ++p) one(p);
         for (; p + 4 <= end; p += 4) {
             const int4 c = __ldg(reinterpret_cast<const int4 *>(ci + p));
             Vec<T, 4> v;
@@ -67,32 +78,41 @@ __device__ __forceinline__ Vec<double, V> rb_row(const int *__restrict__ ci,
             ldg_vec<T, V>(b1, bk + (long long)c.y * N);
             ldg_vec<T, V>(b2, bk + (long long)c.z * N);
             ldg_vec<T, V>(b3, bk + (long long)c.w * N);
-            fma_vec<T, V>(acc, v.v[0], b0);
-            fma_vec<T, V>(acc, v.v[1], b1);
-            fma_vec<T, V>(acc, v.v[2], b2);
-            fma_vec<T, V>(acc, v.v[3], b3);
+            step(v.v[0], b0);
+            step(v.v[1], b1);
+            step(v.v[2], b2);
+            step(v.v[3], b3);
             since_fold += 4;
             if (since_fold >= kFoldEvery) {
-                fold<T, V>(tot, acc);
+                fold2<T, V>(tot, acc, lo);
                 since_fold = 0;
             }
         }
     } else {
         for (; p + 4 <= end; p += 4) {
-            rb_step<T, V>(acc, ci, av, p, bk, N);
-            rb_step<T, V>(acc, ci, av, p + 1, bk, N);
-            rb_step<T, V>(acc, ci, av, p + 2, bk, N);
-            rb_step<T, V>(acc, ci, av, p + 3, bk, N);
+            one(p);
+            one(p + 1);
+            one(p + 2);
+            one(p + 3);
             since_fold += 4;
             if (since_fold >= kFoldEvery) {
-                fold<T, V>(tot, acc);
+                fold2<T, V>(tot, acc, lo);
                 since_fold = 0;
             }
         }
     }
-    for (; p < end; ++p) rb_step<T, V>(acc, ci, av, p, bk, N);
-    fold<T, V>(tot, acc);
+    for (; p < end; ++p) one(p);
+    fold2<T, V>(tot, acc, lo);
     return tot;
+}
+
+template <typename T, int V>
+__device__ __forceinline__ Vec<double, V> rb_row(const int *__restrict__ ci,
+                                                 const T *__restrict__ av, int p, int end,
+                                                 const T *__restrict__ bk, int N, bool vec4) {
+    if (sizeof(T) == 4 && end - p > kExactRow)
+        return rb_row_impl<T, V, true>(ci, av, p, end, bk, N, vec4);
+    return rb_row_impl<T, V, false>(ci, av, p, end, bk, N, vec4);
 }
 
 template <typename T, int V>
@@ -437,6 +457,55 @@ __device__ __forceinline__ void eb_walk4(const ASrc &A, long long q0, long long 
     nwb += V;
 }
 
+// A chunk lying entirely inside one long row (flagged in its row id): the
+// error-free accumulate (TwoProduct + TwoSum, float64 folds), no row changes.
+// Only rows flagged kExactFlag (> kExactRow nonzeros).  These chunks run in their own kernel (k_nnz_multiple_exact) so the hot walk
+// keeps its register budget; chunks that straddle a long row's ends use the
+// fast walk -- at most two per row, too few terms for their float32 rounding
+// to matter.
+template <typename T, int V, class ASrc>
+__device__ __forceinline__ void eb_walk4_exact(const ASrc &A, long long q0, long long qend,
+                                            const T *__restrict__ B, int N, long long kcol,
+                                            T *__restrict__ C, const LongRows &lr,
+                                            unsigned long long &nwb) {
+    const int cur = A.row(q0);
+    Vec<T, V> hi, lo;
+    hi.zero();
+    lo.zero();
+    Vec<double, V> tot;
+    tot.zero();
+    const T *bk = B + kcol;
+    long long q = q0;
+    int since_fold = 0;
+    for (; q + 4 <= qend; q += 4) {
+        int4 c, r;
+        Vec<T, 4> v;
+        A.load4(q, c, v, r);
+        Vec<T, V> b0, b1, b2, b3;
+        ldg_vec<T, V>(b0, bk + (long long)c.x * N);
+        ldg_vec<T, V>(b1, bk + (long long)c.y * N);
+        ldg_vec<T, V>(b2, bk + (long long)c.z * N);
+        ldg_vec<T, V>(b3, bk + (long long)c.w * N);
+        fma_vec_exact<T, V>(hi, lo, v.v[0], b0);
+        fma_vec_exact<T, V>(hi, lo, v.v[1], b1);
+        fma_vec_exact<T, V>(hi, lo, v.v[2], b2);
+        fma_vec_exact<T, V>(hi, lo, v.v[3], b3);
+        since_fold += 4;
+        if (since_fold >= kFoldEvery) {
+            fold2<T, V>(tot, hi, lo);
+            since_fold = 0;
+        }
+    }
+    for (; q < qend; ++q) {
+        Vec<T, V> b;
+        ldg_vec<T, V>(b, bk + (long long)A.col(q) * N);
+        fma_vec_exact<T, V>(hi, lo, A.val(q), b);
+    }
+    fold2<T, V>(tot, hi, lo);
+    flush_row<T, V>(C, N, cur, kcol, tot, lr);  // long rows always go to the float64 table
+    nwb += V;
+}
+
 template <typename T, int V, int U>
 struct WalkBatch {
     int c[U], r[U];
@@ -548,6 +617,11 @@ k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
                 continue;
             }
             const Owner own{rp, base, end, owner != 0};
+            const int r_first = A.row(base);
+            if ((r_first & kExactFlag) && A.row(end - 1) == r_first) {  // the exact kernel's
+                nwb += V;
+                continue;
+            }
             if (VEC4)
                 eb_walk4<T, V>(A, base, end, B, N, (long long)tile * V, C, lr, own, nwb);
             else
@@ -555,6 +629,67 @@ k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
         }
     }
     flush_count(wb, nwb);
+}
+
+// The chunks of nnz-multiple that lie entirely inside one exact-flagged row
+// (> kExactRow nonzeros), walked with the error-free accumulate (see
+// eb_walk4_exact).  Work comes from the long-row list: blockIdx.x picks a long
+// row, blockIdx.y x warps split that row's contained chunks into 32-position
+// pieces (a 239k-nonzero hub row becomes ~7.5k warp items instead of one
+// serial walk).  Each piece flushes into the float64 long-row table (an
+// order-free sum); the main kernel counts the writebacks and skips exactly
+// these chunks (row id of first == last position, exact flag set).
+template <typename T, int V>
+__global__ void __launch_bounds__(256, 4)
+k_nnz_multiple_exact(const int *__restrict__ rowid, const int *__restrict__ ci,
+                     const T *__restrict__ av, const T *__restrict__ B, T *__restrict__ C,
+                     const int *__restrict__ rp, int N, long long nnz, int g, int vec4,
+                     LongRows lr) {
+    const int NT = N / V;
+    const int count = *lr.count;
+    const unsigned lane = lane_id();
+    const int warp = (int)(threadIdx.x >> 5);
+    const int nwarps = (int)(blockDim.x >> 5);
+    const long long per_chunk = ((long long)g + 31) >> 5;
+    const GlobalA<T> A{rowid, ci, av};
+    unsigned long long unused = 0;
+    for (int li = blockIdx.x; li < count; li += gridDim.x) {
+        const int r = __ldg(lr.rows + li);
+        const long long rs = __ldg(rp + r), re = __ldg(rp + r + 1);
+        if (re - rs <= kExactRow) continue;
+        const long long c0 = (rs + g - 1) / g;
+        long long c1 = re / g;                        // chunks ending at (c+1)g <= re
+        if (re == nnz && nnz % g) c1 = nnz / g + 1;   // ... and the final partial chunk
+        if (c1 <= c0) continue;
+        const long long items = (c1 - c0) * per_chunk;
+        for (long long it = (long long)blockIdx.y * nwarps + warp; it < items;
+             it += (long long)gridDim.y * nwarps) {
+            const long long cb = (c0 + it / per_chunk) * g;
+            const long long ce = min(cb + (long long)g, nnz);
+            const long long q0 = cb + (it % per_chunk) * 32;
+            const long long q1 = min(q0 + 32, ce);
+            if (q0 >= q1) continue;
+            for (int tile = (int)lane; tile < NT; tile += 32) {
+                if (vec4) {
+                    eb_walk4_exact<T, V>(A, q0, q1, B, N, (long long)tile * V, C, lr, unused);
+                } else {
+                    Vec<T, V> hi, lo;
+                    hi.zero();
+                    lo.zero();
+                    Vec<double, V> tot;
+                    tot.zero();
+                    for (long long q = q0; q < q1; ++q) {
+                        Vec<T, V> b;
+                        ldg_vec<T, V>(b, B + (long long)A.col(q) * N + (long long)tile * V);
+                        fma_vec_exact<T, V>(hi, lo, A.val(q), b);
+                        if (((q - q0) & (kFoldEvery - 1)) == kFoldEvery - 1) fold2<T, V>(tot, hi, lo);
+                    }
+                    fold2<T, V>(tot, hi, lo);
+                    flush_row<T, V>(C, N, A.row(q0), (long long)tile * V, tot, lr);
+                }
+            }
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -658,6 +793,11 @@ k_nnz_multiple_tma(const int *__restrict__ rowid, const int *__restrict__ ci,
                         continue;
                     }
                     const Owner own{rp, p0 + q0, p0 + qend, owner != 0};
+                    const int r_first = SA.row(q0);
+                    if ((r_first & kExactFlag) && SA.row(qend - 1) == r_first) {  // exact kernel's
+                        nwb += V;
+                        continue;
+                    }
                     if (VEC4)
                         eb_walk4<T, V>(SA, q0, qend, B, N, (long long)tc * V, C, lr, own, nwb);
                     else
@@ -699,7 +839,8 @@ k_row_ids(const int *__restrict__ rp, int M, long long nnz, long long thr, int *
                 next = __ldg(rp + r + 1);
             }
             const bool is_long = thr >= 0 && next - start > thr;
-            out[p] = r | (is_long ? kLongFlag : 0);
+            const bool exact = is_long && next - start > kExactRow;
+            out[p] = r | (is_long ? kLongFlag : 0) | (exact ? kExactFlag : 0);
         }
     }
 }

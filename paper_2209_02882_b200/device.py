@@ -142,12 +142,13 @@ class KernelAux:
     long_acc: torch.Tensor | None = None
     long_capacity: int = 0
     long_threshold: int = -1
+    has_exact_rows: int = 0
 
     def view(self) -> _native.Aux:
         ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
         return _native.Aux(ptr(self.starts), ptr(self.rowid), ptr(self.long_rows),
                            ptr(self.long_count), ptr(self.long_acc), self.long_capacity,
-                           self.long_threshold)
+                           self.long_threshold, self.has_exact_rows)
 
     def nbytes(self) -> int:
         ts = (self.starts, self.rowid, self.long_rows, self.long_count, self.long_acc)
@@ -180,6 +181,9 @@ def prepare_aux(k: LoweredKernel, a: DeviceCsr, *, stream=None, long_rows: bool 
     if thr < 0:
         return aux
     cap = int(L.sgap_long_row_capacity(a.nnz, thr))
+    if a.num_rows:  # plan-time host sync: is the error-free pass needed at all?
+        longest = int((a.row_ptr[1:] - a.row_ptr[:-1]).max().item())
+        aux.has_exact_rows = int(longest > int(L.sgap_exact_row_length()))
     aux.long_threshold = thr
     aux.long_capacity = cap
     aux.long_rows = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
@@ -232,6 +236,8 @@ def launches_per_call(k: LoweredKernel, aux: KernelAux | None, *, accumulate: bo
         n += 1  # k_zero_shared_rows
     if aux is not None and aux.long_threshold >= 0 and k.family in ("nnz-one", "nnz-multiple"):
         n += 1  # k_long_rows_fold
+        if k.family == "nnz-multiple" and aux.has_exact_rows:
+            n += 1  # k_nnz_multiple_exact
     return n
 
 
