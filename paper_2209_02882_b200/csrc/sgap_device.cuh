@@ -60,6 +60,11 @@ __device__ __forceinline__ void ldg_vec<double, 4>(Vec<double, 4> &o, const doub
     o.v[0] = t0.x; o.v[1] = t0.y; o.v[2] = t1.x; o.v[3] = t1.y;
 }
 
+// Software prefetch of a streamed A line into L1 (non-blocking, no register).
+__device__ __forceinline__ void prefetch_l1(const void *p) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 // Plain (read-modify-)write of an exclusively owned C tile.  C is written
 // exactly once per kernel, so the store is marked evict-first (st.global.cs)
 // to keep L2 for the B rows that are re-gathered.

@@ -335,12 +335,19 @@ struct GlobalA {
         r = __ldg(reinterpret_cast<const int4 *>(rowid + q));
         ldg_vec<T, 4>(v, av + q);
     }
+    // pull the A lines `ahead` positions further into L1 (one per 32 positions)
+    __device__ __forceinline__ void prefetch(long long q) const {
+        prefetch_l1(ci + q);
+        prefetch_l1(rowid + q);
+        prefetch_l1(av + q);
+    }
 };
 
 template <typename T>
 struct SharedA {
     const int *sr, *sc;
     const T *sv;
+    __device__ __forceinline__ void prefetch(long long) const {}
     __device__ __forceinline__ int row(long long q) const { return sr[q]; }
     __device__ __forceinline__ int col(long long q) const { return sc[q]; }
     __device__ __forceinline__ T val(long long q) const { return sv[q]; }
@@ -401,6 +408,7 @@ __device__ __forceinline__ void eb_walk4(const ASrc &A, long long q0, long long 
     const T *bk = B + kcol;
     long long q = q0;
     for (; q + 4 <= qend; q += 4) {
+        if ((q & 31) == 0 && q + 64 < qend) A.prefetch(q + 64);  // A lines two ahead
         int4 c, r;
         Vec<T, 4> v;
         A.load4(q, c, v, r);
