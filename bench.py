@@ -287,7 +287,7 @@ def main():
         spmm(k, a, b, c, aux=aux, hw_block=choice.hw_block, hw_variant=choice.hw_variant,
              stream=stream)
 
-    for _ in range(max(args.warmup, 3 if args.warmup >= 3 else args.warmup)):
+    for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if world > 1:
