@@ -69,13 +69,22 @@ def parse_args():
 
 
 def dist_setup():
+    """One process per GPU over NCCL.  SGAP_BENCH_SHARE_GPU=1 (a test hook for
+    boxes with fewer GPUs than ranks) puts every rank on cuda:0 over gloo so
+    the multi-rank path -- shards, barriers, max-over-ranks -- can run on one
+    GPU; numbers from that mode are not scaling results."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("SGAP_BENCH_SHARE_GPU") == "1":
+            local = 0
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return rank, world, local
@@ -151,6 +160,15 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
 
 
+def host_threads() -> int:
+    """All cores this process may run on (torchrun sets OMP_NUM_THREADS=1 for
+    multi-rank jobs; the CPU baseline deliberately uses every core)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
 def measured_peak_hbm() -> tuple[float, str]:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -199,7 +217,7 @@ def run_reference(args, rank, world):
     ci = g.col_idx.cpu().numpy().astype(np.int32)
     vals = g.vals.cpu().numpy().astype(np.float32)
     b = dense_b(g.num_cols, n, args.seed, dev).cpu().numpy()
-    threads = oracle.max_threads()
+    threads = host_threads()
     # bounded sample: leading rows holding ~sample_nnz nonzeros per step
     sample_nnz = min(g.nnz, 4_000_000)
     r_end = int(np.searchsorted(rp, sample_nnz, side="left"))
@@ -369,7 +387,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         import oracle
-        threads = oracle.max_threads()
+        threads = host_threads()
         h_rp32 = rp_host.astype(np.int32)
         h_ci32 = a.col_idx.cpu().numpy()
         h_v32 = a.vals.cpu().numpy()
