@@ -375,9 +375,31 @@ struct SharedA {
 // and flushed atomically.  `base`/`end` are global positions of the chunk.
 struct Owner {
     const int *rp;
-    long long base, end;
+    const int *rowid;      // global row ids (for the row before the chunk)
+    long long base, end;   // global positions of the chunk
+    long long nnz;
+    int m;
     bool on;
 };
+
+// Owner-mode zero-fill of empty rows, done by the walk that passes them:
+// rows strictly between two consecutive nonzeros' rows are empty; the chunk
+// whose first row starts at its base also covers the gap after the previous
+// position's row (or the leading empty rows), the chunk holding the last
+// nonzero covers the trailing ones.  Each lane clears its own column tile.
+template <typename T, int V>
+__device__ __forceinline__ void zero_rows(T *__restrict__ C, int N, long long kcol, int r0, int r1) {
+    Vec<T, V> z;
+    z.zero();
+    for (int r = r0; r < r1; ++r) store_vec<T, V>(C + (long long)r * N + kcol, z, false);
+}
+
+template <typename T, int V>
+__device__ __forceinline__ void zero_gap_before(T *__restrict__ C, int N, long long kcol,
+                                                const Owner &own, int cur_row) {
+    const int prev = own.base > 0 ? (__ldg(own.rowid + own.base - 1) & kRowMask) : -1;
+    zero_rows<T, V>(C, N, kcol, prev + 1, cur_row);
+}
 
 template <typename T, int V>
 __device__ __forceinline__ void flush_owned(T *__restrict__ C, int N, int rid, long long kcol,
@@ -400,6 +422,7 @@ __device__ __forceinline__ void eb_walk4(const ASrc &A, long long q0, long long 
                                          unsigned long long &nwb) {
     int cur = A.row(q0);
     bool here = own.on && __ldg(own.rp + (cur & kRowMask)) == own.base;
+    if (here) zero_gap_before<T, V>(C, N, kcol, own, cur & kRowMask);
     Vec<T, V> acc;
     acc.zero();
     Vec<double, V> tot;
@@ -433,6 +456,7 @@ __device__ __forceinline__ void eb_walk4(const ASrc &A, long long q0, long long 
                     nwb += V;
                     tot.zero();
                     since_fold = 0;
+                    if (own.on) zero_rows<T, V>(C, N, kcol, (cur & kRowMask) + 1, rr[u] & kRowMask);
                     cur = rr[u];
                     here = own.on;
                 }
@@ -454,6 +478,7 @@ __device__ __forceinline__ void eb_walk4(const ASrc &A, long long q0, long long 
             flush_owned<T, V>(C, N, cur, kcol, tot, lr, here);
             nwb += V;
             tot.zero();
+            if (own.on) zero_rows<T, V>(C, N, kcol, (cur & kRowMask) + 1, rq & kRowMask);
             cur = rq;
             here = own.on;
         }
@@ -463,6 +488,7 @@ __device__ __forceinline__ void eb_walk4(const ASrc &A, long long q0, long long 
     const bool complete = here && __ldg(own.rp + (cur & kRowMask) + 1) == own.end;
     flush_owned<T, V>(C, N, cur, kcol, tot, lr, complete);
     nwb += V;
+    if (own.on && own.end == own.nnz) zero_rows<T, V>(C, N, kcol, (cur & kRowMask) + 1, own.m);
 }
 
 // A chunk lying entirely inside one long row (flagged in its row id): the
@@ -547,6 +573,7 @@ __device__ __forceinline__ void eb_walk(const ASrc &A, long long q0, long long q
     };
     int cur = A.row(q0);
     bool here = own.on && __ldg(own.rp + (cur & kRowMask)) == own.base;
+    if (here) zero_gap_before<T, V>(C, N, kcol, own, cur & kRowMask);
     Vec<T, V> acc;
     acc.zero();
     Vec<double, V> tot;
@@ -561,6 +588,7 @@ __device__ __forceinline__ void eb_walk(const ASrc &A, long long q0, long long q
                 nwb += V;
                 tot.zero();
                 since_fold = 0;
+                if (own.on) zero_rows<T, V>(C, N, kcol, (cur & kRowMask) + 1, w.r[u] & kRowMask);
                 cur = w.r[u];
                 here = own.on;
             }
@@ -596,6 +624,7 @@ __device__ __forceinline__ void eb_walk(const ASrc &A, long long q0, long long q
     const bool complete = here && __ldg(own.rp + (cur & kRowMask) + 1) == own.end;
     flush_owned<T, V>(C, N, cur, kcol, tot, lr, complete);
     nwb += V;
+    if (own.on && own.end == own.nnz) zero_rows<T, V>(C, N, kcol, (cur & kRowMask) + 1, own.m);
 }
 
 template <typename T, int V, int W, int U, bool PIPE>
@@ -624,9 +653,13 @@ k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
                 nwb += V;
                 continue;
             }
-            const Owner own{rp, base, end, owner != 0};
+            const Owner own{rp, rowid, base, end, nnz, M, owner != 0};
             const int r_first = A.row(base);
             if ((r_first & kExactFlag) && A.row(end - 1) == r_first) {  // the exact kernel's
+                if (own.on && __ldg(rp + (r_first & kRowMask)) == base)
+                    zero_gap_before<T, V>(C, N, (long long)tile * V, own, r_first & kRowMask);
+                if (own.on && end == nnz)
+                    zero_rows<T, V>(C, N, (long long)tile * V, (r_first & kRowMask) + 1, M);
                 nwb += V;
                 continue;
             }
@@ -800,9 +833,13 @@ k_nnz_multiple_tma(const int *__restrict__ rowid, const int *__restrict__ ci,
                         nwb += V;
                         continue;
                     }
-                    const Owner own{rp, p0 + q0, p0 + qend, owner != 0};
+                    const Owner own{rp, rowid, p0 + q0, p0 + qend, nnz, M, owner != 0};
                     const int r_first = SA.row(q0);
                     if ((r_first & kExactFlag) && SA.row(qend - 1) == r_first) {  // exact kernel's
+                        if (own.on && __ldg(rp + (r_first & kRowMask)) == own.base)
+                            zero_gap_before<T, V>(C, N, (long long)tc * V, own, r_first & kRowMask);
+                        if (own.on && own.end == nnz)
+                            zero_rows<T, V>(C, N, (long long)tc * V, (r_first & kRowMask) + 1, M);
                         nwb += V;
                         continue;
                     }
@@ -869,10 +906,10 @@ k_long_rows_fold(T *__restrict__ C, int N, LongRows lr, int overwrite) {
     }
 }
 
-// Overwrite-mode zero-fill for the owner-write walk: zero only the C rows the
-// walk does not store outright -- empty rows and rows whose nonzeros span more
-// than one g-position chunk (those receive atomic flushes) -- except long rows,
-// which the side-table fold overwrites.  Lanes test one row each; the warp
+// Overwrite-mode zero-fill for the owner-write walk: zero only the rows whose
+// nonzeros span more than one g-position chunk (they receive atomic flushes),
+// except long rows, which the side-table fold overwrites; empty rows are
+// zeroed by the walk itself (zero_rows / zero_gap_before).  Lanes test one row each; the warp
 // then clears the flagged rows cooperatively with 16-byte stores.
 template <typename T>
 __global__ void __launch_bounds__(256)
@@ -886,7 +923,7 @@ k_zero_shared_rows(const int *__restrict__ rp, int M, int N, long long g, long l
         if (r < M) {
             const long long s = __ldg(rp + r), e = __ldg(rp + r + 1);
             const long long len = e - s;
-            need = len == 0 || (s / g != (e - 1) / g && !(thr >= 0 && len > thr));
+            need = len > 0 && s / g != (e - 1) / g && !(thr >= 0 && len > thr);
         }
         unsigned mask = __ballot_sync(kFull, need);
         while (mask) {

@@ -92,7 +92,20 @@ class DeviceCsr:
         return cls(int(a.num_rows), int(a.num_cols), up(rp, np.int32), up(ci, np.int32),
                    up(vals, np_dt))
 
+    def check(self) -> None:
+        for name in ("row_ptr", "col_idx", "vals"):
+            t = getattr(self, name)
+            if not t.is_cuda:
+                raise ValueError(f"DeviceCsr.{name} must be a CUDA tensor (got {t.device})")
+            if not t.is_contiguous():
+                raise ValueError(f"DeviceCsr.{name} must be contiguous")
+        if self.row_ptr.dtype != torch.int32 or self.col_idx.dtype != torch.int32:
+            raise ValueError("row_ptr and col_idx must be int32 on the device")
+        if self.row_ptr.numel() != self.num_rows + 1:
+            raise ValueError("row_ptr must have num_rows + 1 entries")
+
     def view(self) -> _native.Csr:
+        self.check()
         return _native.Csr(self.num_rows, self.num_cols, self.nnz, self.row_ptr.data_ptr(),
                            self.col_idx.data_ptr(), self.vals.data_ptr())
 
@@ -161,6 +174,7 @@ def prepare_aux(k: LoweredKernel, a: DeviceCsr, *, stream=None, long_rows: bool 
     ids (nnz families) and, for float32 values, the long-row table
     (include/sgap.h: sgap_block_starts, sgap_row_ids, sgap_prepare_long_rows)."""
     eb = k.family in ("nnz-one", "nnz-multiple")
+    a.check()
     starts = None
     if eb and k.grid_size > 0 and block_starts:
         starts = device_block_starts(a, k.chunk, k.grid_size, stream=stream)
@@ -211,6 +225,8 @@ def spmm(k: LoweredKernel, a: DeviceCsr, b: torch.Tensor, c: torch.Tensor, *,
     """
     if b.dtype != a.vals.dtype or c.dtype != a.vals.dtype:
         raise ValueError("A, B and C must share one value dtype")
+    if not (b.is_cuda and c.is_cuda):
+        raise ValueError("B and C must be CUDA tensors")
     if tuple(b.shape) != (a.num_cols, k.n) or tuple(c.shape) != (a.num_rows, k.n):
         raise ValueError(
             f"shape mismatch: A is {a.num_rows}x{a.num_cols}, B {tuple(b.shape)}, C {tuple(c.shape)}, n={k.n}")

@@ -136,3 +136,39 @@ def test_config5_rmat_scale24_sampled_rows():
     err = oracle.max_rel_error(got, want)
     assert err <= TOL, err
     print("config5 sampled rows", rows.size, "max_rel_error", err)
+
+
+def test_exact_rows_and_empty_row_gaps():
+    """Rows beyond the error-free threshold (> 65,536 nonzeros) next to empty
+    rows at the start, middle and end of the matrix: the owner-mode walk
+    zero-fills every empty row itself, including around chunks that the
+    exact-row kernel takes over."""
+    rng = np.random.default_rng(11)
+    m, k, n = 64, 100_000, 128
+    lens = np.zeros(m, dtype=np.int64)
+    lens[5] = 70_001      # exact row after 5 leading empty rows
+    lens[9:20] = rng.integers(1, 40, 11)
+    lens[30] = 66_000     # exact row followed by empty rows to the end
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    cols = np.concatenate([np.sort(rng.choice(k, size=L, replace=False)) for L in lens if L])
+    vals = rng.uniform(-1, 1, rp[-1])
+    import types
+    g = types.SimpleNamespace(num_rows=m, num_cols=k, row_ptr=torch.from_numpy(rp).cuda(),
+                              col_idx=torch.from_numpy(cols).cuda(),
+                              vals=torch.from_numpy(vals).cuda())
+    a = _device(g)
+    b = torch.rand((k, n), device="cuda") * 2 - 1
+    want = oracle.spmm_f64(a.row_ptr.cpu().numpy(), a.col_idx.cpu().numpy(), a.vals.cpu().numpy(),
+                           b.cpu().numpy(), n)
+    c = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    for text, p, variant in (("nnz:512,col:4,r:1", 256, 1), ("nnz:64,col:4,r:1", 1024, 2),
+                             ("nnz:32,col:4,r:1", 256, 1)):
+        tpl = algorithm_template(parse_point(text), KernelConfig(n=n, p=p))
+        kk = lower(tpl, _Rp(m, k, rp), compute_starts=False)
+        aux = prepare_aux(kk, a)
+        assert aux.has_exact_rows == 1
+        c.fill_(float("nan"))
+        spmm(kk, a, b, c, aux=aux, hw_variant=variant)
+        got = c.cpu().numpy()
+        assert not np.isnan(got).any(), text
+        assert oracle.max_rel_error(got, want) <= TOL, text
