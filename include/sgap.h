@@ -95,7 +95,9 @@ typedef struct {
     int32_t hw_block;       /* CTA size override: 0 = auto (256), else a warp
                                multiple in [32, 256]                        */
     int32_t hw_variant;     /* nnz-multiple walk: 0 auto, 1 register-staged,
-                               2 TMA-staged (cp.async.bulk + mbarrier ring)  */
+                               2 TMA-staged (cp.async.bulk + mbarrier ring),
+                               3/4 lane-staged (warp per chunk, 4/8 B-row
+                               gathers in flight; needs N/c >= 32)           */
 } sgap_kernel_t;
 
 /* CSR operand on the device (matrices.py:38-86 with int32 indices). */

@@ -175,7 +175,8 @@ int launch_nnz_multiple(bool tma, int tile, int owner, const sgap_kernel_t &k,
     return launch_status();
 }
 
-// hw_variant: 0 auto; 1 register walk; 2 TMA-staged walk.  Measured on config
+// hw_variant: 0 auto; 1 register walk; 2 TMA-staged walk; 3/4 lane-staged walk
+// (whole warp per chunk, 4/8 gathers in flight; needs N/c >= 32).  Measured on config
 // 2 (profiles/): software pipelining and 8-deep batches were slower (the extra
 // registers cost more occupancy than the added in-flight gathers recover), as
 // were L2 evict-first hints on the A stream, L1::no_allocate / evict_last on
@@ -196,9 +197,27 @@ int run_nnz_multiple_w(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, 
     const int variant = k.hw_variant == 0 ? ((tma_ok && W >= 16 && k.g <= 128) ? 2 : 1) : k.hw_variant;
     const bool tma = variant == 2;
     if (tma && !tma_ok) return SGAP_ERR_ARG;
-    if (variant != 1 && variant != 2) return SGAP_ERR_ARG;
-    const int status =
-        launch_nnz_multiple<T, V, W, 4, false>(tma, tile, owner, k, a, B, C, rowid, lr, wb, st);
+    if (variant < 1 || variant > 4) return SGAP_ERR_ARG;
+    if (variant >= 3 && W != 32) return SGAP_ERR_ARG;  // the staged walk takes a whole warp
+    int status;
+    if (variant >= 3) {
+        const long long total_pos = k.grid_size * k.chunk;
+        const long long chunks = total_pos / k.g;
+        const int blk = k.hw_block > 0 ? k.hw_block : kHwBlock;
+        if (blk != kHwBlock) return SGAP_ERR_ARG;
+        if (variant == 3)
+            k_nnz_multiple_staged<T, V, 4, 4><<<grid_for(chunks, blk), blk, 0, st>>>(
+                rowid, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, a.d_row_ptr,
+                (int)a.num_rows, k.n, a.nnz, k.g, total_pos, owner, lr, wb);
+        else
+            k_nnz_multiple_staged<T, V, 8, 3><<<grid_for(chunks, blk), blk, 0, st>>>(
+                rowid, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, a.d_row_ptr,
+                (int)a.num_rows, k.n, a.nnz, k.g, total_pos, owner, lr, wb);
+        status = launch_status();
+    } else {
+        status = launch_nnz_multiple<T, V, W, 4, false>(tma, tile, owner, k, a, B, C, rowid, lr,
+                                                         wb, st);
+    }
     if (status != SGAP_OK || lr.threshold < 0 || sizeof(T) != 4 || !has_exact) return status;
     // chunks inside long rows: error-free accumulate in their own kernel
     const long long total_pos = k.grid_size * k.chunk;
@@ -428,11 +447,18 @@ int sgap_block_starts(const int32_t *d_row_ptr, int64_t num_rows, int64_t chunk,
 
 int64_t sgap_long_row_threshold(const sgap_kernel_t *k, int32_t dtype) {
     if (k == nullptr || dtype != SGAP_F32) return -1;
-    long long unit;
-    if (k->family == SGAP_NNZ_MULTIPLE) unit = k->g;
-    else if (k->family == SGAP_NNZ_ONE) unit = k->r;
-    else return -1;  // row families own their rows: float64 running sums suffice
-    const long long t = 32 * unit;
+    // A row split over m chunk flushes accumulates m float32 roundings of
+    // partial sums that can be far larger than the row's final value (a
+    // power-law row whose column sum cancels).  nnz-multiple: rows longer than
+    // max(4g, 1024) go to the float64 table -- at g = 512 the previous bound
+    // (32g) let 32 flushes of 512-term partials reach 1.0e-5 on config 2.
+    // nnz-one flushes r-term segment sums: rows past 32r (min 128).
+    if (k->family == SGAP_NNZ_MULTIPLE) {
+        const long long t = 4LL * k->g;
+        return t < 1024 ? 1024 : t;
+    }
+    if (k->family != SGAP_NNZ_ONE) return -1;  // row families own their rows
+    const long long t = 32LL * k->r;
     return t < 128 ? 128 : t;
 }
 

@@ -734,6 +734,134 @@ k_nnz_multiple_exact(const int *__restrict__ rowid, const int *__restrict__ ci,
 }
 
 // ---------------------------------------------------------------------------
+// The same family, lane-staged (hw variant 3; a whole warp per chunk, lane l
+// on column tile t0+l).  Per 32-position step lane l holds position s+l's
+// (col, val, row id): one coalesced 128-byte request per array instead of 32
+// broadcast loads, and the next step's triple is loaded while this one is
+// consumed.  U B-row gathers go out back to back from shuffled column
+// indices before any is consumed; a ballot of row changes lets change-free
+// groups (the common case inside long power-law rows) skip the flush test.
+// Writeback semantics, owner writes, long-row routing and float64 folds every
+// kFoldEvery terms are those of eb_walk4 (tools/experiments/walk_probe.cu has
+// the stripped-down loop this came from).
+// ---------------------------------------------------------------------------
+template <typename T, int V, int U>
+__device__ __forceinline__ void eb_walk_staged(const int *__restrict__ rowid,
+                                               const int *__restrict__ ci,
+                                               const T *__restrict__ av, long long q0,
+                                               long long qend, const T *__restrict__ B, int N,
+                                               long long kcol, bool on, T *__restrict__ C,
+                                               const LongRows &lr, const Owner &own,
+                                               unsigned long long &nwb) {
+    static_assert(U == 4 || U == 8, "U in {4, 8}");
+    const unsigned lane = lane_id();
+    long long qn = q0 + lane;
+    int c_n = qn < qend ? __ldg(ci + qn) : 0;
+    T v_n = qn < qend ? __ldg(av + qn) : T(0);
+    int r_n = qn < qend ? __ldg(rowid + qn) : 0;
+    int cur = __shfl_sync(kFull, r_n, 0);
+    bool here = own.on && __ldg(own.rp + (cur & kRowMask)) == own.base;
+    if (here && on) zero_gap_before<T, V>(C, N, kcol, own, cur & kRowMask);
+    Vec<T, V> acc;
+    acc.zero();
+    Vec<double, V> tot;
+    tot.zero();
+    const T *bk = B + kcol;
+    for (long long s = q0; s < qend; s += 32) {
+        const int c_l = c_n, r_l = r_n;
+        const T v_l = v_n;
+        qn = s + 32 + lane;
+        c_n = qn < qend ? __ldg(ci + qn) : 0;
+        v_n = qn < qend ? __ldg(av + qn) : T(0);
+        r_n = qn < qend ? __ldg(rowid + qn) : 0;
+        const int nval = (int)min(32LL, qend - s);
+        const int r_up = __shfl_up_sync(kFull, r_l, 1);
+        const unsigned chm =
+            __ballot_sync(kFull, (int)lane < nval && r_l != (lane == 0 ? cur : r_up));
+#pragma unroll 1
+        for (int j = 0; j < nval; j += U) {
+            Vec<T, V> b[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int c = __shfl_sync(kFull, c_l, j + u);
+                if (on && j + u < nval) ldg_vec<T, V>(b[u], bk + (long long)c * N);
+                else b[u].zero();
+            }
+            const unsigned gm = (chm >> j) & ((1u << U) - 1u);
+            if (gm == 0u) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) fma_vec<T, V>(acc, __shfl_sync(kFull, v_l, j + u), b[u]);
+            } else {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const T v = __shfl_sync(kFull, v_l, j + u);
+                    const int r = __shfl_sync(kFull, r_l, j + u);
+                    if ((gm >> u) & 1u) {
+                        fold<T, V>(tot, acc);
+                        if (on) {
+                            flush_owned<T, V>(C, N, cur, kcol, tot, lr, here);
+                            nwb += V;
+                            if (own.on) zero_rows<T, V>(C, N, kcol, (cur & kRowMask) + 1, r & kRowMask);
+                        }
+                        tot.zero();
+                        cur = r;
+                        here = own.on;
+                    }
+                    fma_vec<T, V>(acc, v, b[u]);
+                }
+            }
+            if (((j + U) & (kFoldEvery - 1)) == 0) fold<T, V>(tot, acc);
+        }
+    }
+    fold<T, V>(tot, acc);
+    const bool complete = here && __ldg(own.rp + (cur & kRowMask) + 1) == own.end;
+    if (on) {
+        flush_owned<T, V>(C, N, cur, kcol, tot, lr, complete);
+        nwb += V;
+        if (own.on && own.end == own.nnz) zero_rows<T, V>(C, N, kcol, (cur & kRowMask) + 1, own.m);
+    }
+}
+
+template <typename T, int V, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+k_nnz_multiple_staged(const int *__restrict__ rowid, const int *__restrict__ ci,
+                      const T *__restrict__ av, const T *__restrict__ B, T *__restrict__ C,
+                      const int *__restrict__ rp, int M, int N, long long nnz, int g,
+                      long long total_pos, int owner, LongRows lr, unsigned long long *wb) {
+    const int NT = N / V;
+    const long long total_chunks = total_pos / g;
+    const unsigned lane = lane_id();
+    unsigned long long nwb = 0;
+    SGAP_WARP_LOOP(ch, total_chunks) {
+        const long long base = ch * g;
+        const long long end = min(base + (long long)g, nnz);
+        for (int t0 = 0; t0 < NT; t0 += 32) {
+            const int tile = t0 + (int)lane;
+            const bool on = tile < NT;
+            const long long kcol = (long long)tile * V;
+            if (base >= end) {  // chunk past nnz: the reference flushes 0 into row M-1
+                if (on) nwb += V;
+                continue;
+            }
+            const Owner own{rp, rowid, base, end, nnz, M, owner != 0};
+            const int r_first = __ldg(rowid + base);
+            if ((r_first & kExactFlag) && __ldg(rowid + end - 1) == r_first) {  // the exact kernel's
+                if (on) {
+                    if (own.on && __ldg(rp + (r_first & kRowMask)) == base)
+                        zero_gap_before<T, V>(C, N, kcol, own, r_first & kRowMask);
+                    if (own.on && end == nnz)
+                        zero_rows<T, V>(C, N, kcol, (r_first & kRowMask) + 1, M);
+                    nwb += V;
+                }
+                continue;
+            }
+            eb_walk_staged<T, V, U>(rowid, ci, av, base, end, B, N, kcol, on, C, lr, own, nwb);
+        }
+    }
+    flush_count(wb, nwb);
+}
+
+// ---------------------------------------------------------------------------
 // The same family, TMA-staged: a persistent CTA walks tiles of `tile`
 // positions (a multiple of g, so chunks stay globally aligned).  One producer
 // warp streams each tile's (col, val, row id) arrays into a shared-memory
