@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define SGAP_ABI_VERSION 1
+#define SGAP_ABI_VERSION 2
 
 typedef enum {
     SGAP_OK = 0,
@@ -143,7 +143,12 @@ int sgap_block_starts(const int32_t *d_row_ptr, int64_t num_rows, int64_t chunk,
  *   flushes go to a float64 table d_long_acc [long_capacity x n] that
  *   sgap_run folds into C (and clears) after the kernel.  d_long_rows holds
  *   the sorted ids of those rows and d_long_count their number, both filled
- *   by sgap_prepare_long_rows.  long_threshold < 0 disables the table.       */
+ *   by sgap_prepare_long_rows.  long_threshold < 0 disables the table.
+ *   long_chunk > 0 (nnz-multiple, = g): rows whose nonzeros straddle a
+ *   g-position chunk boundary join the table too, so every split row is
+ *   summed in float64 and the overwrite mode needs no zero-fill pre-pass.
+ *   d_long_slot: [num_rows] table slot of each table row (other entries
+ *   unused), filled by sgap_prepare_long_rows; NULL = search d_long_rows.     */
 typedef struct {
     const int32_t *d_block_starts;
     const int32_t *d_rowid;
@@ -154,14 +159,18 @@ typedef struct {
     int64_t long_threshold;
     int32_t has_exact_rows;   /* any row longer than sgap_exact_row_length()?
                                  (0 lets sgap_run skip the error-free pass)  */
+    int32_t *d_long_slot;
+    int64_t long_chunk;
 } sgap_aux_t;
 
 /* Per-position row ids (what the reference lowering recovers per lane with
  * binary_search_before over the block window plus a forward advance,
- * lowering.py:459-500), expanded once per matrix; bit 31 marks rows longer
- * than long_threshold (pass -1 for none).                                  */
+ * lowering.py:459-500), expanded once per matrix; bit 31 marks the rows of
+ * the long-row table: longer than long_threshold (pass -1 for none) or, with
+ * long_chunk > 0, straddling a long_chunk-position boundary.               */
 int sgap_row_ids(const int32_t *d_row_ptr, int64_t num_rows, int64_t nnz,
-                 int64_t long_threshold, int32_t *d_rowid, void *stream);
+                 int64_t long_threshold, int64_t long_chunk, int32_t *d_rowid,
+                 void *stream);
 
 /* Rows longer than this (and in the long-row table) are accumulated with an
  * error-free transform (TwoProduct + TwoSum): float32 product rounding alone
@@ -171,12 +180,17 @@ int64_t sgap_exact_row_length(void);
 /* Threshold the engine uses for a kernel (-1: no table needed: row families
  * keep float64 running sums, float64 values accumulate in float64).        */
 int64_t sgap_long_row_threshold(const sgap_kernel_t *kernel, int32_t dtype);
-/* Upper bound on the number of long rows (each holds > threshold nonzeros). */
-int64_t sgap_long_row_capacity(int64_t nnz, int64_t threshold);
+/* Chunk length whose straddling rows join the table (0: none); nnz-multiple
+ * with g >= 128 in float32.                                                 */
+int64_t sgap_long_row_chunk(const sgap_kernel_t *kernel, int32_t dtype);
+/* Upper bound on the number of table rows: rows with > threshold nonzeros
+ * plus (chunk > 0) one straddling row per chunk boundary.                   */
+int64_t sgap_long_row_capacity(int64_t nnz, int64_t threshold, int64_t chunk);
 /* Scratch for the ordered compaction in sgap_prepare_long_rows. */
 size_t sgap_long_rows_tmp_bytes(int64_t num_rows);
-/* Fill aux->d_long_rows / d_long_count for aux->long_threshold and zero
- * aux->d_long_acc (long_capacity x n). */
+/* Fill aux->d_long_rows / d_long_count (and d_long_slot when set) for
+ * aux->long_threshold and aux->long_chunk, and zero aux->d_long_acc
+ * (long_capacity x n). */
 int sgap_prepare_long_rows(const int32_t *d_row_ptr, int64_t num_rows, int32_t n,
                            sgap_aux_t *aux, void *d_tmp, size_t tmp_bytes,
                            void *stream);

@@ -44,6 +44,7 @@ EXPORTED = (
     "sgap_row_ids",
     "sgap_exact_row_length",
     "sgap_long_row_threshold",
+    "sgap_long_row_chunk",
     "sgap_long_row_capacity",
     "sgap_long_rows_tmp_bytes",
     "sgap_prepare_long_rows",
@@ -113,6 +114,8 @@ class Aux(ctypes.Structure):
         ("long_capacity", ctypes.c_int64),
         ("long_threshold", ctypes.c_int64),
         ("has_exact_rows", ctypes.c_int32),
+        ("d_long_slot", ctypes.c_void_p),
+        ("long_chunk", ctypes.c_int64),
     ]
 
 
@@ -143,13 +146,15 @@ def lib():
     L.sgap_build_kernel.restype = ctypes.c_int
     L.sgap_block_starts.argtypes = [vp, i64, i64, i64, vp, vp]
     L.sgap_block_starts.restype = ctypes.c_int
-    L.sgap_row_ids.argtypes = [vp, i64, i64, i64, vp, vp]
+    L.sgap_row_ids.argtypes = [vp, i64, i64, i64, i64, vp, vp]
     L.sgap_row_ids.restype = ctypes.c_int
     L.sgap_exact_row_length.argtypes = []
     L.sgap_exact_row_length.restype = i64
     L.sgap_long_row_threshold.argtypes = [ctypes.POINTER(Kernel), i32]
     L.sgap_long_row_threshold.restype = i64
-    L.sgap_long_row_capacity.argtypes = [i64, i64]
+    L.sgap_long_row_chunk.argtypes = [ctypes.POINTER(Kernel), i32]
+    L.sgap_long_row_chunk.restype = i64
+    L.sgap_long_row_capacity.argtypes = [i64, i64, i64]
     L.sgap_long_row_capacity.restype = i64
     L.sgap_long_rows_tmp_bytes.argtypes = [i64]
     L.sgap_long_rows_tmp_bytes.restype = ctypes.c_size_t

@@ -14,7 +14,7 @@
 
 using namespace sgap;
 
-extern "C" int64_t sgap_long_row_capacity(int64_t nnz, int64_t threshold);
+extern "C" int64_t sgap_long_row_capacity(int64_t nnz, int64_t threshold, int64_t chunk);
 
 namespace {
 
@@ -224,7 +224,7 @@ int run_nnz_multiple_w(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, 
     const int vec4 = (k.g % 4 == 0) && aligned(rowid, 16) && aligned(a.d_col_idx, 16) &&
                      aligned(a.d_vals, 16);
     (void)total_pos;
-    const long long cap = sgap_long_row_capacity(a.nnz, lr.threshold);
+    const long long cap = sgap_long_row_capacity(a.nnz, lr.threshold, lr.chunk);
     const dim3 grid((unsigned)(cap < 1024 ? (cap > 0 ? cap : 1) : 1024), 64);
     k_nnz_multiple_exact<T, V><<<grid, kHwBlock, 0, st>>>(
         rowid, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, a.d_row_ptr, k.n, a.nnz, k.g,
@@ -237,9 +237,12 @@ int run_nnz_multiple(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T 
                      const int *rowid, const LongRows &lr, int acc, bool has_exact,
                      unsigned long long *wb, cudaStream_t st) {
     // overwrite mode: zero only rows that will receive atomic flushes (or no
-    // flush at all), then let the walk store complete rows outright
+    // flush at all), then let the walk store complete rows outright; with
+    // chunk routing every split row is in the float64 table, whose fold
+    // overwrites it, so nothing needs zeroing
     const int owner = acc ? 0 : 1;
-    if (owner) {
+    const bool routed = lr.threshold >= 0 && lr.chunk == k.g;
+    if (owner && !routed) {
         k_zero_shared_rows<T><<<grid_for(ceil_div(a.num_rows, 32), kHwBlock), kHwBlock, 0, st>>>(
             a.d_row_ptr, (int)a.num_rows, k.n, k.g, lr.threshold, C);
     }
@@ -464,14 +467,22 @@ int64_t sgap_long_row_threshold(const sgap_kernel_t *k, int32_t dtype) {
 
 int64_t sgap_exact_row_length(void) { return kExactRow; }
 
-int64_t sgap_long_row_capacity(int64_t nnz, int64_t threshold) {
+int64_t sgap_long_row_chunk(const sgap_kernel_t *k, int32_t dtype) {
+    if (k == nullptr || dtype != SGAP_F32 || k->family != SGAP_NNZ_MULTIPLE) return 0;
+    // short chunks would put most rows in the table (capacity ~ nnz/g rows x n)
+    return k->g >= 128 ? k->g : 0;
+}
+
+int64_t sgap_long_row_capacity(int64_t nnz, int64_t threshold, int64_t chunk) {
     if (threshold < 0) return 0;
-    return nnz / (threshold + 1) + 1;
+    long long cap = nnz / (threshold + 1) + 1;
+    if (chunk > 0) cap += (nnz + chunk - 1) / chunk;  // one straddling row per boundary
+    return cap;
 }
 
 size_t sgap_long_rows_tmp_bytes(int64_t num_rows) {
     size_t bytes = 0;
-    LongRowPred pred{nullptr, 0};
+    LongRowPred pred{nullptr, 0, 0};
     cub::DeviceSelect::If(nullptr, bytes, thrust::counting_iterator<int>(0), (int *)nullptr,
                           (int *)nullptr, (int)(num_rows > 0 ? num_rows : 1), pred);
     return bytes;
@@ -491,11 +502,18 @@ int sgap_prepare_long_rows(const int32_t *d_row_ptr, int64_t num_rows, int32_t n
     }
     size_t need = sgap_long_rows_tmp_bytes(num_rows);
     if (d_tmp == nullptr || tmp_bytes < need) return SGAP_ERR_ARG;
-    LongRowPred pred{d_row_ptr, aux->long_threshold};
+    LongRowPred pred{d_row_ptr, aux->long_threshold, aux->long_chunk};
     if (cub::DeviceSelect::If(d_tmp, tmp_bytes, thrust::counting_iterator<int>(0),
                               aux->d_long_rows, aux->d_long_count, (int)num_rows, pred, st) !=
         cudaSuccess)
         return SGAP_ERR_CUDA;
+    if (aux->d_long_slot != nullptr) {
+        long long cap = aux->long_capacity;
+        unsigned blocks = (unsigned)ceil_div(cap > 0 ? cap : 1, kHwBlock);
+        if (blocks > 4096) blocks = 4096;
+        k_long_slots<<<blocks, kHwBlock, 0, st>>>(aux->d_long_rows, aux->d_long_count,
+                                                  aux->d_long_slot);
+    }
     const size_t acc_bytes = (size_t)aux->long_capacity * (size_t)n * sizeof(double);
     if (acc_bytes && cudaMemsetAsync(aux->d_long_acc, 0, acc_bytes, st) != cudaSuccess)
         return SGAP_ERR_CUDA;
@@ -503,13 +521,14 @@ int sgap_prepare_long_rows(const int32_t *d_row_ptr, int64_t num_rows, int32_t n
 }
 
 int sgap_row_ids(const int32_t *d_row_ptr, int64_t num_rows, int64_t nnz,
-                 int64_t long_threshold, int32_t *d_rowid, void *stream) {
+                 int64_t long_threshold, int64_t long_chunk, int32_t *d_rowid, void *stream) {
+    if (long_chunk < 0) return SGAP_ERR_ARG;
     if (num_rows < 0 || nnz < 0 || num_rows > INT_MAX - 1 || nnz > INT_MAX) return SGAP_ERR_SHAPE;
     if (nnz == 0) return SGAP_OK;
     if (d_row_ptr == nullptr || d_rowid == nullptr || num_rows == 0) return SGAP_ERR_ARG;
     const long long items = ceil_div(nnz, 1024);
     k_row_ids<<<grid_for(items, kHwBlock), kHwBlock, 0, as_stream(stream)>>>(
-        d_row_ptr, (int)num_rows, nnz, long_threshold, d_rowid);
+        d_row_ptr, (int)num_rows, nnz, long_threshold, long_chunk, d_rowid);
     return launch_status();
 }
 
@@ -537,12 +556,13 @@ int sgap_run(const sgap_kernel_t *k, const sgap_csr_t *a, const void *d_b, void 
     const int32_t *rowid = aux ? aux->d_rowid : nullptr;
     if (eb && k->grid_size > 0 && a->nnz > 0 && rowid == nullptr) return SGAP_ERR_ARG;
     if (k->family == SGAP_NNZ_MULTIPLE && (k->g < 1 || k->chunk % k->g)) return SGAP_ERR_CONFIG;
-    LongRows lr{nullptr, nullptr, nullptr, -1};
+    LongRows lr{nullptr, nullptr, nullptr, -1, nullptr, 0};
     const bool has_exact = aux != nullptr && aux->has_exact_rows != 0;
     if (eb && aux && aux->long_threshold >= 0 && dtype == SGAP_F32) {
         if (aux->d_long_rows == nullptr || aux->d_long_count == nullptr || aux->d_long_acc == nullptr)
             return SGAP_ERR_ARG;
-        lr = LongRows{aux->d_long_rows, aux->d_long_count, aux->d_long_acc, aux->long_threshold};
+        lr = LongRows{aux->d_long_rows, aux->d_long_count, aux->d_long_acc, aux->long_threshold,
+                      aux->d_long_slot, aux->long_chunk};
     }
     if (k->family == SGAP_NNZ_ONE && !accumulate) {
         // atomic-writeback families accumulate into C: zero-fill (counts as

@@ -60,6 +60,30 @@ __device__ __forceinline__ void ldg_vec<double, 4>(Vec<double, 4> &o, const doub
     o.v[0] = t0.x; o.v[1] = t0.y; o.v[2] = t1.x; o.v[3] = t1.y;
 }
 
+// B-row gather as a volatile load: issued where written (the compiler may not
+// sink it into the branch that consumes it), so U gathers stay back to back.
+template <typename T, int V>
+__device__ __forceinline__ void gather_vec(Vec<T, V> &o, const T *p) {
+    if constexpr (sizeof(T) == 4 && V == 4) {
+        asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(o.v[0]), "=f"(o.v[1]), "=f"(o.v[2]), "=f"(o.v[3])
+                     : "l"(p));
+    } else if constexpr (sizeof(T) == 4 && V == 2) {
+        asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(o.v[0]), "=f"(o.v[1]) : "l"(p));
+    } else if constexpr (sizeof(T) == 4 && V == 1) {
+        asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(o.v[0]) : "l"(p));
+    } else if constexpr (sizeof(T) == 8 && V == 1) {
+        asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(o.v[0]) : "l"(p));
+    } else if constexpr (sizeof(T) == 8 && V == 2) {
+        asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(o.v[0]), "=d"(o.v[1]) : "l"(p));
+    } else {
+        asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(o.v[0]), "=d"(o.v[1]) : "l"(p));
+        asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];"
+                     : "=d"(o.v[2]), "=d"(o.v[3])
+                     : "l"(p + 2));
+    }
+}
+
 // Software prefetch of a streamed A line into L1 (non-blocking, no register).
 __device__ __forceinline__ void prefetch_l1(const void *p) {
     asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
@@ -183,10 +207,12 @@ __device__ __forceinline__ Vec<T, V> narrow(const Vec<double, V> &tot) {
 // of power-law matrices) accumulate those flushes in a float64 side table
 // instead of float32 C; a fold pass adds the table into C afterwards.
 struct LongRows {
-    const int *rows;      // sorted row ids whose length exceeds `threshold`
+    const int *rows;      // sorted row ids of the table (long or chunk-straddling)
     const int *count;     // number of entries in `rows` (device scalar)
     double *acc;          // [capacity x N] float64 partial sums
     long long threshold;  // < 0: side table disabled (float64 values, RB families)
+    const int *slot;      // row -> table slot (nullptr: binary search of `rows`)
+    long long chunk;      // > 0: every row straddling a `chunk` boundary is in the table
 };
 
 // Row ids carry bit 31 when the row belongs to the long-row table and bit 30
@@ -205,10 +231,16 @@ __device__ __forceinline__ void flush_row(T *__restrict__ C, int N, int rid, lon
                                           const Vec<double, V> &tot, const LongRows &lr) {
     const int row = rid & kRowMask;
     if (rid < 0 && lr.threshold >= 0) {
-        int lo = 0, hi = *lr.count;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (__ldg(lr.rows + mid) < row) lo = mid + 1; else hi = mid;
+        int lo;
+        if (lr.slot != nullptr) {
+            lo = __ldg(lr.slot + row);
+        } else {
+            lo = 0;
+            int hi = *lr.count;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (__ldg(lr.rows + mid) < row) lo = mid + 1; else hi = mid;
+            }
         }
         double *p = lr.acc + (long long)lo * N + kcol;
 #pragma unroll

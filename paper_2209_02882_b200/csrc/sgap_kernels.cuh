@@ -756,6 +756,8 @@ __device__ __forceinline__ void eb_walk_staged(const int *__restrict__ rowid,
     static_assert(U == 4 || U == 8, "U in {4, 8}");
     const unsigned lane = lane_id();
     long long qn = q0 + lane;
+    // positions past the chunk read column 0 with value 0; their products are
+    // never accumulated (the fast path only takes full groups)
     int c_n = qn < qend ? __ldg(ci + qn) : 0;
     T v_n = qn < qend ? __ldg(av + qn) : T(0);
     int r_n = qn < qend ? __ldg(rowid + qn) : 0;
@@ -766,7 +768,7 @@ __device__ __forceinline__ void eb_walk_staged(const int *__restrict__ rowid,
     acc.zero();
     Vec<double, V> tot;
     tot.zero();
-    const T *bk = B + kcol;
+    const T *bk = B + (on ? kcol : 0);  // lanes past the last tile gather tile 0, store nothing
     for (long long s = q0; s < qend; s += 32) {
         const int c_l = c_n, r_l = r_n;
         const T v_l = v_n;
@@ -780,22 +782,26 @@ __device__ __forceinline__ void eb_walk_staged(const int *__restrict__ rowid,
             __ballot_sync(kFull, (int)lane < nval && r_l != (lane == 0 ? cur : r_up));
 #pragma unroll 1
         for (int j = 0; j < nval; j += U) {
+            // U gathers back to back (volatile: not sunk into the branch below)
             Vec<T, V> b[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int c = __shfl_sync(kFull, c_l, j + u);
-                if (on && j + u < nval) ldg_vec<T, V>(b[u], bk + (long long)c * N);
-                else b[u].zero();
-            }
+            for (int u = 0; u < U; ++u)
+                gather_vec<T, V>(b[u], bk + (long long)__shfl_sync(kFull, c_l, j + u) * N);
             const unsigned gm = (chm >> j) & ((1u << U) - 1u);
-            if (gm == 0u) {
+            if (gm == 0u && j + U <= nval) {
 #pragma unroll
                 for (int u = 0; u < U; ++u) fma_vec<T, V>(acc, __shfl_sync(kFull, v_l, j + u), b[u]);
             } else {
-#pragma unroll
+                // a row change (or the chunk end) inside this group: one
+                // position at a time, each B row re-read from L1 where the
+                // gathers above just put it, so the flush path is instantiated
+                // once and keeps no gathered rows live
+#pragma unroll 1
                 for (int u = 0; u < U; ++u) {
+                    const int c = __shfl_sync(kFull, c_l, j + u);
                     const T v = __shfl_sync(kFull, v_l, j + u);
                     const int r = __shfl_sync(kFull, r_l, j + u);
+                    if (j + u >= nval) break;
                     if ((gm >> u) & 1u) {
                         fold<T, V>(tot, acc);
                         if (on) {
@@ -807,7 +813,9 @@ __device__ __forceinline__ void eb_walk_staged(const int *__restrict__ rowid,
                         cur = r;
                         here = own.on;
                     }
-                    fma_vec<T, V>(acc, v, b[u]);
+                    Vec<T, V> bb;
+                    ldg_vec<T, V>(bb, bk + (long long)c * N);
+                    fma_vec<T, V>(acc, v, bb);
                 }
             }
             if (((j + U) & (kFoldEvery - 1)) == 0) fold<T, V>(tot, acc);
@@ -990,7 +998,8 @@ k_nnz_multiple_tma(const int *__restrict__ rowid, const int *__restrict__ ci,
 // binary search and then walks forward; bit 31 flags rows of the long-row
 // table (length > thr).
 __global__ void __launch_bounds__(256)
-k_row_ids(const int *__restrict__ rp, int M, long long nnz, long long thr, int *__restrict__ out) {
+k_row_ids(const int *__restrict__ rp, int M, long long nnz, long long thr, long long chunk,
+          int *__restrict__ out) {
     const long long items = (nnz + 1023) >> 10;
     const unsigned lane = lane_id();
     SGAP_WARP_LOOP(item, items) {
@@ -1012,8 +1021,9 @@ k_row_ids(const int *__restrict__ rp, int M, long long nnz, long long thr, int *
                 next = __ldg(rp + r + 1);
             }
             const bool is_long = thr >= 0 && next - start > thr;
+            const bool split = thr >= 0 && chunk > 0 && start / chunk != (next - 1) / chunk;
             const bool exact = is_long && next - start > kExactRow;
-            out[p] = r | (is_long ? kLongFlag : 0) | (exact ? kExactFlag : 0);
+            out[p] = r | ((is_long || split) ? kLongFlag : 0) | (exact ? kExactFlag : 0);
         }
     }
 }
@@ -1045,13 +1055,19 @@ k_zero_shared_rows(const int *__restrict__ rp, int M, int N, long long g, long l
                    T *__restrict__ C) {
     const long long items = ((long long)M + 31) >> 5;
     const unsigned lane = lane_id();
+    // positions are < 2^31: 32-bit chunk numbers (a shift when g is a power
+    // of two) -- two 64-bit divisions per row made this pass 6% of config 2
+    const unsigned ug = (unsigned)g;
+    const int shift = (ug & (ug - 1u)) == 0u ? __ffs((int)ug) - 1 : -1;
     SGAP_WARP_LOOP(item, items) {
         const long long r = item * 32 + lane;
         bool need = false;
         if (r < M) {
-            const long long s = __ldg(rp + r), e = __ldg(rp + r + 1);
-            const long long len = e - s;
-            need = len > 0 && s / g != (e - 1) / g && !(thr >= 0 && len > thr);
+            const unsigned s = (unsigned)__ldg(rp + r), e = (unsigned)__ldg(rp + r + 1);
+            const unsigned len = e - s;
+            const bool split = shift >= 0 ? (s >> shift) != ((e - 1u) >> shift)
+                                          : s / ug != (e - 1u) / ug;
+            need = len > 0u && split && !(thr >= 0 && (long long)len > thr);
         }
         unsigned mask = __ballot_sync(kFull, need);
         while (mask) {
@@ -1073,10 +1089,21 @@ k_zero_shared_rows(const int *__restrict__ rp, int M, int N, long long g, long l
 struct LongRowPred {
     const int *rp;
     long long threshold;
+    long long chunk;  // > 0: rows straddling a chunk boundary join the table
     __host__ __device__ __forceinline__ bool operator()(const int &r) const {
-        return (long long)(rp[r + 1] - rp[r]) > threshold;
+        const long long s = rp[r], e = rp[r + 1];
+        if (e - s > threshold) return true;
+        return chunk > 0 && e > s && s / chunk != (e - 1) / chunk;
     }
 };
+
+// Row -> slot map of the table (only the table's rows are written).
+__global__ void k_long_slots(const int *__restrict__ rows, const int *__restrict__ count,
+                             int *__restrict__ slot) {
+    const int n = *count;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        slot[rows[i]] = i;
+}
 
 // The verification product of runner.verify_point (runner.py:193-194): the
 // dense reference C = A@B in float64, per (i,k) ascending-p order with the

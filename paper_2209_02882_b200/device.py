@@ -156,23 +156,33 @@ class KernelAux:
     long_capacity: int = 0
     long_threshold: int = -1
     has_exact_rows: int = 0
+    long_slot: torch.Tensor | None = None
+    long_chunk: int = 0
 
     def view(self) -> _native.Aux:
         ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
         return _native.Aux(ptr(self.starts), ptr(self.rowid), ptr(self.long_rows),
                            ptr(self.long_count), ptr(self.long_acc), self.long_capacity,
-                           self.long_threshold, self.has_exact_rows)
+                           self.long_threshold, self.has_exact_rows, ptr(self.long_slot),
+                           self.long_chunk)
 
     def nbytes(self) -> int:
-        ts = (self.starts, self.rowid, self.long_rows, self.long_count, self.long_acc)
+        ts = (self.starts, self.rowid, self.long_rows, self.long_count, self.long_acc,
+              self.long_slot)
         return sum(t.numel() * t.element_size() for t in ts if t is not None)
 
 
 def prepare_aux(k: LoweredKernel, a: DeviceCsr, *, stream=None, long_rows: bool = True,
-                long_threshold: int | None = None, block_starts: bool = True) -> KernelAux:
+                long_threshold: int | None = None, block_starts: bool = True,
+                split_rows: bool = False) -> KernelAux:
     """Per-matrix side data of kernel ``k``: block starts and per-position row
     ids (nnz families) and, for float32 values, the long-row table
-    (include/sgap.h: sgap_block_starts, sgap_row_ids, sgap_prepare_long_rows)."""
+    (include/sgap.h: sgap_block_starts, sgap_row_ids, sgap_prepare_long_rows).
+
+    ``split_rows``: nnz-multiple rows that straddle a g-chunk boundary also
+    go to the float64 table (every split row summed in float64, no zero-fill
+    pre-pass).  Off by default: on config 2 its float64 flushes cost more
+    than the pre-pass they replace (0.764 vs 0.754 ms at g=512)."""
     eb = k.family in ("nnz-one", "nnz-multiple")
     a.check()
     starts = None
@@ -184,22 +194,27 @@ def prepare_aux(k: LoweredKernel, a: DeviceCsr, *, stream=None, long_rows: bool 
     L = _native.lib()
     dev = a.device
     thr = -1
+    chunk = 0
     if long_rows:
         ks = kernel_struct(k)
         thr = int(L.sgap_long_row_threshold(ctypes.byref(ks), native_dtype(a.vals.dtype)))
         if long_threshold is not None and thr >= 0:
             thr = int(long_threshold)
+        if thr >= 0 and split_rows:
+            chunk = int(L.sgap_long_row_chunk(ctypes.byref(ks), native_dtype(a.vals.dtype)))
     aux.rowid = torch.empty(max(a.nnz, 4), dtype=torch.int32, device=dev)
-    _native.check(L.sgap_row_ids(a.row_ptr.data_ptr(), a.num_rows, a.nnz, thr,
+    _native.check(L.sgap_row_ids(a.row_ptr.data_ptr(), a.num_rows, a.nnz, thr, chunk,
                                  aux.rowid.data_ptr(), _stream_handle(stream)), "sgap_row_ids")
     if thr < 0:
         return aux
-    cap = int(L.sgap_long_row_capacity(a.nnz, thr))
+    cap = int(L.sgap_long_row_capacity(a.nnz, thr, chunk))
     if a.num_rows:  # plan-time host sync: is the error-free pass needed at all?
         longest = int((a.row_ptr[1:] - a.row_ptr[:-1]).max().item())
         aux.has_exact_rows = int(longest > int(L.sgap_exact_row_length()))
     aux.long_threshold = thr
+    aux.long_chunk = chunk
     aux.long_capacity = cap
+    aux.long_slot = torch.empty(max(a.num_rows, 1), dtype=torch.int32, device=dev)
     aux.long_rows = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
     aux.long_count = torch.zeros(1, dtype=torch.int32, device=dev)
     aux.long_acc = torch.empty(max(cap, 1) * k.n, dtype=torch.float64, device=dev)
@@ -248,7 +263,8 @@ def launches_per_call(k: LoweredKernel, aux: KernelAux | None, *, accumulate: bo
     """Kernels of libsgap.so one ``spmm`` call launches (the driver's memset
     for the nnz-one zero-fill is not ours and not counted)."""
     n = 1
-    if k.family == "nnz-multiple" and not accumulate:
+    routed = aux is not None and aux.long_threshold >= 0 and aux.long_chunk == k.g
+    if k.family == "nnz-multiple" and not accumulate and not routed:
         n += 1  # k_zero_shared_rows
     if aux is not None and aux.long_threshold >= 0 and k.family in ("nnz-one", "nnz-multiple"):
         n += 1  # k_long_rows_fold

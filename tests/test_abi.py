@@ -36,7 +36,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_status_strings():
     L = _native.lib()
-    assert L.sgap_abi_version() == 1
+    assert L.sgap_abi_version() == 2
     assert _native.status_string(_native.ERR_NO_TEMPLATE) == "no template covers the point"
     assert _native.status_string(99) == "unknown status"
 
@@ -53,8 +53,10 @@ def test_argument_validation_without_device():
     k = _native.Kernel()
     assert L.sgap_run(None, None, None, None, 0, 0, None, None, None) == _native.ERR_ARG
     assert L.sgap_long_row_threshold(None, 0) == -1
-    assert L.sgap_long_row_capacity(1000, -1) == 0
-    assert L.sgap_long_row_capacity(1000, 99) == 11
+    assert L.sgap_long_row_capacity(1000, -1, 0) == 0
+    assert L.sgap_long_row_capacity(1000, 99, 0) == 11
+    assert L.sgap_long_row_capacity(1000, 99, 100) == 21  # + one straddling row per boundary
+    assert L.sgap_long_row_chunk(None, 0) == 0
     L.sgap_long_rows_tmp_bytes(1 << 20)  # needs a device to size CUB scratch; must not crash
     k.n, k.c = 4, 1
     a = _native.Csr()

@@ -48,15 +48,18 @@ def _check(g, n, points):
     want = oracle.spmm_f64(rp, a.col_idx.cpu().numpy(), a.vals.cpu().numpy(), b.cpu().numpy(), n)
     c = torch.empty((a.num_rows, n), dtype=torch.float32, device=dev)
     worst = {}
-    for text, p in points:
+    for item in points:
+        text, p = item[:2]
+        hw_variant = item[2] if len(item) > 2 else 0
+        split_rows = item[3] if len(item) > 3 else False
         tpl = algorithm_template(parse_point(text), KernelConfig(n=n, p=p))
         assert tpl is not None, text
         k = lower(tpl, _Rp(a.num_rows, a.num_cols, rp.astype(np.int64)), compute_starts=False)
         c.fill_(float("nan"))
-        spmm(k, a, b, c, aux=prepare_aux(k, a))
+        spmm(k, a, b, c, aux=prepare_aux(k, a, split_rows=split_rows), hw_variant=hw_variant)
         err = oracle.max_rel_error(c.cpu().numpy(), want)
-        worst[text] = err
-        assert err <= TOL, (text, p, err)
+        worst[item] = err
+        assert err <= TOL, (item, err)
     return worst
 
 
@@ -64,6 +67,16 @@ def test_config2_rmat_every_family():
     g = G.rmat(20, 16, seed=1, device="cuda")
     assert g.nnz > 16_000_000
     print(_check(g, 128, POINTS_N128))
+
+
+def test_config2_long_chunk_walks():
+    """The bench's schedules (long chunks, g up to 2048) on every walk
+    variant, with and without split-row routing to the float64 table."""
+    g = G.rmat(20, 16, seed=1, device="cuda")
+    pts = [(t, 256, v, split) for t in ("nnz:512,col:4,r:1", "nnz:2048,col:4,r:1", "nnz:128,col:4,r:1")
+           for v in (1, 3, 4) for split in (False, True)]
+    pts += [("nnz:128,col:4,r:1", 256, 2, False), ("nnz:64,col:2,r:1", 1024, 3, True)]
+    print(_check(g, 128, pts))
 
 
 def test_stencil_small_n():
