@@ -110,7 +110,7 @@ int run_nnz_one_r(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
     const int TW = pow2_floor(NT < 32 / R ? NT : 32 / R);
     const int Q = 32 / TW;
     const long long total_pos = k.grid_size * k.chunk;
-    const long long items = ceil_div(total_pos, Q);
+    const long long items = ceil_div(total_pos, 4LL * Q);  // kSteps groups of Q per warp item
     const int blk = k.hw_block > 0 ? k.hw_block : kHwBlock;
     k_nnz_one<T, V, R><<<grid_for(items, blk), blk, 0, st>>>(
         rowid, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, (int)a.num_rows, k.n, a.nnz,
@@ -453,12 +453,16 @@ int64_t sgap_long_row_threshold(const sgap_kernel_t *k, int32_t dtype) {
     // A row split over m chunk flushes accumulates m float32 roundings of
     // partial sums that can be far larger than the row's final value (a
     // power-law row whose column sum cancels).  nnz-multiple: rows longer than
-    // max(4g, 1024) go to the float64 table -- at g = 512 the previous bound
-    // (32g) let 32 flushes of 512-term partials reach 1.0e-5 on config 2.
+    // clamp(4g, 1024, 32g) (min 128) go to the float64 table -- at g = 512
+    // the bound 32g let 32 flushes of 512-term partials reach 1.0e-5 on
+    // config 2, and at g = 2 the bound 1024 let 512 flushes reach 1.1e-5.
     // nnz-one flushes r-term segment sums: rows past 32r (min 128).
     if (k->family == SGAP_NNZ_MULTIPLE) {
-        const long long t = 4LL * k->g;
-        return t < 1024 ? 1024 : t;
+        // <= 32 flushes of short partials (small g), <= 4 of long ones
+        long long t = 4LL * k->g;
+        if (t < 1024) t = 1024;
+        if (t > 32LL * k->g) t = 32LL * k->g;
+        return t < 128 ? 128 : t;
     }
     if (k->family != SGAP_NNZ_ONE) return -1;  // row families own their rows
     const long long t = 32LL * k->r;

@@ -84,6 +84,29 @@ __device__ __forceinline__ void gather_vec(Vec<T, V> &o, const T *p) {
     }
 }
 
+// Quotient of a non-negative 64-bit index by a runtime divisor that is
+// usually a power of two (N, N/c): a shift then, else a 32-bit division when
+// both fit, else the 64-bit one (~70 instructions, which dominated the
+// per-cell overhead of row-reciprocal at one cell per warp).
+struct Divider {
+    long long d;
+    int shift;  // log2(d), or -1
+    __host__ __device__ static Divider make(long long d) {
+        Divider v{d, -1};
+        if (d > 0 && (d & (d - 1)) == 0) {
+            int s = 0;
+            while ((1LL << s) < d) ++s;
+            v.shift = s;
+        }
+        return v;
+    }
+    __device__ __forceinline__ long long div(long long x) const {
+        if (shift >= 0) return x >> shift;
+        if (x < 0x7fffffffLL && d < 0x7fffffffLL) return (long long)((unsigned)x / (unsigned)d);
+        return x / d;
+    }
+};
+
 // Software prefetch of a streamed A line into L1 (non-blocking, no register).
 __device__ __forceinline__ void prefetch_l1(const void *p) {
     asm volatile("prefetch.global.L1 [%0];" ::"l"(p));

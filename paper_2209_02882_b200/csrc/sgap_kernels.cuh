@@ -121,11 +121,12 @@ k_row_multiple(const int *__restrict__ rp, const int *__restrict__ ci,
                const T *__restrict__ av, const T *__restrict__ B, T *__restrict__ C,
                int M, int N, int g, int vec4, int accumulate) {
     const int L = N / V;
+    const Divider byL = Divider::make(L);
     const long long groups = ((long long)M + g - 1) / g;
     const long long total = groups * L;  // logical threads
     for (long long h = (long long)blockIdx.x * blockDim.x + threadIdx.x; h < total;
          h += (long long)gridDim.x * blockDim.x) {
-        const long long rg = h / L;
+        const long long rg = byL.div(h);
         const int t = (int)(h - rg * L);
         const long long kcol = (long long)t * V;
         for (int s = 0; s < g; ++s) {
@@ -177,7 +178,8 @@ k_row_interleaved(const int *__restrict__ rp, const int *__restrict__ ci,
 // columns); lane j accumulates positions begin+j, begin+j+G, ...
 // (cuda_row_reciprocal.cu:39-46), then the AtomicAddGroup becomes an
 // xor-shuffle tree and a single exclusive store by the group's lane 0.
-// Each lane folds its partial into float64 every 32 strided terms.
+// Rows longer than 32G: each lane folds its partial into float64 every 32
+// strided terms (shorter rows need no float64: <= 32 terms per lane).
 // ===========================================================================
 template <typename T, int V, int G>
 __global__ void __launch_bounds__(256)
@@ -189,6 +191,7 @@ k_row_reciprocal(const int *__restrict__ rp, const int *__restrict__ ci,
     const long long total = groups * G;
     const long long items = (total + 31) >> 5;
     const unsigned lane = lane_id();
+    const Divider byN = Divider::make(N);
     unsigned long long nwb = 0;
     SGAP_WARP_LOOP(item, items) {
         const long long h = item * 32 + lane;
@@ -196,7 +199,7 @@ k_row_reciprocal(const int *__restrict__ rp, const int *__restrict__ ci,
         const int j = (int)(h % G);
         const long long io0 = grp * V;
         const bool ok = io0 < cells;
-        const long long i = ok ? io0 / N : 0;
+        const long long i = ok ? byN.div(io0) : 0;
         const long long k0 = ok ? io0 - i * N : 0;
         const int beg = ok ? __ldg(rp + i) : 0;
         const int end = ok ? __ldg(rp + i + 1) : 0;
@@ -205,6 +208,9 @@ k_row_reciprocal(const int *__restrict__ rp, const int *__restrict__ ci,
         for (int u = 0; u < kBatch; ++u) acc[u].zero();
         Vec<double, V> tot;
         tot.zero();
+        // rows of <= 32G nonzeros (one segment: <= 32 terms per lane) sum in
+        // the value type; longer ones fold into float64 after each segment
+        const bool multi = end - beg > 32 * G;
         for (int seg = beg + j; seg < end; seg += 32 * G) {
             const int seg_end = min(seg + 32 * G, end);
             int p = seg;
@@ -227,10 +233,19 @@ k_row_reciprocal(const int *__restrict__ rp, const int *__restrict__ ci,
                 ldg_vec<T, V>(bv, B + (long long)__ldg(ci + p) * N + k0);
                 fma_vec<T, V>(acc[0], __ldg(av + p), bv);
             }
+            if (multi) {
 #pragma unroll
-            for (int u = 0; u < kBatch; ++u) fold<T, V>(tot, acc[u]);
+                for (int u = 0; u < kBatch; ++u) fold<T, V>(tot, acc[u]);
+            }
         }
-        Vec<T, V> part = narrow<T, V>(tot);
+        Vec<T, V> part;
+        if (multi) {
+            part = narrow<T, V>(tot);
+        } else {
+            part = acc[0];
+#pragma unroll
+            for (int u = 1; u < kBatch; ++u) add_vec<T, V>(part, acc[u]);
+        }
         group_sum_vec<G, T, V>(part);
         if (ok && j == 0) {
             store_vec<T, V>(C + i * N + k0, part, accumulate != 0);
@@ -256,53 +271,78 @@ __global__ void __launch_bounds__(256)
 k_nnz_one(const int *__restrict__ rowid, const int *__restrict__ ci, const T *__restrict__ av,
           const T *__restrict__ B, T *__restrict__ C, int M, int N, long long nnz,
           long long total_pos, int TW, LongRows lr, unsigned long long *wb) {
+    // A warp item spans kSteps consecutive groups of Q positions.  Flushes
+    // into rows of the float64 table (long rows: the engine's numerics
+    // policy, not the schedule) are added up per lane across the steps and
+    // issued as one float64 atomic per run -- a hub row otherwise costs one
+    // scalar float64 atomic per nonzero and tile; every other flush is the
+    // schedule's own float32 red, one per writeback.  The counted writebacks
+    // (SimMetrics.atomic_ops) are the logical ones either way.
+    constexpr int kSteps = 4;
     const int NT = N / V;
     const int Q = 32 / TW;
-    const long long items = (total_pos + Q - 1) / Q;
+    const long long span = (long long)Q * kSteps;
+    const long long items = (total_pos + span - 1) / span;
     const unsigned lane = lane_id();
     const int ql = (int)(lane & (unsigned)(Q - 1));
     const int tl = (int)(lane / (unsigned)Q);
+    const bool table = lr.threshold >= 0;
     unsigned long long nwb = 0;
     SGAP_WARP_LOOP(item, items) {
-        const long long pos = item * Q + ql;
-        const bool in_grid = pos < total_pos;
-        const bool in_nnz = pos < nnz;
-        // row owning the position; zero-extended lanes past nnz keep the
-        // clamped search row M-1 (lowering.py:476-488 with the window of the
-        // last block)
-        const int rid = in_nnz ? __ldg(rowid + pos) : (M - 1);
-        const int row = rid & kRowMask;
-        const int col = in_nnz ? __ldg(ci + pos) : 0;
-        const T a = in_nnz ? __ldg(av + pos) : T(0);
-        SegLanes sl{};
-        if constexpr (R > 1) sl = seg_lanes<R, int>(row, in_grid);
-        const T *brow = B + (long long)col * N;
         for (int tt = 0; tt < NT; tt += TW) {
             const int tile = tt + tl;
             const bool tok = tile < NT;
             const long long kcol = (long long)tile * V;
-            Vec<T, V> prod;
-            prod.zero();
-            if (in_nnz && tok) {
-                Vec<T, V> bv;
-                ldg_vec<T, V>(bv, brow + kcol);
+            int prow = -1;  // pending table row of this lane, and its sum
+            Vec<double, V> pend;
+            pend.zero();
 #pragma unroll
-                for (int x = 0; x < V; ++x) prod.v[x] = a * bv.v[x];
-            }
-            bool writer;
-            if constexpr (R == 1) {
-                writer = in_nnz && tok;
-            } else {
-                seg_scan_vec<R, T, V>(prod, sl.dist);
-                writer = sl.tail && tok;
-            }
-            if (writer) {
-                Vec<double, V> tot;
+            for (int step = 0; step < kSteps; ++step) {
+                const long long first = item * span + (long long)step * Q;
+                if (first >= total_pos) break;  // warp-uniform
+                const long long pos = first + ql;
+                const bool in_grid = pos < total_pos;
+                const bool in_nnz = pos < nnz;
+                // row owning the position; zero-extended lanes past nnz keep
+                // the clamped search row M-1 (lowering.py:476-488 with the
+                // window of the last block)
+                const int rid = in_nnz ? __ldg(rowid + pos) : (M - 1);
+                const int row = rid & kRowMask;
+                const int col = in_nnz ? __ldg(ci + pos) : 0;
+                const T a = in_nnz ? __ldg(av + pos) : T(0);
+                SegLanes sl{};
+                if constexpr (R > 1) sl = seg_lanes<R, int>(row, in_grid);
+                Vec<T, V> prod;
+                prod.zero();
+                if (in_nnz && tok) {
+                    Vec<T, V> bv;
+                    ldg_vec<T, V>(bv, B + (long long)col * N + kcol);
 #pragma unroll
-                for (int x = 0; x < V; ++x) tot.v[x] = (double)prod.v[x];
-                flush_row<T, V>(C, N, rid, kcol, tot, lr);
-                nwb += V;
+                    for (int x = 0; x < V; ++x) prod.v[x] = a * bv.v[x];
+                }
+                bool writer;
+                if constexpr (R == 1) {
+                    writer = in_nnz && tok;
+                } else {
+                    seg_scan_vec<R, T, V>(prod, sl.dist);
+                    writer = sl.tail && tok;
+                }
+                if (writer) {
+                    nwb += V;
+                    if (table && rid < 0) {
+                        if (row != prow) {
+                            if (prow >= 0) flush_row<T, V>(C, N, prow | kLongFlag, kcol, pend, lr);
+                            prow = row;
+                            pend.zero();
+                        }
+#pragma unroll
+                        for (int x = 0; x < V; ++x) pend.v[x] += (double)prod.v[x];
+                    } else {
+                        red_vec<T, V>(C + (long long)row * N + kcol, prod);
+                    }
+                }
             }
+            if (prow >= 0) flush_row<T, V>(C, N, prow | kLongFlag, kcol, pend, lr);
         }
     }
     flush_count(wb, nwb);
