@@ -84,9 +84,16 @@ int run_row_reciprocal_g(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B
     const long long cells = a.num_rows * (long long)k.n;
     const long long total = ceil_div(cells, V) * G;
     const int blk = k.hw_block > 0 ? k.hw_block : kHwBlock;
-    k_row_reciprocal<T, V, G><<<grid_for(ceil_div(total, 32), blk), blk, 0, st>>>(
-        a.d_row_ptr, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, (int)a.num_rows, k.n,
-        acc, wb);
+    const int n_shift = (k.n & (k.n - 1)) == 0 ? __builtin_ctz((unsigned)k.n) : -1;
+    const unsigned grid = grid_for(ceil_div(total, 32), blk);
+    if (cells + 64 < (1LL << 32) && a.num_cols * (long long)k.n < (1LL << 32))
+        k_row_reciprocal<T, V, G, unsigned><<<grid, blk, 0, st>>>(
+            a.d_row_ptr, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, (int)a.num_rows,
+            k.n, n_shift, acc, wb);
+    else
+        k_row_reciprocal<T, V, G, long long><<<grid, blk, 0, st>>>(
+            a.d_row_ptr, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, (int)a.num_rows,
+            k.n, n_shift, acc, wb);
     return launch_status();
 }
 

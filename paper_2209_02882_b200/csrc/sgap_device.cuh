@@ -113,14 +113,22 @@ __device__ __forceinline__ void prefetch_l1(const void *p) {
 }
 
 // Plain (read-modify-)write of an exclusively owned C tile.  C is written
-// exactly once per kernel, so the store is marked evict-first (st.global.cs)
-// to keep L2 for the B rows that are re-gathered.
+// exactly once per kernel, so 16-byte tiles are stored evict-first
+// (st.global.cs) to keep L2 for the B rows that are re-gathered.
 template <typename T, int V>
 __device__ __forceinline__ void store_vec(T *p, const Vec<T, V> &a, bool accumulate) {
     Vec<T, V> o = a;
     if (accumulate) {
 #pragma unroll
         for (int x = 0; x < V; ++x) o.v[x] += p[x];
+    }
+    if constexpr (sizeof(T) * V < 16) {
+        // narrow tiles: one warp writes a few bytes of a sector, its
+        // neighbours the rest -- an evict-first line would leave L2 before
+        // they land and cost a DRAM read-modify-write, so plain stores
+#pragma unroll
+        for (int x = 0; x < V; ++x) p[x] = o.v[x];
+        return;
     }
     if constexpr (sizeof(T) * V == 16) {
         if constexpr (sizeof(T) == 4)

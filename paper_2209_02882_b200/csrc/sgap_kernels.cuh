@@ -181,28 +181,31 @@ k_row_interleaved(const int *__restrict__ rp, const int *__restrict__ ci,
 // Rows longer than 32G: each lane folds its partial into float64 every 32
 // strided terms (shorter rows need no float64: <= 32 terms per lane).
 // ===========================================================================
-template <typename T, int V, int G>
+// IT: the index type of cells/groups -- unsigned 32-bit whenever M*N fits
+// (the host picks; ncu showed 2.4x the reference kernel's instruction count
+// at one cell per warp with 64-bit index math), else 64-bit.
+template <typename T, int V, int G, typename IT>
 __global__ void __launch_bounds__(256)
 k_row_reciprocal(const int *__restrict__ rp, const int *__restrict__ ci,
                  const T *__restrict__ av, const T *__restrict__ B, T *__restrict__ C,
-                 int M, int N, int accumulate, unsigned long long *wb) {
-    const long long cells = (long long)M * N;
-    const long long groups = (cells + V - 1) / V;
-    const long long total = groups * G;
-    const long long items = (total + 31) >> 5;
+                 int M, int N, int n_shift, int accumulate, unsigned long long *wb) {
+    constexpr int GPW = 32 / G;  // groups per warp
+    const IT cells = (IT)M * (IT)N;
+    const IT groups = (cells + V - 1) / V;
+    const IT items = (groups + GPW - 1) / GPW;
     const unsigned lane = lane_id();
-    const Divider byN = Divider::make(N);
+    const int j = (int)(lane % G);
     unsigned long long nwb = 0;
-    SGAP_WARP_LOOP(item, items) {
-        const long long h = item * 32 + lane;
-        const long long grp = h / G;
-        const int j = (int)(h % G);
-        const long long io0 = grp * V;
+    for (IT item = (IT)((blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5);
+         item < items; item += (IT)((gridDim.x * (unsigned long long)blockDim.x) >> 5)) {
+        const IT grp = item * GPW + lane / G;
+        const IT io0 = grp * V;
         const bool ok = io0 < cells;
-        const long long i = ok ? byN.div(io0) : 0;
-        const long long k0 = ok ? io0 - i * N : 0;
+        const IT i = ok ? (n_shift >= 0 ? io0 >> n_shift : io0 / (IT)N) : 0;
+        const IT k0 = ok ? io0 - i * (IT)N : 0;
         const int beg = ok ? __ldg(rp + i) : 0;
         const int end = ok ? __ldg(rp + i + 1) : 0;
+        const T *bk = B + k0;
         Vec<T, V> acc[kBatch];
 #pragma unroll
         for (int u = 0; u < kBatch; ++u) acc[u].zero();
@@ -211,31 +214,37 @@ k_row_reciprocal(const int *__restrict__ rp, const int *__restrict__ ci,
         // rows of <= 32G nonzeros (one segment: <= 32 terms per lane) sum in
         // the value type; longer ones fold into float64 after each segment
         const bool multi = end - beg > 32 * G;
-        for (int seg = beg + j; seg < end; seg += 32 * G) {
-            const int seg_end = min(seg + 32 * G, end);
-            int p = seg;
-            for (; p + (kBatch - 1) * G < seg_end; p += kBatch * G) {
-                int cc[kBatch];
-                T vv[kBatch];
-                Vec<T, V> bv[kBatch];
+        if (V == 1 && !multi) {
+            // one scalar column, <= 32 terms per lane: the plain strided loop
+            for (int p = beg + j; p < end; p += G)
+                acc[0].v[0] = fma(__ldg(av + p), __ldg(bk + (IT)__ldg(ci + p) * (IT)N), acc[0].v[0]);
+        } else {
+            for (int seg = beg + j; seg < end; seg += 32 * G) {
+                const int seg_end = min(seg + 32 * G, end);
+                int p = seg;
+                for (; p + (kBatch - 1) * G < seg_end; p += kBatch * G) {
+                    int cc[kBatch];
+                    T vv[kBatch];
+                    Vec<T, V> bv[kBatch];
 #pragma unroll
-                for (int u = 0; u < kBatch; ++u) {
-                    cc[u] = __ldg(ci + p + u * G);
-                    vv[u] = __ldg(av + p + u * G);
+                    for (int u = 0; u < kBatch; ++u) {
+                        cc[u] = __ldg(ci + p + u * G);
+                        vv[u] = __ldg(av + p + u * G);
+                    }
+#pragma unroll
+                    for (int u = 0; u < kBatch; ++u) ldg_vec<T, V>(bv[u], bk + (IT)cc[u] * (IT)N);
+#pragma unroll
+                    for (int u = 0; u < kBatch; ++u) fma_vec<T, V>(acc[u], vv[u], bv[u]);
                 }
+                for (; p < seg_end; p += G) {
+                    Vec<T, V> bv;
+                    ldg_vec<T, V>(bv, bk + (IT)__ldg(ci + p) * (IT)N);
+                    fma_vec<T, V>(acc[0], __ldg(av + p), bv);
+                }
+                if (multi) {
 #pragma unroll
-                for (int u = 0; u < kBatch; ++u) ldg_vec<T, V>(bv[u], B + (long long)cc[u] * N + k0);
-#pragma unroll
-                for (int u = 0; u < kBatch; ++u) fma_vec<T, V>(acc[u], vv[u], bv[u]);
-            }
-            for (; p < seg_end; p += G) {
-                Vec<T, V> bv;
-                ldg_vec<T, V>(bv, B + (long long)__ldg(ci + p) * N + k0);
-                fma_vec<T, V>(acc[0], __ldg(av + p), bv);
-            }
-            if (multi) {
-#pragma unroll
-                for (int u = 0; u < kBatch; ++u) fold<T, V>(tot, acc[u]);
+                    for (int u = 0; u < kBatch; ++u) fold<T, V>(tot, acc[u]);
+                }
             }
         }
         Vec<T, V> part;
@@ -248,7 +257,7 @@ k_row_reciprocal(const int *__restrict__ rp, const int *__restrict__ ci,
         }
         group_sum_vec<G, T, V>(part);
         if (ok && j == 0) {
-            store_vec<T, V>(C + i * N + k0, part, accumulate != 0);
+            store_vec<T, V>(C + i * (IT)N + k0, part, accumulate != 0);
             nwb += V;
         }
     }

@@ -202,15 +202,18 @@ def prepare_aux(k: LoweredKernel, a: DeviceCsr, *, stream=None, long_rows: bool 
             thr = int(long_threshold)
         if thr >= 0 and split_rows:
             chunk = int(L.sgap_long_row_chunk(ctypes.byref(ks), native_dtype(a.vals.dtype)))
+    longest = 0
+    if thr >= 0 and a.num_rows:  # plan-time host sync: does any row need the table?
+        longest = int((a.row_ptr[1:] - a.row_ptr[:-1]).max().item())
+        if longest <= thr and chunk == 0:
+            thr = -1  # no long rows: no table, no fold launch
     aux.rowid = torch.empty(max(a.nnz, 4), dtype=torch.int32, device=dev)
     _native.check(L.sgap_row_ids(a.row_ptr.data_ptr(), a.num_rows, a.nnz, thr, chunk,
                                  aux.rowid.data_ptr(), _stream_handle(stream)), "sgap_row_ids")
     if thr < 0:
         return aux
     cap = int(L.sgap_long_row_capacity(a.nnz, thr, chunk))
-    if a.num_rows:  # plan-time host sync: is the error-free pass needed at all?
-        longest = int((a.row_ptr[1:] - a.row_ptr[:-1]).max().item())
-        aux.has_exact_rows = int(longest > int(L.sgap_exact_row_length()))
+    aux.has_exact_rows = int(longest > int(L.sgap_exact_row_length()))
     aux.long_threshold = thr
     aux.long_chunk = chunk
     aux.long_capacity = cap
