@@ -44,6 +44,9 @@ sys.path.insert(0, str(ROOT))
 METRIC = "SpMM GFLOP/s (2*nnz*N/t)"
 UNIT = "GFLOP/s"
 FALLBACK_HBM_GBS = 6650.0
+# B-row gather ceiling of config 2 (8.2 GB of 512-B rows in 0.416 ms; the
+# same probe reads 19-20 TB/s from any L2-resident table): measured, not nominal
+GATHER_CEILING_TBS = 19.8
 
 
 # --------------------------------------------------------------------------- setup
@@ -342,6 +345,17 @@ def main():
             "kernel_ms_covers": "the whole SpMM call (zero-fill pre-pass + main kernel + "
                                 "long-row fold), CUDA events on the launch stream",
             "kernel_share": kernel_ms / ms_per_step}
+    # what actually binds on power-law matrices: every nonzero gathers a whole
+    # B row through L2 (profiles/r01_gather_ceiling.md)
+    gbytes = a.nnz * n * 4
+    roof["b_gather"] = {
+        "bytes": gbytes, "achieved_tbs": gbytes / (kernel_ms * 1e-3) / 1e12,
+        "ceiling_tbs": GATHER_CEILING_TBS if (cfg == 2 and world == 1) else None,
+        "ceiling_source": "gather-only kernel over config 2's col_idx in CSR order, same B "
+                          "layout (tools/experiments/l2_gather_probe.cu), best of 5 on B200",
+    }
+    if roof["b_gather"]["ceiling_tbs"]:
+        roof["b_gather"]["frac"] = roof["b_gather"]["achieved_tbs"] / GATHER_CEILING_TBS
 
     # ---- end to end through host buffers (pipelined: B up, then per row
     # block A up / SpMM / C down on three streams)

@@ -53,13 +53,23 @@ __global__ void __launch_bounds__(256) k_gather(const int *__restrict__ ci, long
     if (acc.x == 1.2345f) C[0] = acc.y + acc.z + acc.w;
 }
 
-struct Acc {  // NUM 0: float32; 1: float32 folded into float64 every 8; 2: Kahan float32
+struct Acc {  // NUM 0: float32; 1: float32 folded into float64 every 8; 2: Kahan float32;
+              // 3: float32 partials TwoSum-folded into a (hi, lo) float32 pair every 8
     float4 a, c;
     double4 t;
+    float4 h, l;
 };
+__device__ __forceinline__ void twosum_fold(float &hi, float &lo, float a) {
+    const float s = __fadd_rn(hi, a);
+    const float bb = __fsub_rn(s, hi);
+    const float err = __fadd_rn(__fsub_rn(hi, __fsub_rn(s, bb)), __fsub_rn(a, bb));
+    hi = s;
+    lo = __fadd_rn(lo, err);
+}
 template <int NUM> __device__ __forceinline__ void acc_zero(Acc &s) {
     s.a = make_float4(0, 0, 0, 0); s.c = s.a;
     if (NUM == 1) s.t = make_double4(0, 0, 0, 0);
+    if (NUM == 3) { s.h = s.a; s.l = s.a; }
 }
 __device__ __forceinline__ float kadd(float &sum, float &c, float x) {
     const float y = x - c; const float t = sum + y; c = (t - sum) - y; sum = t; return t;
@@ -74,6 +84,11 @@ template <int NUM> __device__ __forceinline__ void acc_fma(Acc &s, float v, floa
     }
 }
 template <int NUM> __device__ __forceinline__ void acc_fold(Acc &s) {
+    if (NUM == 3) {
+        twosum_fold(s.h.x, s.l.x, s.a.x); twosum_fold(s.h.y, s.l.y, s.a.y);
+        twosum_fold(s.h.z, s.l.z, s.a.z); twosum_fold(s.h.w, s.l.w, s.a.w);
+        s.a = make_float4(0, 0, 0, 0);
+    }
     if (NUM == 1) {
         s.t.x += s.a.x; s.t.y += s.a.y; s.t.z += s.a.z; s.t.w += s.a.w;
         s.a = make_float4(0, 0, 0, 0);
@@ -82,6 +97,7 @@ template <int NUM> __device__ __forceinline__ void acc_fold(Acc &s) {
 template <int NUM> __device__ __forceinline__ float4 acc_out(Acc &s) {
     acc_fold<NUM>(s);
     if (NUM == 1) return make_float4((float)s.t.x, (float)s.t.y, (float)s.t.z, (float)s.t.w);
+    if (NUM == 3) return make_float4(s.h.x + s.l.x, s.h.y + s.l.y, s.h.z + s.l.z, s.h.w + s.l.w);
     return s.a;
 }
 
@@ -250,9 +266,9 @@ int main(int argc, char **argv) {
             check(nm, ms);                                                                     \
         } else printf("%-28s %.3f ms\n", nm, ms);                                             \
     }
-    STAGEDN(4, 256, 0, 1, 0) STAGEDN(4, 256, 0, 1, 1) STAGEDN(4, 256, 0, 1, 2)
-    STAGEDN(8, 256, 0, 1, 0) STAGEDN(8, 256, 0, 1, 1) STAGEDN(8, 256, 0, 1, 2)
-    STAGEDN(4, 256, 0, 4, 1) STAGEDN(8, 256, 0, 3, 1) STAGEDN(4, 256, 2, 1, 1) STAGEDN(4, 512, 0, 1, 1)
+    STAGEDN(4, 256, 0, 4, 0) STAGEDN(4, 256, 0, 4, 1) STAGEDN(4, 256, 0, 4, 3)
+    STAGEDN(8, 256, 0, 3, 0) STAGEDN(8, 256, 0, 3, 1) STAGEDN(8, 256, 0, 3, 3)
+    STAGEDN(4, 256, 2, 4, 0) STAGEDN(4, 256, 2, 4, 1) STAGEDN(4, 256, 2, 4, 3)
     float zms = timeit([&] { cudaMemsetAsync(C, 0, (size_t)M * N * 4); });
     printf("%-28s %.3f ms\n", "memset C alone", zms);
     return 0;
