@@ -389,9 +389,34 @@ def main():
         te = torch.tensor([e0.elapsed_time(e1) / e_steps], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        # the PCIe floor of one step: the same bytes up and down at once, no compute
+        s_up, s_dn = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        d_rp, d_ci, d_v = (torch.empty_like(x, device=dev) for x in (h_rp, h_ci, h_v))
+        d_b, d_c = torch.empty_like(h_b, device=dev), torch.empty_like(h_c, device=dev)
+
+        def copies():
+            s_up.wait_stream(stream)
+            s_dn.wait_stream(stream)
+            with torch.cuda.stream(s_up):
+                for dst, src in ((d_rp, h_rp), (d_ci, h_ci), (d_v, h_v), (d_b, h_b)):
+                    dst.copy_(src, non_blocking=True)
+            with torch.cuda.stream(s_dn):
+                h_c.copy_(d_c, non_blocking=True)
+            stream.wait_stream(s_up)
+            stream.wait_stream(s_dn)
+
+        floor = float("inf")
+        for _ in range(3):
+            e0.record(stream)
+            copies()
+            e1.record(stream)
+            e1.synchronize()
+            floor = min(floor, e0.elapsed_time(e1))
+        del d_rp, d_ci, d_v, d_b, d_c
         e2e = {"value": 2.0 * total_nnz * n / (float(te.item()) * 1e6), "unit": UNIT,
                "h2d_bytes_per_step": pipe.h2d_bytes(), "d2h_bytes_per_step": pipe.d2h_bytes(),
                "ms_per_step": float(te.item()), "steps": e_steps,
+               "pcie_floor_ms": floor, "frac_of_pcie_floor": floor / float(te.item()),
                "path": f"pinned host A,B -> {args.e2e_blocks} row blocks: H2D / plan + SpMM / "
                        "D2H C overlapped on 3 streams, device buffers double-buffered across "
                        "steps (paper_2209_02882_b200.pipeline.HostSpmm)"}

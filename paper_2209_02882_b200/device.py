@@ -174,7 +174,7 @@ class KernelAux:
 
 def prepare_aux(k: LoweredKernel, a: DeviceCsr, *, stream=None, long_rows: bool = True,
                 long_threshold: int | None = None, block_starts: bool = True,
-                split_rows: bool = False) -> KernelAux:
+                split_rows: bool = False, row_ptr_host=None) -> KernelAux:
     """Per-matrix side data of kernel ``k``: block starts and per-position row
     ids (nnz families) and, for float32 values, the long-row table
     (include/sgap.h: sgap_block_starts, sgap_row_ids, sgap_prepare_long_rows).
@@ -182,7 +182,10 @@ def prepare_aux(k: LoweredKernel, a: DeviceCsr, *, stream=None, long_rows: bool 
     ``split_rows``: nnz-multiple rows that straddle a g-chunk boundary also
     go to the float64 table (every split row summed in float64, no zero-fill
     pre-pass).  Off by default: on config 2 its float64 flushes cost more
-    than the pre-pass they replace (0.764 vs 0.754 ms at g=512)."""
+    than the pre-pass they replace (0.764 vs 0.754 ms at g=512).
+
+    ``row_ptr_host``: the same row_ptr on the host (numpy); given, planning
+    never synchronises with the device (the longest-row check runs on it)."""
     eb = k.family in ("nnz-one", "nnz-multiple")
     a.check()
     starts = None
@@ -203,8 +206,12 @@ def prepare_aux(k: LoweredKernel, a: DeviceCsr, *, stream=None, long_rows: bool 
         if thr >= 0 and split_rows:
             chunk = int(L.sgap_long_row_chunk(ctypes.byref(ks), native_dtype(a.vals.dtype)))
     longest = 0
-    if thr >= 0 and a.num_rows:  # plan-time host sync: does any row need the table?
-        longest = int((a.row_ptr[1:] - a.row_ptr[:-1]).max().item())
+    if thr >= 0 and a.num_rows:  # does any row need the table?
+        if row_ptr_host is not None:
+            rph = np.asarray(row_ptr_host)
+            longest = int((rph[1:] - rph[:-1]).max())
+        else:  # plan-time host sync
+            longest = int((a.row_ptr[1:] - a.row_ptr[:-1]).max().item())
         if longest <= thr and chunk == 0:
             thr = -1  # no long rows: no table, no fold launch
     aux.rowid = torch.empty(max(a.nnz, 4), dtype=torch.int32, device=dev)
