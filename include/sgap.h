@@ -97,7 +97,10 @@ typedef struct {
     int32_t hw_variant;     /* nnz-multiple walk: 0 auto, 1 register-staged,
                                2 TMA-staged (cp.async.bulk + mbarrier ring),
                                3/4 lane-staged (warp per chunk, 4/8 B-row
-                               gathers in flight; needs N/c >= 32)           */
+                               gathers in flight; needs N/c >= 32).
+                               row-multiple: 0/1 logical mapping, 2
+                               interleaved rows, 3/4 interleaved + warp per
+                               row, lane-staged A (needs N/c == 32)          */
 } sgap_kernel_t;
 
 /* CSR operand on the device (matrices.py:38-86 with int32 indices). */

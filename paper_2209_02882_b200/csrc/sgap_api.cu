@@ -54,13 +54,29 @@ bool aligned(const void *p, size_t bytes) {
 
 // hw_variant for row-multiple: 0/1 the logical mapping (thread (rg, t) owns
 // rows rg*g .. rg*g+g-1), 2 the interleaved mapping (a CTA's warps on adjacent
-// rows; needs N/c <= CTA size).
+// rows; needs N/c <= CTA size), 3/4 the interleaved mapping with a warp per
+// row and lane-staged A (8/4 gathers in flight; needs N/c == 32).
 template <typename T, int V>
 int run_row_multiple(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
                      int acc, cudaStream_t st) {
     const int N = k.n, L = N / V;
     const int blk = k.hw_block > 0 ? k.hw_block : kHwBlock;
     const int vec4 = aligned(a.d_col_idx, 16) && aligned(a.d_vals, 16);
+    if (k.hw_variant == 3 || k.hw_variant == 4) {  // lane-staged, a warp per row
+        if (L != 32) return SGAP_ERR_ARG;
+        const long long tile_rows = (long long)(blk / 32) * k.g;
+        const long long tiles = ceil_div(a.num_rows, tile_rows);
+        const unsigned ctas = (unsigned)(tiles < (1LL << 30) ? (tiles > 0 ? tiles : 1) : (1LL << 30));
+        if (k.hw_variant == 3)
+            k_row_staged<T, V, 8><<<ctas, blk, 0, st>>>(a.d_row_ptr, a.d_col_idx,
+                                                         static_cast<const T *>(a.d_vals), B, C,
+                                                         (int)a.num_rows, N, k.g, vec4, acc);
+        else
+            k_row_staged<T, V, 4><<<ctas, blk, 0, st>>>(a.d_row_ptr, a.d_col_idx,
+                                                         static_cast<const T *>(a.d_vals), B, C,
+                                                         (int)a.num_rows, N, k.g, vec4, acc);
+        return launch_status();
+    }
     if (k.hw_variant == 2) {
         if (L > blk) return SGAP_ERR_ARG;
         const long long tile_rows = (long long)(blk / L) * k.g;

@@ -172,6 +172,121 @@ k_row_interleaved(const int *__restrict__ rp, const int *__restrict__ ci,
     }
 }
 
+// The interleaved mapping with a whole warp per row (hw variant 3, N/c == 32):
+// per 32 positions each lane loads one position's (col, val) -- one coalesced
+// request per array instead of per-lane broadcast loads with an alignment
+// prologue and a tail -- and U B-row gathers go out back to back from
+// shuffled columns.  A short tail group re-gathers a valid column and skips
+// its FMAs.  Each (row, tile) is still one serial sum in position order: in
+// float32 for rows of <= 64 nonzeros (stencil rows: 27), folded into float64
+// every 32 positions beyond that, error-free past kExactRow (rb_row).
+// ncu on config 4 (27-pt stencil, N=128) for the broadcast walk: 24.5 warp
+// instructions per nonzero, 47% warps active, long-scoreboard 62%.
+template <typename T, int V, int U>
+__device__ __forceinline__ Vec<double, V> rb_row_staged(const int *__restrict__ ci,
+                                                        const T *__restrict__ av, int beg,
+                                                        int end, const T *__restrict__ bk,
+                                                        int N) {
+    const unsigned lane = lane_id();
+    Vec<T, V> acc;
+    acc.zero();
+    Vec<double, V> tot;
+    tot.zero();
+    const bool longrow = end - beg > 64;
+    for (int s = beg; s < end; s += 32) {
+        const int q = s + (int)lane;
+        const int c_l = q < end ? __ldg(ci + q) : __ldg(ci + s);
+        const T v_l = q < end ? __ldg(av + q) : T(0);
+        const int nv = min(32, end - s);
+        for (int j = 0; j < nv; j += U) {
+            Vec<T, V> b[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                gather_vec<T, V>(b[u], bk + (long long)__shfl_sync(kFull, c_l, (j + u) & 31) * N);
+            if (j + U <= nv) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) fma_vec<T, V>(acc, __shfl_sync(kFull, v_l, j + u), b[u]);
+            } else {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const T v = __shfl_sync(kFull, v_l, (j + u) & 31);
+                    if (j + u < nv) fma_vec<T, V>(acc, v, b[u]);
+                }
+            }
+        }
+        if (longrow) fold<T, V>(tot, acc);
+    }
+    fold<T, V>(tot, acc);
+    return tot;
+}
+
+// Rows of <= 64 nonzeros: the float32 walk alone (no float64 state live, so
+// the kernel keeps few registers and many warps); longer rows go through a
+// call so their float64 state does not set the kernel's register count.
+template <typename T, int V, int U>
+__device__ __forceinline__ Vec<T, V> rb_short_staged(const int *__restrict__ ci,
+                                                     const T *__restrict__ av, int beg, int end,
+                                                     const T *__restrict__ bk, int N) {
+    const unsigned lane = lane_id();
+    Vec<T, V> acc;
+    acc.zero();
+    for (int s = beg; s < end; s += 32) {
+        const int q = s + (int)lane;
+        const int c_l = q < end ? __ldg(ci + q) : __ldg(ci + s);
+        const T v_l = q < end ? __ldg(av + q) : T(0);
+        const int nv = min(32, end - s);
+        for (int j = 0; j < nv; j += U) {
+            Vec<T, V> b[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                gather_vec<T, V>(b[u], bk + (long long)__shfl_sync(kFull, c_l, (j + u) & 31) * N);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const T v = __shfl_sync(kFull, v_l, (j + u) & 31);
+                if (j + u < nv) fma_vec<T, V>(acc, v, b[u]);
+            }
+        }
+    }
+    return acc;
+}
+
+template <typename T, int V, int U>
+__device__ __noinline__ void rb_long_staged(const int *__restrict__ ci, const T *__restrict__ av,
+                                            int beg, int end, const T *__restrict__ bk, int N,
+                                            int vec4, T *__restrict__ out, int accumulate) {
+    const Vec<double, V> tot = (sizeof(T) == 4 && end - beg > kExactRow)
+                                   ? rb_row<T, V>(ci, av, beg, end, bk, N, vec4 != 0)
+                                   : rb_row_staged<T, V, U>(ci, av, beg, end, bk, N);
+    store_vec<T, V>(out, narrow<T, V>(tot), accumulate != 0);
+}
+
+template <typename T, int V, int U>
+__global__ void __launch_bounds__(256, U >= 8 ? 4 : 5)
+k_row_staged(const int *__restrict__ rp, const int *__restrict__ ci, const T *__restrict__ av,
+             const T *__restrict__ B, T *__restrict__ C, int M, int N, int g, int vec4,
+             int accumulate) {
+    const int warps = (int)(blockDim.x >> 5);
+    const int w = (int)(threadIdx.x >> 5);
+    const long long kcol = (long long)lane_id() * V;
+    const long long tile_rows = (long long)warps * g;
+    const long long tiles = ((long long)M + tile_rows - 1) / tile_rows;
+    for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        for (int s = 0; s < g; ++s) {
+            const long long i = tile * tile_rows + (long long)s * warps + w;
+            if (i >= M) break;
+            const int beg = __ldg(rp + i), end = __ldg(rp + i + 1);
+            if (end - beg > 64) {
+                rb_long_staged<T, V, U>(ci, av, beg, end, B + kcol, N, vec4, C + i * N + kcol,
+                                        accumulate);
+            } else {
+                store_vec<T, V>(C + i * N + kcol,
+                                rb_short_staged<T, V, U>(ci, av, beg, end, B + kcol, N),
+                                accumulate != 0);
+            }
+        }
+    }
+}
+
 // ===========================================================================
 // RB + parallel group reduction: row:1/g,col:c,r:g (row-reciprocal).
 // A group of G lanes owns c consecutive fused cells io = i*N + k (one row, c

@@ -21,6 +21,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+from . import _native
 from .device import DeviceCsr, prepare_aux, spmm
 from .lowering import KernelConfig, LoweredKernel, lower
 from .space import enumerate_space, parse_point
@@ -90,7 +91,8 @@ def candidates(n: int, p_values=(256, 1024), g_values=GPU_G_VALUES,
                variants: bool = True) -> list[Candidate]:
     """Every templated point at dense width n for each p (deduplicated by
     the kernel it lowers to); nnz-multiple points come with both walks
-    (register-staged and TMA-staged) when ``variants``."""
+    (register-staged, TMA-staged, lane-staged) and row-multiple points with
+    the logical, interleaved and warp-per-row mappings when ``variants``."""
     out, seen = [], set()
     for p in p_values:
         cfg = KernelConfig(n=n, p=p)
@@ -103,9 +105,11 @@ def candidates(n: int, p_values=(256, 1024), g_values=GPU_G_VALUES,
                 continue
             seen.add(key)
             if variants and tpl.family == "nnz-multiple":
-                out.extend(Candidate(str(pt), p, 0, v) for v in (1, 2))
+                vs = (1, 2, 3) if n // tpl.c >= 32 else (1, 2)
+                out.extend(Candidate(str(pt), p, 0, v) for v in vs)
             elif variants and tpl.family == "row-multiple" and n // tpl.c <= 256:
-                out.extend(Candidate(str(pt), p, 0, v) for v in (0, 2))
+                vs = (0, 2, 4) if n // tpl.c == 32 else (0, 2)
+                out.extend(Candidate(str(pt), p, 0, v) for v in vs)
             else:
                 out.append(Candidate(str(pt), p))
     return out
@@ -162,7 +166,8 @@ def heuristic(stats: MatrixStats, n: int) -> Candidate:
             pt = f"row:4,col:{col(widest)},r:1"
             p = _first_p(pt, n)
             if p is not None:
-                return Candidate(pt, p, 0, 2)
+                # a warp per row when N/c == 32 (config 4 N=128: 3.35 vs 3.82 ms)
+                return Candidate(pt, p, 0, 4 if n // widest == 32 else 2)
         pt = f"row:1,col:{col(widest)},r:1"
         return Candidate(pt, _first_p(pt, n) or 256)
     c = widest if n >= 16 else min(widest, max(1, n // 4))
@@ -190,8 +195,13 @@ def autotune(a: DeviceCsr, b: torch.Tensor, c: torch.Tensor, n: int, cands, *, r
         if k is None:
             continue
         aux = prepare_aux(k, a, stream=stream)
-        spmm(k, a, b, c, aux=aux, hw_block=cand.hw_block, hw_variant=cand.hw_variant,
-             stream=stream)  # warm
+        try:
+            spmm(k, a, b, c, aux=aux, hw_block=cand.hw_block, hw_variant=cand.hw_variant,
+                 stream=stream)  # warm
+        except _native.SgapError as e:
+            if e.status != _native.ERR_ARG:  # only "variant not applicable" is skipped
+                raise
+            continue
         best = float("inf")
         for i in range(reps):
             e0.record(stream)

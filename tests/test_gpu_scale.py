@@ -79,6 +79,19 @@ def test_config2_long_chunk_walks():
     print(_check(g, 128, pts))
 
 
+def test_row_staged_variants():
+    """Row-multiple with a warp per row (hw variants 3/4, N/c == 32): stencil
+    rows (<= 27, the float32 path) and R-MAT hub rows (> 64, the float64
+    path) at N = 128 / 64 / 32."""
+    st = G.stencil27(64, device="cuda")
+    rm = G.rmat(16, 16, seed=5, device="cuda")
+    for g in (st, rm):
+        print(_check(g, 128, [("row:4,col:4,r:1", 256, 3), ("row:4,col:4,r:1", 256, 4),
+                              ("row:1,col:4,r:1", 256, 4), ("row:16,col:4,r:1", 256, 4)]))
+        print(_check(g, 64, [("row:4,col:2,r:1", 256, 4), ("row:2,col:2,r:1", 256, 3)]))
+        print(_check(g, 32, [("row:4,col:1,r:1", 256, 4)]))
+
+
 def test_stencil_small_n():
     g = G.stencil27(48, device="cuda")
     assert g.nnz == (3 * 48 - 2) ** 3
