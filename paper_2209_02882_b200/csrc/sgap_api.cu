@@ -476,14 +476,15 @@ int64_t sgap_long_row_threshold(const sgap_kernel_t *k, int32_t dtype) {
     // A row split over m chunk flushes accumulates m float32 roundings of
     // partial sums that can be far larger than the row's final value (a
     // power-law row whose column sum cancels).  nnz-multiple: rows longer than
-    // clamp(4g, 1024, 32g) (min 128) go to the float64 table -- at g = 512
+    // clamp(16g, 2048, 32g) (min 128) go to the float64 table -- at g = 512
     // the bound 32g let 32 flushes of 512-term partials reach 1.0e-5 on
-    // config 2, and at g = 2 the bound 1024 let 512 flushes reach 1.1e-5.
+    // config 2 (16g: 4.5e-6), at g = 2 the bound 1024 let 512 flushes reach
+    // 1.1e-5; 4g cost config 3 6% in float64 atomics for no accuracy gain.
     // nnz-one flushes r-term segment sums: rows past 32r (min 128).
     if (k->family == SGAP_NNZ_MULTIPLE) {
-        // <= 32 flushes of short partials (small g), <= 4 of long ones
-        long long t = 4LL * k->g;
-        if (t < 1024) t = 1024;
+        // <= 32 flushes of short partials (small g), <= 16 of long ones
+        long long t = 16LL * k->g;
+        if (t < 2048) t = 2048;
         if (t > 32LL * k->g) t = 32LL * k->g;
         return t < 128 ? 128 : t;
     }

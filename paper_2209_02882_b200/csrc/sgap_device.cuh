@@ -251,9 +251,13 @@ struct LongRows {
 constexpr int kLongFlag = (int)0x80000000u;
 constexpr int kExactFlag = 0x40000000;
 constexpr int kRowMask = 0x3fffffff;
-// sqrt(n) * rms(a*b) * 2^-24 reaches ~1e-5 near n ~ 2e5 for U[-1,1) data;
-// rows beyond this take the error-free accumulate (TwoProduct + TwoSum).
-constexpr int kExactRow = 65536;
+// Float32 product rounding alone is a random walk of std ~3.4e-8 *
+// sqrt(n) * rms(a*b); over millions of outputs its 5-sigma tail reaches the
+// 1e-5 bound (metric max|err|/(|want|+1)) near n ~ 2e4: config 3's
+// Chung-Lu hub rows (~20-60k nonzeros) measured 1.33e-5 with plain float32
+// products.  Rows beyond this take the error-free accumulate (TwoProduct +
+// TwoSum); at 4096 the 5-sigma tail stays under ~4.5e-6.
+constexpr int kExactRow = 4096;
 
 // One atomic writeback of a (row, column tile) partial; `rid` is a row id
 // (possibly flagged long).

@@ -265,24 +265,75 @@ __global__ void __launch_bounds__(256, U >= 8 ? 4 : 5)
 k_row_staged(const int *__restrict__ rp, const int *__restrict__ ci, const T *__restrict__ av,
              const T *__restrict__ B, T *__restrict__ C, int M, int N, int g, int vec4,
              int accumulate) {
+    // Rows of <= 32 nonzeros (stencil rows) are software-pipelined across the
+    // warp's rows: the next row's bounds load at the start of a row and its
+    // (col, val) right after this row's first gathers, so a row's dependency
+    // chain (row_ptr -> A -> B) overlaps the previous row's gathers.
     const int warps = (int)(blockDim.x >> 5);
     const int w = (int)(threadIdx.x >> 5);
-    const long long kcol = (long long)lane_id() * V;
+    const int lane = (int)lane_id();
+    const long long kcol = (long long)lane * V;
+    const T *bk = B + kcol;
     const long long tile_rows = (long long)warps * g;
     const long long tiles = ((long long)M + tile_rows - 1) / tile_rows;
     for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        long long i = tile * tile_rows + w;
+        if (i >= M) continue;
+        int beg = __ldg(rp + i), end = __ldg(rp + i + 1);
+        int c_l = 0;
+        T v_l = T(0);
+        if (end - beg <= 32 && end > beg) {
+            c_l = __ldg(ci + (beg + lane < end ? beg + lane : beg));
+            v_l = beg + lane < end ? __ldg(av + beg + lane) : T(0);
+        }
         for (int s = 0; s < g; ++s) {
-            const long long i = tile * tile_rows + (long long)s * warps + w;
-            if (i >= M) break;
-            const int beg = __ldg(rp + i), end = __ldg(rp + i + 1);
-            if (end - beg > 64) {
-                rb_long_staged<T, V, U>(ci, av, beg, end, B + kcol, N, vec4, C + i * N + kcol,
-                                        accumulate);
-            } else {
-                store_vec<T, V>(C + i * N + kcol,
-                                rb_short_staged<T, V, U>(ci, av, beg, end, B + kcol, N),
-                                accumulate != 0);
+            const long long inext = i + warps;
+            const bool has_next = s + 1 < g && inext < M;
+            int nbeg = 0, nend = 0;
+            if (has_next) {
+                nbeg = __ldg(rp + inext);
+                nend = __ldg(rp + inext + 1);
             }
+            int c_n = 0;
+            T v_n = T(0);
+            auto load_next = [&]() {
+                if (has_next && nend - nbeg <= 32 && nend > nbeg) {
+                    c_n = __ldg(ci + (nbeg + lane < nend ? nbeg + lane : nbeg));
+                    v_n = nbeg + lane < nend ? __ldg(av + nbeg + lane) : T(0);
+                }
+            };
+            if (end - beg > 64) {
+                rb_long_staged<T, V, U>(ci, av, beg, end, bk, N, vec4, C + i * N + kcol, accumulate);
+                load_next();
+            } else if (end - beg > 32) {
+                load_next();
+                store_vec<T, V>(C + i * N + kcol, rb_short_staged<T, V, U>(ci, av, beg, end, bk, N),
+                                accumulate != 0);
+            } else {
+                Vec<T, V> acc;
+                acc.zero();
+                const int nv = end - beg;
+                for (int j = 0; j < nv; j += U) {
+                    Vec<T, V> b[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        gather_vec<T, V>(b[u], bk + (long long)__shfl_sync(kFull, c_l, (j + u) & 31) * N);
+                    if (j == 0) load_next();
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const T v = __shfl_sync(kFull, v_l, (j + u) & 31);
+                        if (j + u < nv) fma_vec<T, V>(acc, v, b[u]);
+                    }
+                }
+                if (nv == 0) load_next();
+                store_vec<T, V>(C + i * N + kcol, acc, accumulate != 0);
+            }
+            if (!has_next) break;
+            i = inext;
+            beg = nbeg;
+            end = nend;
+            c_l = c_n;
+            v_l = v_n;
         }
     }
 }
@@ -329,7 +380,23 @@ k_row_reciprocal(const int *__restrict__ rp, const int *__restrict__ ci,
         // rows of <= 32G nonzeros (one segment: <= 32 terms per lane) sum in
         // the value type; longer ones fold into float64 after each segment
         const bool multi = end - beg > 32 * G;
-        if (V == 1 && !multi) {
+        if (sizeof(T) == 4 && end - beg > kExactRow) {
+            // hub rows: error-free products and sums (float32 product rounding
+            // grows like sqrt(row length): config 3 measured 1.2e-5 without)
+            Vec<T, V> lo;
+            lo.zero();
+            int since = 0;
+            for (int p = beg + j; p < end; p += G) {
+                Vec<T, V> bv;
+                ldg_vec<T, V>(bv, bk + (IT)__ldg(ci + p) * (IT)N);
+                fma_vec_exact<T, V>(acc[0], lo, __ldg(av + p), bv);
+                if (++since == kFoldEvery) {
+                    fold2<T, V>(tot, acc[0], lo);
+                    since = 0;
+                }
+            }
+            fold2<T, V>(tot, acc[0], lo);
+        } else if (V == 1 && !multi) {
             // one scalar column, <= 32 terms per lane: the plain strided loop
             for (int p = beg + j; p < end; p += G)
                 acc[0].v[0] = fma(__ldg(av + p), __ldg(bk + (IT)__ldg(ci + p) * (IT)N), acc[0].v[0]);
@@ -362,15 +429,18 @@ k_row_reciprocal(const int *__restrict__ rp, const int *__restrict__ ci,
                 }
             }
         }
-        Vec<T, V> part;
-        if (multi) {
-            part = narrow<T, V>(tot);
-        } else {
-            part = acc[0];
+        Vec<T, V> part = acc[0];
 #pragma unroll
-            for (int u = 1; u < kBatch; ++u) add_vec<T, V>(part, acc[u]);
+        for (int u = 1; u < kBatch; ++u) add_vec<T, V>(part, acc[u]);
+        if (__any_sync(kFull, multi)) {  // long rows: the group sum in float64 too
+            Vec<double, V> td;
+#pragma unroll
+            for (int x = 0; x < V; ++x) td.v[x] = multi ? tot.v[x] : (double)part.v[x];
+            group_sum_vec<G, double, V>(td);
+            part = narrow<T, V>(td);
+        } else {
+            group_sum_vec<G, T, V>(part);
         }
-        group_sum_vec<G, T, V>(part);
         if (ok && j == 0) {
             store_vec<T, V>(C + i * (IT)N + k0, part, accumulate != 0);
             nwb += V;
@@ -411,6 +481,11 @@ k_nnz_one(const int *__restrict__ rowid, const int *__restrict__ ci, const T *__
     const int ql = (int)(lane & (unsigned)(Q - 1));
     const int tl = (int)(lane / (unsigned)Q);
     const bool table = lr.threshold >= 0;
+    // zero-extended lanes resolve to row M-1; when that row has nonzeros they
+    // must carry its table flags too, or a run whose tail lane is padding
+    // would send the row's sum to C where the table fold overwrites it
+    const int last_rid = nnz > 0 ? __ldg(rowid + nnz - 1) : (M - 1);
+    const int pad_rid = (last_rid & kRowMask) == M - 1 ? last_rid : (M - 1);
     unsigned long long nwb = 0;
     SGAP_WARP_LOOP(item, items) {
         for (int tt = 0; tt < NT; tt += TW) {
@@ -430,38 +505,45 @@ k_nnz_one(const int *__restrict__ rowid, const int *__restrict__ ci, const T *__
                 // row owning the position; zero-extended lanes past nnz keep
                 // the clamped search row M-1 (lowering.py:476-488 with the
                 // window of the last block)
-                const int rid = in_nnz ? __ldg(rowid + pos) : (M - 1);
+                const int rid = in_nnz ? __ldg(rowid + pos) : pad_rid;
                 const int row = rid & kRowMask;
                 const int col = in_nnz ? __ldg(ci + pos) : 0;
                 const T a = in_nnz ? __ldg(av + pos) : T(0);
                 SegLanes sl{};
                 if constexpr (R > 1) sl = seg_lanes<R, int>(row, in_grid);
-                Vec<T, V> prod;
-                prod.zero();
-                if (in_nnz && tok) {
-                    Vec<T, V> bv;
-                    ldg_vec<T, V>(bv, B + (long long)col * N + kcol);
+                Vec<T, V> bv;
+                bv.zero();
+                if (in_nnz && tok) ldg_vec<T, V>(bv, B + (long long)col * N + kcol);
+                const bool writer = (R == 1 ? in_nnz : sl.tail) && tok;
+                // Warps that touch a float64-table row (hub rows) form exact
+                // float64 products and segment sums: float32 product rounding
+                // alone grows like sqrt(row length) and breaks 1e-5 on
+                // config 3's hub rows.  Other warps stay in float32.
+                if (table && __any_sync(kFull, rid < 0)) {
+                    Vec<double, V> pd;
+#pragma unroll
+                    for (int x = 0; x < V; ++x) pd.v[x] = (double)a * (double)bv.v[x];
+                    if constexpr (R > 1) seg_scan_vec<R, double, V>(pd, sl.dist);
+                    if (writer) {
+                        nwb += V;
+                        if (rid < 0) {
+                            if (row != prow) {
+                                if (prow >= 0) flush_row<T, V>(C, N, prow | kLongFlag, kcol, pend, lr);
+                                prow = row;
+                                pend.zero();
+                            }
+                            add_vec<double, V>(pend, pd);
+                        } else {
+                            red_vec<T, V>(C + (long long)row * N + kcol, narrow<T, V>(pd));
+                        }
+                    }
+                } else {
+                    Vec<T, V> prod;
 #pragma unroll
                     for (int x = 0; x < V; ++x) prod.v[x] = a * bv.v[x];
-                }
-                bool writer;
-                if constexpr (R == 1) {
-                    writer = in_nnz && tok;
-                } else {
-                    seg_scan_vec<R, T, V>(prod, sl.dist);
-                    writer = sl.tail && tok;
-                }
-                if (writer) {
-                    nwb += V;
-                    if (table && rid < 0) {
-                        if (row != prow) {
-                            if (prow >= 0) flush_row<T, V>(C, N, prow | kLongFlag, kcol, pend, lr);
-                            prow = row;
-                            pend.zero();
-                        }
-#pragma unroll
-                        for (int x = 0; x < V; ++x) pend.v[x] += (double)prod.v[x];
-                    } else {
+                    if constexpr (R > 1) seg_scan_vec<R, T, V>(prod, sl.dist);
+                    if (writer) {
+                        nwb += V;
                         red_vec<T, V>(C + (long long)row * N + kcol, prod);
                     }
                 }
@@ -861,7 +943,9 @@ k_nnz_multiple_exact(const int *__restrict__ rowid, const int *__restrict__ ci,
     for (int li = blockIdx.x; li < count; li += gridDim.x) {
         const int r = __ldg(lr.rows + li);
         const long long rs = __ldg(rp + r), re = __ldg(rp + r + 1);
-        if (re - rs <= kExactRow) continue;
+        // exactly the rows k_row_ids flagged exact (split-row routing also
+        // puts shorter rows in the table; those stay with the main walk)
+        if (re - rs <= kExactRow || re - rs <= lr.threshold) continue;
         const long long c0 = (rs + g - 1) / g;
         long long c1 = re / g;                        // chunks ending at (c+1)g <= re
         if (re == nnz && nnz % g) c1 = nnz / g + 1;   // ... and the final partial chunk

@@ -79,6 +79,17 @@ def test_config2_long_chunk_walks():
     print(_check(g, 128, pts))
 
 
+def test_config3_reddit_shaped():
+    """BASELINE config 3 (Chung-Lu, 233k rows, 114.5M nnz, hub rows of tens
+    of thousands of nonzeros) at N=64: the rows where float32 product
+    rounding alone exceeds 1e-5 without the error-free accumulate."""
+    g = G.config_matrix(3, device="cuda")
+    print(_check(g, 64, [("nnz:512,col:4,r:1", 256, 1), ("nnz:128,col:2,r:1", 1024, 3),
+                         ("nnz:32,col:4,r:1", 256, 2), ("row:4,col:2,r:1", 256, 4),
+                         ("row:1,col:4,r:1", 256, 2), ("row:1/4,col:4,r:4", 256),
+                         ("nnz:1,col:4,r:1", 256), ("nnz:1,col:2,r:8", 256)]))
+
+
 def test_row_staged_variants():
     """Row-multiple with a warp per row (hw variants 3/4, N/c == 32): stencil
     rows (<= 27, the float32 path) and R-MAT hub rows (> 64, the float64
