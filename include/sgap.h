@@ -218,6 +218,38 @@ int sgap_run(const sgap_kernel_t *kernel, const sgap_csr_t *a, const void *d_b,
 int sgap_reference_spmm_f64(const sgap_csr_t *a, const void *d_b, int32_t n,
                             int32_t dtype, double *d_c, void *stream);
 
+/* ---- Matrix Market ingest on the device -------------
+ * Replaces the entry loop of matrices.loads_matrix_market
+ * (matrices.py:144-212) and _coo_to_csr (matrices.py:124-141); the header and
+ * any line outside the strict device grammar stay with the host (Python
+ * int()/float()), so values, errors and line numbers are the reference's.
+ *   sgap_mm_line_flags: d_flag[i] = 1 where a line starts (byte 0 and after
+ *     each '\n'); *d_special |= 1 when str.splitlines()/split() would see
+ *     separators a '\n' scan does not (lone '\r', control bytes, non-ASCII).
+ *   sgap_mm_parse: per line d_status (0 blank/comment, 1 entry, 2 not three
+ *     tokens, 3 non-numeric, 4 coordinate out of range, 5 the host checks
+ *     the line, 6 entry whose plain-decimal value the host converts) and, for
+ *     status 1 and 6, zero-based row/col, the value token's byte offset and
+ *     length; for status 1 the value (correctly rounded: Clinger's fast path).
+ *   sgap_mm_expand: COO in the reference's append order at d_pos (exclusive
+ *     scan of 1 per entry, 2 for symmetric off-diagonals), key = row<<32|col.
+ *   sgap_mm_sum_runs: per run of equal keys in the stably sorted COO, the
+ *     np.add.reduceat sum (first + numpy pairwise sum of the rest).
+ *   sgap_mm_row_ptr: row_ptr[r] = lower bound of r in the sorted rows.      */
+int sgap_mm_line_flags(const uint8_t *d_text, int64_t len, uint8_t *d_flag, int32_t *d_special,
+                       void *stream);
+int sgap_mm_parse(const uint8_t *d_text, int64_t len, const int64_t *d_starts, int64_t nlines,
+                  int64_t rows, int64_t cols, uint8_t *d_status, int64_t *d_r, int64_t *d_c,
+                  double *d_v, int64_t *d_tok_off, int32_t *d_tok_len, void *stream);
+int sgap_mm_expand(int64_t nlines, const uint8_t *d_status, const int64_t *d_r, const int64_t *d_c,
+                   const double *d_v, const int64_t *d_pos, int32_t symmetric, int64_t *d_key,
+                   double *d_val, void *stream);
+int sgap_mm_sum_runs(int64_t total, const int64_t *d_key, const double *d_val,
+                     const int64_t *d_run_start, int64_t nruns, int64_t *d_row, int64_t *d_col,
+                     double *d_out, void *stream);
+int sgap_mm_row_ptr(const int64_t *d_row, int64_t nnz, int64_t num_rows, int64_t *d_row_ptr,
+                    void *stream);
+
 /* Device restatements of the simulator's group macros over lane vectors
  * (lanes = multiple of group_size, group_size in {1,2,4,8,16,32}).  They run
  * the same warp-shuffle code as the SpMM kernels.

@@ -52,6 +52,11 @@ EXPORTED = (
     "sgap_reference_spmm_f64",
     "sgap_seg_reduce_group",
     "sgap_atomic_add_group",
+    "sgap_mm_line_flags",
+    "sgap_mm_parse",
+    "sgap_mm_expand",
+    "sgap_mm_sum_runs",
+    "sgap_mm_row_ptr",
 )
 
 
@@ -165,6 +170,14 @@ def lib():
     L.sgap_run.restype = ctypes.c_int
     L.sgap_reference_spmm_f64.argtypes = [ctypes.POINTER(Csr), vp, i32, i32, vp, vp]
     L.sgap_reference_spmm_f64.restype = ctypes.c_int
+    L.sgap_mm_line_flags.argtypes = [vp, i64, vp, vp, vp]
+    L.sgap_mm_parse.argtypes = [vp, i64, vp, i64, i64, i64, vp, vp, vp, vp, vp, vp, vp]
+    L.sgap_mm_expand.argtypes = [i64, vp, vp, vp, vp, vp, i32, vp, vp, vp]
+    L.sgap_mm_sum_runs.argtypes = [i64, vp, vp, vp, i64, vp, vp, vp, vp]
+    L.sgap_mm_row_ptr.argtypes = [vp, i64, i64, vp, vp]
+    for name in ("sgap_mm_line_flags", "sgap_mm_parse", "sgap_mm_expand", "sgap_mm_sum_runs",
+                 "sgap_mm_row_ptr"):
+        getattr(L, name).restype = ctypes.c_int
     for name in ("sgap_seg_reduce_group", "sgap_atomic_add_group"):
         fn = getattr(L, name)
         fn.argtypes = [vp, vp, vp, i64, i32, vp, i64, i32, vp, vp, vp]

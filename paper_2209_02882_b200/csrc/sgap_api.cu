@@ -11,6 +11,7 @@
 
 #include "../../include/sgap.h"
 #include "sgap_kernels.cuh"
+#include "sgap_ingest.cuh"
 
 using namespace sgap;
 
@@ -632,6 +633,73 @@ int sgap_reference_spmm_f64(const sgap_csr_t *a, const void *d_b, int32_t n, int
         k_reference_f64<double><<<(unsigned)blocks, kHwBlock, 0, st>>>(
             a->d_row_ptr, a->d_col_idx, static_cast<const double *>(a->d_vals),
             static_cast<const double *>(d_b), d_c, (int)a->num_rows, n);
+    return launch_status();
+}
+
+// ------------------------------------------------------------ Matrix Market ingest
+
+static unsigned ingest_grid(long long items) {
+    long long b = ceil_div(items > 0 ? items : 1, 256);
+    return (unsigned)(b < 65536 ? b : 65536);
+}
+
+int sgap_mm_line_flags(const uint8_t *d_text, int64_t len, uint8_t *d_flag, int32_t *d_special,
+                       void *stream) {
+    if (len < 0) return SGAP_ERR_ARG;
+    if (len == 0) return SGAP_OK;
+    if (d_text == nullptr || d_flag == nullptr || d_special == nullptr) return SGAP_ERR_ARG;
+    k_mm_line_flags<<<ingest_grid(len), 256, 0, as_stream(stream)>>>(d_text, len, d_flag,
+                                                                      d_special);
+    return launch_status();
+}
+
+int sgap_mm_parse(const uint8_t *d_text, int64_t len, const int64_t *d_starts, int64_t nlines,
+                  int64_t rows, int64_t cols, uint8_t *d_status, int64_t *d_r, int64_t *d_c,
+                  double *d_v, int64_t *d_tok_off, int32_t *d_tok_len, void *stream) {
+    if (len < 0 || nlines < 0 || rows < 0 || cols < 0) return SGAP_ERR_ARG;
+    if (nlines == 0) return SGAP_OK;
+    if (!d_text || !d_starts || !d_status || !d_r || !d_c || !d_v || !d_tok_off || !d_tok_len)
+        return SGAP_ERR_ARG;
+    k_mm_parse<<<ingest_grid(nlines), 256, 0, as_stream(stream)>>>(
+        d_text, len, reinterpret_cast<const long long *>(d_starts), nlines, rows, cols, d_status,
+        reinterpret_cast<long long *>(d_r), reinterpret_cast<long long *>(d_c), d_v,
+        reinterpret_cast<long long *>(d_tok_off), reinterpret_cast<int *>(d_tok_len));
+    return launch_status();
+}
+
+int sgap_mm_expand(int64_t nlines, const uint8_t *d_status, const int64_t *d_r, const int64_t *d_c,
+                   const double *d_v, const int64_t *d_pos, int32_t symmetric, int64_t *d_key,
+                   double *d_val, void *stream) {
+    if (nlines < 0) return SGAP_ERR_ARG;
+    if (nlines == 0) return SGAP_OK;
+    if (!d_status || !d_r || !d_c || !d_v || !d_pos || !d_key || !d_val) return SGAP_ERR_ARG;
+    k_mm_expand<<<ingest_grid(nlines), 256, 0, as_stream(stream)>>>(
+        nlines, d_status, reinterpret_cast<const long long *>(d_r),
+        reinterpret_cast<const long long *>(d_c), d_v, reinterpret_cast<const long long *>(d_pos),
+        symmetric, reinterpret_cast<long long *>(d_key), d_val);
+    return launch_status();
+}
+
+int sgap_mm_sum_runs(int64_t total, const int64_t *d_key, const double *d_val,
+                     const int64_t *d_run_start, int64_t nruns, int64_t *d_row, int64_t *d_col,
+                     double *d_out, void *stream) {
+    if (total < 0 || nruns < 0) return SGAP_ERR_ARG;
+    if (nruns == 0) return SGAP_OK;
+    if (!d_key || !d_val || !d_run_start || !d_row || !d_col || !d_out) return SGAP_ERR_ARG;
+    k_mm_sum_runs<<<ingest_grid(nruns), 256, 0, as_stream(stream)>>>(
+        total, reinterpret_cast<const long long *>(d_key), d_val,
+        reinterpret_cast<const long long *>(d_run_start), nruns,
+        reinterpret_cast<long long *>(d_row), reinterpret_cast<long long *>(d_col), d_out);
+    return launch_status();
+}
+
+int sgap_mm_row_ptr(const int64_t *d_row, int64_t nnz, int64_t num_rows, int64_t *d_row_ptr,
+                    void *stream) {
+    if (nnz < 0 || num_rows < 0 || d_row_ptr == nullptr || (nnz > 0 && d_row == nullptr))
+        return SGAP_ERR_ARG;
+    k_mm_row_ptr<<<ingest_grid(num_rows + 1), 256, 0, as_stream(stream)>>>(
+        reinterpret_cast<const long long *>(d_row), nnz, num_rows,
+        reinterpret_cast<long long *>(d_row_ptr));
     return launch_status();
 }
 

@@ -261,3 +261,41 @@ def test_reference_objects_are_accepted():
         got, m = run(ref_k, ref_a, ref_b)
         assert oracle.max_rel_error(got.vals, want) <= F64_TOL
         assert m.grid_size == ours.grid_size
+
+
+def test_config1_every_candidate_every_walk():
+    """Every candidate of the B200 knob grid (g up to 512, every walk variant
+    the point admits) on config 1 at N=32, float32, within 1e-5 of the
+    float64 reference; the device reference itself is pinned to the CPU
+    oracle first (tools/parity_sweep.py runs the same check at configs 2-4)."""
+    import torch
+
+    from paper_2209_02882_b200 import _native
+    from paper_2209_02882_b200.device import DeviceCsr, prepare_aux, reference_spmm_f64, spmm
+    from paper_2209_02882_b200.selector import candidates, plan_for
+
+    dev = torch.device("cuda", 0)
+    a_h = random_csr(4096, 4096, 0.01, seed=1)
+    b_h = random_dense(4096, 32, seed=2)
+    a = DeviceCsr(4096, 4096, torch.as_tensor(np.asarray(a_h.row_ptr, np.int32), device=dev),
+                  torch.as_tensor(np.asarray(a_h.col_idx, np.int32), device=dev),
+                  torch.as_tensor(np.asarray(a_h.vals, np.float32), device=dev))
+    b = torch.as_tensor(np.asarray(b_h.vals, np.float32).reshape(4096, 32), device=dev)
+    want = reference_spmm_f64(a, b, 32)
+    assert np.array_equal(want.cpu().numpy(), oracle_f32(a_h, b_h, 32).reshape(4096, 32))
+    c = torch.empty((4096, 32), dtype=torch.float32, device=dev)
+    rp = np.asarray(a_h.row_ptr, np.int64)
+    runs = 0
+    for cand in candidates(32):
+        k = plan_for(cand, 32, 4096, 4096, rp)
+        aux = prepare_aux(k, a, row_ptr_host=rp)
+        c.fill_(float("nan"))
+        try:
+            spmm(k, a, b, c, aux=aux, hw_block=cand.hw_block, hw_variant=cand.hw_variant)
+        except _native.SgapError as e:
+            assert e.status == _native.ERR_ARG  # variant not applicable to this point
+            continue
+        err = float(((c.double() - want).abs() / (want.abs() + 1)).max())
+        assert err <= F32_TOL, (cand.label(), err)
+        runs += 1
+    assert runs > 250
