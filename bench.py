@@ -460,7 +460,7 @@ def main():
                 "stats": stats.as_dict(),
             },
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": args.steps * launches_per_call(k, aux),
+            "gpu_launches": args.steps * launches_per_call(k, aux, hw_variant=choice.hw_variant),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define SGAP_ABI_VERSION 2
+#define SGAP_ABI_VERSION 3
 
 typedef enum {
     SGAP_OK = 0,
@@ -164,6 +164,10 @@ typedef struct {
                                  (0 lets sgap_run skip the error-free pass)  */
     int32_t *d_long_slot;
     int64_t long_chunk;
+    const int32_t *d_exact_rows;  /* rows with > max(long_threshold,
+                                     sgap_exact_row_length()) nonzeros: the
+                                     error-free pass walks exactly these    */
+    int32_t exact_count;          /* their number (host-known: sizes the grid) */
 } sgap_aux_t;
 
 /* Per-position row ids (what the reference lowering recovers per lane with

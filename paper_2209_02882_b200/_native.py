@@ -121,6 +121,8 @@ class Aux(ctypes.Structure):
         ("has_exact_rows", ctypes.c_int32),
         ("d_long_slot", ctypes.c_void_p),
         ("long_chunk", ctypes.c_int64),
+        ("d_exact_rows", ctypes.c_void_p),
+        ("exact_count", ctypes.c_int32),
     ]
 
 

@@ -51,6 +51,26 @@ bool aligned(const void *p, size_t bytes) {
     return (reinterpret_cast<uintptr_t>(p) % bytes) == 0;
 }
 
+// Launch with programmatic stream serialisation when `pdl` (the kernel may
+// start while the previous grid on the stream is still running; it calls
+// griddepcontrol.wait before it exits).
+template <typename... KArgs, typename... Args>
+int launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+             bool pdl, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...) == cudaSuccess
+               ? SGAP_OK : SGAP_ERR_CUDA;
+}
+
 // ------------------------------------------------------------------ dispatch
 
 // hw_variant for row-multiple: 0/1 the logical mapping (thread (rg, t) owns
@@ -168,7 +188,8 @@ inline int tma_tile_for(int g) {
 template <typename T, int V, int W, int U, bool PIPE, int STAGES = 3, int MINB = 3>
 int launch_nnz_multiple(bool tma, int tile, int owner, const sgap_kernel_t &k,
                         const sgap_csr_t &a, const T *B, T *C, const int *rowid,
-                        const LongRows &lr, unsigned long long *wb, cudaStream_t st) {
+                        const LongRows &lr, unsigned long long *wb, cudaStream_t st, bool pdl,
+                        int exact_inline) {
     const long long total_pos = k.grid_size * k.chunk;
     if (tma) {
         const size_t smem = tma_smem_bytes<T, STAGES>();
@@ -184,19 +205,17 @@ int launch_nnz_multiple(bool tma, int tile, int owner, const sgap_kernel_t &k,
         long long ctas = (long long)sms * (per_sm > 0 ? per_sm : 1);
         if (ctas > ntiles) ctas = ntiles;
         if (ctas < 1) ctas = 1;
-        kern<<<(unsigned)ctas, kTmaThreads, smem, st>>>(
-            rowid, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, a.d_row_ptr,
-            (int)a.num_rows, k.n, a.nnz, k.g, total_pos, tile, owner, lr, wb);
-        return launch_status();
+        return launch_k(kern, dim3((unsigned)ctas), dim3(kTmaThreads), smem, st, pdl, rowid,
+                        a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, a.d_row_ptr,
+                        (int)a.num_rows, k.n, a.nnz, k.g, total_pos, tile, owner, lr, wb);
     }
     const long long items = ceil_div(total_pos / k.g, 32 / W);
     const int blk = k.hw_block > 0 ? k.hw_block : kHwBlock;
     const int vec4 = (k.g % 4 == 0) && aligned(rowid, 16) && aligned(a.d_col_idx, 16) &&
                      aligned(a.d_vals, 16);
-    k_nnz_multiple<T, V, W, U, PIPE><<<grid_for(items, blk), blk, 0, st>>>(
-        rowid, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, a.d_row_ptr, (int)a.num_rows,
-        k.n, a.nnz, k.g, total_pos, vec4, owner, lr, wb);
-    return launch_status();
+    return launch_k(k_nnz_multiple<T, V, W, U, PIPE>, dim3(grid_for(items, blk)), dim3(blk), 0, st,
+                    pdl, rowid, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, a.d_row_ptr,
+                    (int)a.num_rows, k.n, a.nnz, k.g, total_pos, vec4, owner, lr, wb, exact_inline);
 }
 
 // hw_variant: 0 auto; 1 register walk; 2 TMA-staged walk; 3/4 lane-staged walk
@@ -223,37 +242,44 @@ int run_nnz_multiple_w(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, 
     if (tma && !tma_ok) return SGAP_ERR_ARG;
     if (variant < 1 || variant > 4) return SGAP_ERR_ARG;
     if (variant >= 3 && W != 32) return SGAP_ERR_ARG;  // the staged walk takes a whole warp
-    int status;
+    // chunks inside exact-flagged rows (error-free accumulate) run in their
+    // own kernel, launched first; the main walk follows with programmatic
+    // dependent launch, so the two overlap (no data dependency: both only add
+    // into the float64 table) and the walk's grid exits after the exact pass
+    bool pdl = false;
+    // the register walk (variant 1) takes exact chunks inline (float64
+    // products); the other walks leave them to k_nnz_multiple_exact
+    const bool exact_inline = variant == 1 && lr.threshold >= 0 && sizeof(T) == 4;
+    if (!exact_inline && lr.threshold >= 0 && sizeof(T) == 4 && has_exact && lr.exact_count > 0 &&
+        lr.exact_rows != nullptr) {
+        const int vec4 = (k.g % 4 == 0) && aligned(rowid, 16) && aligned(a.d_col_idx, 16) &&
+                         aligned(a.d_vals, 16);
+        const int gx = lr.exact_count < 1024 ? lr.exact_count : 1024;
+        int gy = (2 * 148 * 8 + gx - 1) / gx;  // ~2 waves of 8-warp CTAs
+        gy = gy < 1 ? 1 : (gy > 64 ? 64 : gy);
+        k_nnz_multiple_exact<T, V><<<dim3((unsigned)gx, (unsigned)gy), kHwBlock, 0, st>>>(
+            rowid, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, a.d_row_ptr, k.n, a.nnz,
+            k.g, vec4, lr);
+        const int s0 = launch_status();
+        if (s0 != SGAP_OK) return s0;
+        pdl = true;
+    }
     if (variant >= 3) {
         const long long total_pos = k.grid_size * k.chunk;
         const long long chunks = total_pos / k.g;
         const int blk = k.hw_block > 0 ? k.hw_block : kHwBlock;
         if (blk != kHwBlock) return SGAP_ERR_ARG;
+        const dim3 grid(grid_for(chunks, blk));
         if (variant == 3)
-            k_nnz_multiple_staged<T, V, 4, 4><<<grid_for(chunks, blk), blk, 0, st>>>(
-                rowid, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, a.d_row_ptr,
-                (int)a.num_rows, k.n, a.nnz, k.g, total_pos, owner, lr, wb);
-        else
-            k_nnz_multiple_staged<T, V, 8, 3><<<grid_for(chunks, blk), blk, 0, st>>>(
-                rowid, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, a.d_row_ptr,
-                (int)a.num_rows, k.n, a.nnz, k.g, total_pos, owner, lr, wb);
-        status = launch_status();
-    } else {
-        status = launch_nnz_multiple<T, V, W, 4, false>(tma, tile, owner, k, a, B, C, rowid, lr,
-                                                         wb, st);
+            return launch_k(k_nnz_multiple_staged<T, V, 4, 4>, grid, dim3(blk), 0, st, pdl, rowid,
+                            a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, a.d_row_ptr,
+                            (int)a.num_rows, k.n, a.nnz, k.g, total_pos, owner, lr, wb);
+        return launch_k(k_nnz_multiple_staged<T, V, 8, 3>, grid, dim3(blk), 0, st, pdl, rowid,
+                        a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, a.d_row_ptr,
+                        (int)a.num_rows, k.n, a.nnz, k.g, total_pos, owner, lr, wb);
     }
-    if (status != SGAP_OK || lr.threshold < 0 || sizeof(T) != 4 || !has_exact) return status;
-    // chunks inside long rows: error-free accumulate in their own kernel
-    const long long total_pos = k.grid_size * k.chunk;
-    const int vec4 = (k.g % 4 == 0) && aligned(rowid, 16) && aligned(a.d_col_idx, 16) &&
-                     aligned(a.d_vals, 16);
-    (void)total_pos;
-    const long long cap = sgap_long_row_capacity(a.nnz, lr.threshold, lr.chunk);
-    const dim3 grid((unsigned)(cap < 1024 ? (cap > 0 ? cap : 1) : 1024), 64);
-    k_nnz_multiple_exact<T, V><<<grid, kHwBlock, 0, st>>>(
-        rowid, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, a.d_row_ptr, k.n, a.nnz, k.g,
-        vec4, lr);
-    return launch_status();
+    return launch_nnz_multiple<T, V, W, 4, false>(tma, tile, owner, k, a, B, C, rowid, lr, wb, st,
+                                                   pdl, exact_inline ? 1 : 0);
 }
 
 template <typename T, int V>
@@ -585,13 +611,17 @@ int sgap_run(const sgap_kernel_t *k, const sgap_csr_t *a, const void *d_b, void 
     const int32_t *rowid = aux ? aux->d_rowid : nullptr;
     if (eb && k->grid_size > 0 && a->nnz > 0 && rowid == nullptr) return SGAP_ERR_ARG;
     if (k->family == SGAP_NNZ_MULTIPLE && (k->g < 1 || k->chunk % k->g)) return SGAP_ERR_CONFIG;
-    LongRows lr{nullptr, nullptr, nullptr, -1, nullptr, 0};
+    LongRows lr{nullptr, nullptr, nullptr, -1, nullptr, 0, nullptr, 0};
     const bool has_exact = aux != nullptr && aux->has_exact_rows != 0;
+    // exact-flagged chunks are skipped by the main walk: their pass needs the list
+    if (has_exact && k->family == SGAP_NNZ_MULTIPLE && dtype == SGAP_F32 &&
+        aux->long_threshold >= 0 && (aux->d_exact_rows == nullptr || aux->exact_count <= 0))
+        return SGAP_ERR_ARG;
     if (eb && aux && aux->long_threshold >= 0 && dtype == SGAP_F32) {
         if (aux->d_long_rows == nullptr || aux->d_long_count == nullptr || aux->d_long_acc == nullptr)
             return SGAP_ERR_ARG;
         lr = LongRows{aux->d_long_rows, aux->d_long_count, aux->d_long_acc, aux->long_threshold,
-                      aux->d_long_slot, aux->long_chunk};
+                      aux->d_long_slot, aux->long_chunk, aux->d_exact_rows, aux->exact_count};
     }
     if (k->family == SGAP_NNZ_ONE && !accumulate) {
         // atomic-writeback families accumulate into C: zero-fill (counts as

@@ -244,6 +244,8 @@ struct LongRows {
     long long threshold;  // < 0: side table disabled (float64 values, RB families)
     const int *slot;      // row -> table slot (nullptr: binary search of `rows`)
     long long chunk;      // > 0: every row straddling a `chunk` boundary is in the table
+    const int *exact_rows;  // rows taking the error-free pass (nnz-multiple)
+    int exact_count;
 };
 
 // Row ids carry bit 31 when the row belongs to the long-row table and bit 30
@@ -390,6 +392,14 @@ __device__ __forceinline__ void group_sum_vec(Vec<T, V> &a) {
         for (int x = 0; x < V; ++x) a.v[x] += __shfl_xor_sync(kFull, a.v[x], off, R);
     }
 }
+
+// Programmatic dependent launch (sm_90+): a primary grid lets its dependent
+// start early; the dependent waits for the primary's completion (and memory)
+// where it needs it.  Both are no-ops for a normally launched grid.
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // Warp-aggregated writeback counter (SimMetrics.atomic_ops).
 __device__ __forceinline__ void flush_count(unsigned long long *counter, unsigned long long mine) {

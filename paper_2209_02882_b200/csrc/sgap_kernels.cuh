@@ -746,14 +746,10 @@ __device__ __forceinline__ void eb_walk4(const ASrc &A, long long q0, long long 
 template <typename T, int V, class ASrc>
 __device__ __forceinline__ void eb_walk4_exact(const ASrc &A, long long q0, long long qend,
                                             const T *__restrict__ B, int N, long long kcol,
-                                            T *__restrict__ C, const LongRows &lr,
-                                            unsigned long long &nwb) {
-    const int cur = A.row(q0);
+                                            Vec<double, V> &tot) {
     Vec<T, V> hi, lo;
     hi.zero();
     lo.zero();
-    Vec<double, V> tot;
-    tot.zero();
     const T *bk = B + kcol;
     long long q = q0;
     int since_fold = 0;
@@ -782,8 +778,6 @@ __device__ __forceinline__ void eb_walk4_exact(const ASrc &A, long long q0, long
         fma_vec_exact<T, V>(hi, lo, A.val(q), b);
     }
     fold2<T, V>(tot, hi, lo);
-    flush_row<T, V>(C, N, cur, kcol, tot, lr);  // long rows always go to the float64 table
-    nwb += V;
 }
 
 template <typename T, int V, int U>
@@ -878,7 +872,8 @@ __global__ void __launch_bounds__(256, 4)
 k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
                const T *__restrict__ av, const T *__restrict__ B, T *__restrict__ C,
                const int *__restrict__ rp, int M, int N, long long nnz, int g,
-               long long total_pos, int vec4, int owner, LongRows lr, unsigned long long *wb) {
+               long long total_pos, int vec4, int owner, LongRows lr, unsigned long long *wb,
+               int exact_inline) {
     const bool VEC4 = vec4 != 0;  // g % 4 == 0 and 16-byte aligned A arrays
     const int NT = N / V;
     constexpr int SG = 32 / W;
@@ -901,12 +896,47 @@ k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
             }
             const Owner own{rp, rowid, base, end, nnz, M, owner != 0};
             const int r_first = A.row(base);
-            if ((r_first & kExactFlag) && A.row(end - 1) == r_first) {  // the exact kernel's
+            if ((r_first & kExactFlag) && A.row(end - 1) == r_first) {
+                const long long kcol = (long long)tile * V;
                 if (own.on && __ldg(rp + (r_first & kRowMask)) == base)
-                    zero_gap_before<T, V>(C, N, (long long)tile * V, own, r_first & kRowMask);
+                    zero_gap_before<T, V>(C, N, kcol, own, r_first & kRowMask);
                 if (own.on && end == nnz)
-                    zero_rows<T, V>(C, N, (long long)tile * V, (r_first & kRowMask) + 1, M);
+                    zero_rows<T, V>(C, N, kcol, (r_first & kRowMask) + 1, M);
                 nwb += V;
+                if (exact_inline) {
+                    // a chunk inside an exact-flagged (hub) row: float64
+                    // products (exact for float32 inputs) summed in float64,
+                    // in this walk -- no separate error-free pass to launch
+                    Vec<double, V> tot;
+                    tot.zero();
+                    const T *bk = B + kcol;
+                    long long q = base;
+                    for (; VEC4 && q + 4 <= end; q += 4) {
+                        int4 c, r;
+                        Vec<T, 4> v;
+                        A.load4(q, c, v, r);
+                        Vec<T, V> b0, b1, b2, b3;
+                        ldg_vec<T, V>(b0, bk + (long long)c.x * N);
+                        ldg_vec<T, V>(b1, bk + (long long)c.y * N);
+                        ldg_vec<T, V>(b2, bk + (long long)c.z * N);
+                        ldg_vec<T, V>(b3, bk + (long long)c.w * N);
+#pragma unroll
+                        for (int x = 0; x < V; ++x) {
+                            tot.v[x] = fma((double)v.v[0], (double)b0.v[x], tot.v[x]);
+                            tot.v[x] = fma((double)v.v[1], (double)b1.v[x], tot.v[x]);
+                            tot.v[x] = fma((double)v.v[2], (double)b2.v[x], tot.v[x]);
+                            tot.v[x] = fma((double)v.v[3], (double)b3.v[x], tot.v[x]);
+                        }
+                    }
+                    for (; q < end; ++q) {
+                        Vec<T, V> b;
+                        ldg_vec<T, V>(b, bk + (long long)A.col(q) * N);
+                        const double a = (double)A.val(q);
+#pragma unroll
+                        for (int x = 0; x < V; ++x) tot.v[x] = fma(a, (double)b.v[x], tot.v[x]);
+                    }
+                    flush_row<T, V>(C, N, r_first, kcol, tot, lr);  // the float64 table
+                }
                 continue;
             }
             if (VEC4)
@@ -916,6 +946,7 @@ k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
         }
     }
     flush_count(wb, nwb);
+    pdl_wait();  // launched after the error-free pass: finish after it too
 }
 
 // The chunks of nnz-multiple that lie entirely inside one exact-flagged row
@@ -933,52 +964,58 @@ k_nnz_multiple_exact(const int *__restrict__ rowid, const int *__restrict__ ci,
                      const int *__restrict__ rp, int N, long long nnz, int g, int vec4,
                      LongRows lr) {
     const int NT = N / V;
-    const int count = *lr.count;
     const unsigned lane = lane_id();
     const int warp = (int)(threadIdx.x >> 5);
     const int nwarps = (int)(blockDim.x >> 5);
     const long long per_chunk = ((long long)g + 31) >> 5;
     const GlobalA<T> A{rowid, ci, av};
     unsigned long long unused = 0;
-    for (int li = blockIdx.x; li < count; li += gridDim.x) {
-        const int r = __ldg(lr.rows + li);
+    pdl_launch_dependents();  // the main walk (no data dependency) may start now
+    // exactly the rows k_row_ids flagged exact (host-compacted list; the grid
+    // is sized to it -- iterating the whole table launched ~65k mostly idle
+    // CTAs, 77 us per call on config 2)
+    for (int li = blockIdx.x; li < lr.exact_count; li += gridDim.x) {
+        const int r = __ldg(lr.exact_rows + li);
         const long long rs = __ldg(rp + r), re = __ldg(rp + r + 1);
-        // exactly the rows k_row_ids flagged exact (split-row routing also
-        // puts shorter rows in the table; those stay with the main walk)
-        if (re - rs <= kExactRow || re - rs <= lr.threshold) continue;
         const long long c0 = (rs + g - 1) / g;
         long long c1 = re / g;                        // chunks ending at (c+1)g <= re
         if (re == nnz && nnz % g) c1 = nnz / g + 1;   // ... and the final partial chunk
         if (c1 <= c0) continue;
         const long long items = (c1 - c0) * per_chunk;
-        for (long long it = (long long)blockIdx.y * nwarps + warp; it < items;
-             it += (long long)gridDim.y * nwarps) {
-            const long long cb = (c0 + it / per_chunk) * g;
-            const long long ce = min(cb + (long long)g, nnz);
-            const long long q0 = cb + (it % per_chunk) * 32;
-            const long long q1 = min(q0 + 32, ce);
-            if (q0 >= q1) continue;
-            for (int tile = (int)lane; tile < NT; tile += 32) {
+        // a warp sums all its pieces of this row and flushes once per tile
+        // (one float64 atomic per piece and tile serialised on the row's
+        // table slot: 59 us per call on config 2's hub rows)
+        const long long first = (long long)blockIdx.y * nwarps + warp;
+        if (first >= items) continue;
+        for (int tile = (int)lane; tile < NT; tile += 32) {
+            const long long kcol = (long long)tile * V;
+            Vec<double, V> tot;
+            tot.zero();
+            for (long long it = first; it < items; it += (long long)gridDim.y * nwarps) {
+                const long long cb = (c0 + it / per_chunk) * g;
+                const long long ce = min(cb + (long long)g, nnz);
+                const long long q0 = cb + (it % per_chunk) * 32;
+                const long long q1 = min(q0 + 32, ce);
+                if (q0 >= q1) continue;
                 if (vec4) {
-                    eb_walk4_exact<T, V>(A, q0, q1, B, N, (long long)tile * V, C, lr, unused);
+                    eb_walk4_exact<T, V>(A, q0, q1, B, N, kcol, tot);
                 } else {
                     Vec<T, V> hi, lo;
                     hi.zero();
                     lo.zero();
-                    Vec<double, V> tot;
-                    tot.zero();
                     for (long long q = q0; q < q1; ++q) {
                         Vec<T, V> b;
-                        ldg_vec<T, V>(b, B + (long long)A.col(q) * N + (long long)tile * V);
+                        ldg_vec<T, V>(b, B + (long long)A.col(q) * N + kcol);
                         fma_vec_exact<T, V>(hi, lo, A.val(q), b);
                         if (((q - q0) & (kFoldEvery - 1)) == kFoldEvery - 1) fold2<T, V>(tot, hi, lo);
                     }
                     fold2<T, V>(tot, hi, lo);
-                    flush_row<T, V>(C, N, A.row(q0), (long long)tile * V, tot, lr);
                 }
             }
+            flush_row<T, V>(C, N, r | kLongFlag, kcol, tot, lr);  // the float64 table
         }
     }
+    (void)unused;
 }
 
 // ---------------------------------------------------------------------------
@@ -1115,6 +1152,7 @@ k_nnz_multiple_staged(const int *__restrict__ rowid, const int *__restrict__ ci,
         }
     }
     flush_count(wb, nwb);
+    pdl_wait();  // launched after the error-free pass: finish after it too
 }
 
 // ---------------------------------------------------------------------------
@@ -1239,6 +1277,7 @@ k_nnz_multiple_tma(const int *__restrict__ rowid, const int *__restrict__ ci,
         }
     }
     flush_count(wb, nwb);
+    pdl_wait();  // launched after the error-free pass: finish after it too
 }
 
 // Per-position row ids (the row owning each nonzero, lowering.py:459-500),

@@ -158,17 +158,19 @@ class KernelAux:
     has_exact_rows: int = 0
     long_slot: torch.Tensor | None = None
     long_chunk: int = 0
+    exact_rows: torch.Tensor | None = None
 
     def view(self) -> _native.Aux:
         ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+        n_exact = int(self.exact_rows.numel()) if self.exact_rows is not None else 0
         return _native.Aux(ptr(self.starts), ptr(self.rowid), ptr(self.long_rows),
                            ptr(self.long_count), ptr(self.long_acc), self.long_capacity,
                            self.long_threshold, self.has_exact_rows, ptr(self.long_slot),
-                           self.long_chunk)
+                           self.long_chunk, ptr(self.exact_rows), n_exact)
 
     def nbytes(self) -> int:
         ts = (self.starts, self.rowid, self.long_rows, self.long_count, self.long_acc,
-              self.long_slot)
+              self.long_slot, self.exact_rows)
         return sum(t.numel() * t.element_size() for t in ts if t is not None)
 
 
@@ -206,12 +208,14 @@ def prepare_aux(k: LoweredKernel, a: DeviceCsr, *, stream=None, long_rows: bool 
         if thr >= 0 and split_rows:
             chunk = int(L.sgap_long_row_chunk(ctypes.byref(ks), native_dtype(a.vals.dtype)))
     longest = 0
+    lens = None
     if thr >= 0 and a.num_rows:  # does any row need the table?
         if row_ptr_host is not None:
-            rph = np.asarray(row_ptr_host)
-            longest = int((rph[1:] - rph[:-1]).max())
-        else:  # plan-time host sync
-            longest = int((a.row_ptr[1:] - a.row_ptr[:-1]).max().item())
+            rph = np.asarray(row_ptr_host, dtype=np.int64)
+        else:  # plan-time copy of row_ptr
+            rph = a.row_ptr.cpu().numpy().astype(np.int64)
+        lens = rph[1:] - rph[:-1]
+        longest = int(lens.max())
         if longest <= thr and chunk == 0:
             thr = -1  # no long rows: no table, no fold launch
     aux.rowid = torch.empty(max(a.nnz, 4), dtype=torch.int32, device=dev)
@@ -220,7 +224,13 @@ def prepare_aux(k: LoweredKernel, a: DeviceCsr, *, stream=None, long_rows: bool 
     if thr < 0:
         return aux
     cap = int(L.sgap_long_row_capacity(a.nnz, thr, chunk))
-    aux.has_exact_rows = int(longest > int(L.sgap_exact_row_length()))
+    # rows k_row_ids flags exact (longer than the table threshold and the
+    # error-free length), compacted for the error-free pass's grid
+    if lens is not None and k.family == "nnz-multiple":
+        exact = np.flatnonzero(lens > max(thr, int(L.sgap_exact_row_length()))).astype(np.int32)
+        if exact.size:
+            aux.exact_rows = torch.as_tensor(exact, device=dev)
+    aux.has_exact_rows = int(aux.exact_rows is not None)
     aux.long_threshold = thr
     aux.long_chunk = chunk
     aux.long_capacity = cap
@@ -269,7 +279,8 @@ def spmm(k: LoweredKernel, a: DeviceCsr, b: torch.Tensor, c: torch.Tensor, *,
     _native.check(st, "sgap_run")
 
 
-def launches_per_call(k: LoweredKernel, aux: KernelAux | None, *, accumulate: bool = False) -> int:
+def launches_per_call(k: LoweredKernel, aux: KernelAux | None, *, accumulate: bool = False,
+                      hw_variant: int = 0) -> int:
     """Kernels of libsgap.so one ``spmm`` call launches (the driver's memset
     for the nnz-one zero-fill is not ours and not counted)."""
     n = 1
@@ -279,7 +290,11 @@ def launches_per_call(k: LoweredKernel, aux: KernelAux | None, *, accumulate: bo
     if aux is not None and aux.long_threshold >= 0 and k.family in ("nnz-one", "nnz-multiple"):
         n += 1  # k_long_rows_fold
         if k.family == "nnz-multiple" and aux.has_exact_rows:
-            n += 1  # k_nnz_multiple_exact
+            # the register walk takes exact chunks inline; the others launch
+            # k_nnz_multiple_exact (sgap_api.cu run_nnz_multiple_w)
+            w = min(32, max(1, k.n // k.c))
+            variant = hw_variant or (2 if (w >= 16 and k.g <= 128) else 1)
+            n += 0 if variant == 1 else 1
     return n
 
 

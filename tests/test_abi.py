@@ -36,7 +36,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_status_strings():
     L = _native.lib()
-    assert L.sgap_abi_version() == 2
+    assert L.sgap_abi_version() == 3
     assert _native.status_string(_native.ERR_NO_TEMPLATE) == "no template covers the point"
     assert _native.status_string(99) == "unknown status"
 
