@@ -59,8 +59,12 @@ __device__ __forceinline__ Vec<double, V> rb_row_impl(const int *__restrict__ ci
     tot.zero();
     int since_fold = 0;
     auto step = [&](T a, const Vec<T, V> &b) {
-        if constexpr (EXACT) fma_vec_exact<T, V>(acc, lo, a, b);
-        else fma_vec<T, V>(acc, a, b);
+        if constexpr (EXACT) {  // float64 products of float32 inputs are exact
+#pragma unroll
+            for (int x = 0; x < V; ++x) tot.v[x] = fma((double)a, (double)b.v[x], tot.v[x]);
+        } else {
+            fma_vec<T, V>(acc, a, b);
+        }
     };
     auto one = [&](int q) {
         Vec<T, V> b;
@@ -381,21 +385,34 @@ k_row_reciprocal(const int *__restrict__ rp, const int *__restrict__ ci,
         // the value type; longer ones fold into float64 after each segment
         const bool multi = end - beg > 32 * G;
         if (sizeof(T) == 4 && end - beg > kExactRow) {
-            // hub rows: error-free products and sums (float32 product rounding
-            // grows like sqrt(row length): config 3 measured 1.2e-5 without)
-            Vec<T, V> lo;
-            lo.zero();
-            int since = 0;
-            for (int p = beg + j; p < end; p += G) {
+            // hub rows: float64 products (exact) summed in float64 (float32
+            // product rounding grows like sqrt(row length): config 3 measured
+            // 1.2e-5 without), kBatch gathers in flight
+            int p = beg + j;
+            for (; p + (kBatch - 1) * G < end; p += kBatch * G) {
+                int cc[kBatch];
+                T vv[kBatch];
+                Vec<T, V> bv[kBatch];
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) {
+                    cc[u] = __ldg(ci + p + u * G);
+                    vv[u] = __ldg(av + p + u * G);
+                }
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) ldg_vec<T, V>(bv[u], bk + (IT)cc[u] * (IT)N);
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u)
+#pragma unroll
+                    for (int x = 0; x < V; ++x)
+                        tot.v[x] = fma((double)vv[u], (double)bv[u].v[x], tot.v[x]);
+            }
+            for (; p < end; p += G) {
                 Vec<T, V> bv;
                 ldg_vec<T, V>(bv, bk + (IT)__ldg(ci + p) * (IT)N);
-                fma_vec_exact<T, V>(acc[0], lo, __ldg(av + p), bv);
-                if (++since == kFoldEvery) {
-                    fold2<T, V>(tot, acc[0], lo);
-                    since = 0;
-                }
+                const double a = (double)__ldg(av + p);
+#pragma unroll
+                for (int x = 0; x < V; ++x) tot.v[x] = fma(a, (double)bv.v[x], tot.v[x]);
             }
-            fold2<T, V>(tot, acc[0], lo);
         } else if (V == 1 && !multi) {
             // one scalar column, <= 32 terms per lane: the plain strided loop
             for (int p = beg + j; p < end; p += G)
@@ -747,12 +764,10 @@ template <typename T, int V, class ASrc>
 __device__ __forceinline__ void eb_walk4_exact(const ASrc &A, long long q0, long long qend,
                                             const T *__restrict__ B, int N, long long kcol,
                                             Vec<double, V> &tot) {
-    Vec<T, V> hi, lo;
-    hi.zero();
-    lo.zero();
+    // float64 products of float32 inputs are exact; their float64 sum is
+    // error-free at float32 output precision
     const T *bk = B + kcol;
     long long q = q0;
-    int since_fold = 0;
     for (; q + 4 <= qend; q += 4) {
         int4 c, r;
         Vec<T, 4> v;
@@ -762,22 +777,21 @@ __device__ __forceinline__ void eb_walk4_exact(const ASrc &A, long long q0, long
         ldg_vec<T, V>(b1, bk + (long long)c.y * N);
         ldg_vec<T, V>(b2, bk + (long long)c.z * N);
         ldg_vec<T, V>(b3, bk + (long long)c.w * N);
-        fma_vec_exact<T, V>(hi, lo, v.v[0], b0);
-        fma_vec_exact<T, V>(hi, lo, v.v[1], b1);
-        fma_vec_exact<T, V>(hi, lo, v.v[2], b2);
-        fma_vec_exact<T, V>(hi, lo, v.v[3], b3);
-        since_fold += 4;
-        if (since_fold >= kFoldEvery) {
-            fold2<T, V>(tot, hi, lo);
-            since_fold = 0;
+#pragma unroll
+        for (int x = 0; x < V; ++x) {
+            tot.v[x] = fma((double)v.v[0], (double)b0.v[x], tot.v[x]);
+            tot.v[x] = fma((double)v.v[1], (double)b1.v[x], tot.v[x]);
+            tot.v[x] = fma((double)v.v[2], (double)b2.v[x], tot.v[x]);
+            tot.v[x] = fma((double)v.v[3], (double)b3.v[x], tot.v[x]);
         }
     }
     for (; q < qend; ++q) {
         Vec<T, V> b;
         ldg_vec<T, V>(b, bk + (long long)A.col(q) * N);
-        fma_vec_exact<T, V>(hi, lo, A.val(q), b);
+        const double a = (double)A.val(q);
+#pragma unroll
+        for (int x = 0; x < V; ++x) tot.v[x] = fma(a, (double)b.v[x], tot.v[x]);
     }
-    fold2<T, V>(tot, hi, lo);
 }
 
 template <typename T, int V, int U>
@@ -1000,16 +1014,13 @@ k_nnz_multiple_exact(const int *__restrict__ rowid, const int *__restrict__ ci,
                 if (vec4) {
                     eb_walk4_exact<T, V>(A, q0, q1, B, N, kcol, tot);
                 } else {
-                    Vec<T, V> hi, lo;
-                    hi.zero();
-                    lo.zero();
                     for (long long q = q0; q < q1; ++q) {
                         Vec<T, V> b;
                         ldg_vec<T, V>(b, B + (long long)A.col(q) * N + kcol);
-                        fma_vec_exact<T, V>(hi, lo, A.val(q), b);
-                        if (((q - q0) & (kFoldEvery - 1)) == kFoldEvery - 1) fold2<T, V>(tot, hi, lo);
+                        const double a = (double)A.val(q);
+#pragma unroll
+                        for (int x = 0; x < V; ++x) tot.v[x] = fma(a, (double)b.v[x], tot.v[x]);
                     }
-                    fold2<T, V>(tot, hi, lo);
                 }
             }
             flush_row<T, V>(C, N, r | kLongFlag, kcol, tot, lr);  // the float64 table
