@@ -88,14 +88,14 @@ int run_row_multiple(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T 
         const long long tile_rows = (long long)(blk / 32) * k.g;
         const long long tiles = ceil_div(a.num_rows, tile_rows);
         const unsigned ctas = (unsigned)(tiles < (1LL << 30) ? (tiles > 0 ? tiles : 1) : (1LL << 30));
+        const T *Av = static_cast<const T *>(a.d_vals);
+        const int M = (int)a.num_rows;
         if (k.hw_variant == 3)
-            k_row_staged<T, V, 8><<<ctas, blk, 0, st>>>(a.d_row_ptr, a.d_col_idx,
-                                                         static_cast<const T *>(a.d_vals), B, C,
-                                                         (int)a.num_rows, N, k.g, vec4, acc);
+            k_row_staged<T, V, 8><<<ctas, blk, 0, st>>>(a.d_row_ptr, a.d_col_idx, Av, B, C, M, N,
+                                                         k.g, vec4, acc, -1);
         else
-            k_row_staged<T, V, 4><<<ctas, blk, 0, st>>>(a.d_row_ptr, a.d_col_idx,
-                                                         static_cast<const T *>(a.d_vals), B, C,
-                                                         (int)a.num_rows, N, k.g, vec4, acc);
+            k_row_staged<T, V, 4><<<ctas, blk, 0, st>>>(a.d_row_ptr, a.d_col_idx, Av, B, C, M, N,
+                                                         k.g, vec4, acc, -1);
         return launch_status();
     }
     if (k.hw_variant == 2) {

@@ -268,76 +268,31 @@ template <typename T, int V, int U>
 __global__ void __launch_bounds__(256, U >= 8 ? 4 : 5)
 k_row_staged(const int *__restrict__ rp, const int *__restrict__ ci, const T *__restrict__ av,
              const T *__restrict__ B, T *__restrict__ C, int M, int N, int g, int vec4,
-             int accumulate) {
-    // Rows of <= 32 nonzeros (stencil rows) are software-pipelined across the
-    // warp's rows: the next row's bounds load at the start of a row and its
-    // (col, val) right after this row's first gathers, so a row's dependency
-    // chain (row_ptr -> A -> B) overlaps the previous row's gathers.
+             int accumulate, int min_len) {
+    // Measured and not kept on config 4 (N=128, 3.26 ms here):
+    // software-pipelining a warp's rows (next row's bounds and (col, val)
+    // under this row's gathers): 3.41 ms; a 32-register walk for rows <= 32
+    // at 56 warps/SM plus a second launch for longer rows: 3.50 ms (more
+    // warps, more L1 thrash: the walk is L1-throughput- not occupancy-bound).
     const int warps = (int)(blockDim.x >> 5);
     const int w = (int)(threadIdx.x >> 5);
-    const int lane = (int)lane_id();
-    const long long kcol = (long long)lane * V;
-    const T *bk = B + kcol;
+    const long long kcol = (long long)lane_id() * V;
     const long long tile_rows = (long long)warps * g;
     const long long tiles = ((long long)M + tile_rows - 1) / tile_rows;
     for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        long long i = tile * tile_rows + w;
-        if (i >= M) continue;
-        int beg = __ldg(rp + i), end = __ldg(rp + i + 1);
-        int c_l = 0;
-        T v_l = T(0);
-        if (end - beg <= 32 && end > beg) {
-            c_l = __ldg(ci + (beg + lane < end ? beg + lane : beg));
-            v_l = beg + lane < end ? __ldg(av + beg + lane) : T(0);
-        }
         for (int s = 0; s < g; ++s) {
-            const long long inext = i + warps;
-            const bool has_next = s + 1 < g && inext < M;
-            int nbeg = 0, nend = 0;
-            if (has_next) {
-                nbeg = __ldg(rp + inext);
-                nend = __ldg(rp + inext + 1);
-            }
-            int c_n = 0;
-            T v_n = T(0);
-            auto load_next = [&]() {
-                if (has_next && nend - nbeg <= 32 && nend > nbeg) {
-                    c_n = __ldg(ci + (nbeg + lane < nend ? nbeg + lane : nbeg));
-                    v_n = nbeg + lane < nend ? __ldg(av + nbeg + lane) : T(0);
-                }
-            };
+            const long long i = tile * tile_rows + (long long)s * warps + w;
+            if (i >= M) break;
+            const int beg = __ldg(rp + i), end = __ldg(rp + i + 1);
+            if (end - beg <= min_len) continue;  // rows another launch took (min_len < 0: none)
             if (end - beg > 64) {
-                rb_long_staged<T, V, U>(ci, av, beg, end, bk, N, vec4, C + i * N + kcol, accumulate);
-                load_next();
-            } else if (end - beg > 32) {
-                load_next();
-                store_vec<T, V>(C + i * N + kcol, rb_short_staged<T, V, U>(ci, av, beg, end, bk, N),
-                                accumulate != 0);
+                rb_long_staged<T, V, U>(ci, av, beg, end, B + kcol, N, vec4, C + i * N + kcol,
+                                        accumulate);
             } else {
-                Vec<T, V> acc;
-                acc.zero();
-                const int nv = end - beg;
-                for (int j = 0; j < nv; j += U) {
-                    Vec<T, V> b[U];
-#pragma unroll
-                    for (int u = 0; u < U; ++u)
-                        gather_vec<T, V>(b[u], bk + (long long)__shfl_sync(kFull, c_l, (j + u) & 31) * N);
-                    if (j == 0) load_next();
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const T v = __shfl_sync(kFull, v_l, (j + u) & 31);
-                        if (j + u < nv) fma_vec<T, V>(acc, v, b[u]);
-                    }
-                }
-                if (nv == 0) load_next();
-                store_vec<T, V>(C + i * N + kcol, acc, accumulate != 0);
+                store_vec<T, V>(C + i * N + kcol,
+                                rb_short_staged<T, V, U>(ci, av, beg, end, B + kcol, N),
+                                accumulate != 0);
             }
-            if (!has_next) break;
-            i = inext;
-            beg = nbeg;
-            end = nend;
-            c_l = c_n;
-            v_l = v_n;
         }
     }
 }
