@@ -190,41 +190,9 @@ __device__ __forceinline__ void fold(Vec<double, V> &tot, Vec<T, V> &acc) {
     }
 }
 
-// Error-free accumulate for rows long enough that float32 product rounding
-// itself would show (config 5's 239k-nonzero hub row: 2^-24 * sqrt(n) * |ab|
-// ~ 1.5e-5 where a column sum cancels to ~0).  TwoProduct (the FMA returns
-// the exact rounding error of a*b) + TwoSum into (hi, lo); the _rn
-// intrinsics keep the compiler from contracting the error terms away.
-__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
-__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
-__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
-__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
-__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
-__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
-
-template <typename T, int V>
-__device__ __forceinline__ void fma_vec_exact(Vec<T, V> &hi, Vec<T, V> &lo, T a, const Vec<T, V> &b) {
-#pragma unroll
-    for (int x = 0; x < V; ++x) {
-        const T p = mul_rn(a, b.v[x]);
-        const T e = fma(a, b.v[x], -p);  // exact: a*b == p + e
-        const T s = add_rn(hi.v[x], p);
-        const T bb = sub_rn(s, hi.v[x]);
-        const T err = add_rn(sub_rn(hi.v[x], sub_rn(s, bb)), sub_rn(p, bb));
-        hi.v[x] = s;
-        lo.v[x] = add_rn(lo.v[x], add_rn(err, e));
-    }
-}
-
-template <typename T, int V>
-__device__ __forceinline__ void fold2(Vec<double, V> &tot, Vec<T, V> &hi, Vec<T, V> &lo) {
-#pragma unroll
-    for (int x = 0; x < V; ++x) {
-        tot.v[x] += (double)hi.v[x] + (double)lo.v[x];
-        hi.v[x] = T(0);
-        lo.v[x] = T(0);
-    }
-}
+// Error-free accumulation of long rows (> kExactRow nonzeros) uses float64
+// products of the float32 inputs -- exact, since 24 + 24 bits fit in 53 --
+// summed in float64 (DFMA), in every family.
 
 template <typename T, int V>
 __device__ __forceinline__ Vec<T, V> narrow(const Vec<double, V> &tot) {

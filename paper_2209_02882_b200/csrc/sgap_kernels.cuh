@@ -52,9 +52,8 @@ __device__ __forceinline__ Vec<double, V> rb_row_impl(const int *__restrict__ ci
                                                       const T *__restrict__ av, int p, int end,
                                                       const T *__restrict__ bk, int N,
                                                       bool vec4) {
-    Vec<T, V> acc, lo;
+    Vec<T, V> acc;
     acc.zero();
-    lo.zero();
     Vec<double, V> tot;
     tot.zero();
     int since_fold = 0;
@@ -88,7 +87,7 @@ __device__ __forceinline__ Vec<double, V> rb_row_impl(const int *__restrict__ ci
             step(v.v[3], b3);
             since_fold += 4;
             if (since_fold >= kFoldEvery) {
-                fold2<T, V>(tot, acc, lo);
+                fold<T, V>(tot, acc);
                 since_fold = 0;
             }
         }
@@ -100,13 +99,13 @@ __device__ __forceinline__ Vec<double, V> rb_row_impl(const int *__restrict__ ci
             one(p + 3);
             since_fold += 4;
             if (since_fold >= kFoldEvery) {
-                fold2<T, V>(tot, acc, lo);
+                fold<T, V>(tot, acc);
                 since_fold = 0;
             }
         }
     }
     for (; p < end; ++p) one(p);
-    fold2<T, V>(tot, acc, lo);
+    fold<T, V>(tot, acc);
     return tot;
 }
 
