@@ -17,7 +17,8 @@ import numpy as np
 
 from .lowering import compute_block_starts
 
-__all__ = ["ShardPlan", "shard_starts", "bytes_balanced_starts", "plan_shards", "shard_csr"]
+__all__ = ["ShardPlan", "shard_starts", "shard_starts_device", "bytes_balanced_starts",
+           "plan_shards", "shard_csr"]
 
 
 def shard_starts(row_ptr, k: int) -> np.ndarray:
@@ -34,6 +35,30 @@ def shard_starts(row_ptr, k: int) -> np.ndarray:
     starts[0] = 0
     starts[k] = m
     return starts
+
+
+def shard_starts_device(row_ptr, k: int):
+    """``shard_starts`` on the device: the same cut points from the device
+    block-start kernel (sgap_block_starts, lowering.compute_block_starts) and
+    the two fix-ups; ``row_ptr`` is an int32 CUDA tensor, the result an int32
+    CUDA tensor [k+1] (bit-identical to the host version, tests/test_gpu_parity)."""
+    import torch
+
+    from . import _native
+
+    if k < 1:
+        raise ValueError("shard count must be positive")
+    m = int(row_ptr.numel()) - 1
+    nnz = int(row_ptr[-1].item())
+    if nnz == 0:
+        return ((torch.arange(k + 1, dtype=torch.int64, device=row_ptr.device) * m) // k).to(torch.int32)
+    out = torch.empty(k + 1, dtype=torch.int32, device=row_ptr.device)
+    st = torch.cuda.current_stream(row_ptr.device).cuda_stream
+    _native.check(_native.lib().sgap_block_starts(row_ptr.data_ptr(), m, -(-nnz // k), k,
+                                                   out.data_ptr(), st), "sgap_block_starts")
+    out[0] = 0
+    out[k] = m
+    return out
 
 
 def bytes_balanced_starts(row_ptr, k: int, n: int) -> np.ndarray:

@@ -299,3 +299,20 @@ def test_config1_every_candidate_every_walk():
         assert err <= F32_TOL, (cand.label(), err)
         runs += 1
     assert runs > 250
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 8])
+def test_device_shard_cuts_bit_exact(k):
+    """partition.shard_starts_device == partition.shard_starts (the multi-GPU
+    cut points) on R-MAT, a matrix with leading/trailing empty
+    rows and an empty one."""
+    from paper_2209_02882_b200 import generators as G
+    from paper_2209_02882_b200.partition import shard_starts, shard_starts_device
+
+    rm = G.rmat(14, 16, seed=2)
+    cases = [rm.row_ptr.numpy().astype(np.int64),
+             np.array([0, 0, 0, 3, 3, 7, 7, 7, 9, 9, 9], np.int64),
+             np.zeros(6, np.int64)]
+    for rp in cases:
+        got = shard_starts_device(torch.as_tensor(rp.astype(np.int32), device="cuda"), k)
+        assert np.array_equal(got.cpu().numpy(), shard_starts(rp, k)), (k, rp[:8])
