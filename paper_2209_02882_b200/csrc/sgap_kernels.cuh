@@ -42,7 +42,7 @@ __device__ __forceinline__ void rb_step(Vec<T, V> &acc, const int *__restrict__ 
                                         const T *__restrict__ av, int p,
                                         const T *__restrict__ bk, int N) {
     Vec<T, V> b;
-    ldg_vec<T, V>(b, bk + (long long)__ldg(ci + p) * N);
+    ldg_vec<T, V>(b, row_ptr(bk, __ldg(ci + p), N));
     fma_vec<T, V>(acc, __ldg(av + p), b);
 }
 
@@ -67,7 +67,7 @@ __device__ __forceinline__ Vec<double, V> rb_row_impl(const int *__restrict__ ci
     };
     auto one = [&](int q) {
         Vec<T, V> b;
-        ldg_vec<T, V>(b, bk + (long long)__ldg(ci + q) * N);
+        ldg_vec<T, V>(b, row_ptr(bk, __ldg(ci + q), N));
         step(__ldg(av + q), b);
     };
     if (vec4) {
@@ -77,10 +77,10 @@ __device__ __forceinline__ Vec<double, V> rb_row_impl(const int *__restrict__ ci
             Vec<T, 4> v;
             ldg_vec<T, 4>(v, av + p);
             Vec<T, V> b0, b1, b2, b3;
-            ldg_vec<T, V>(b0, bk + (long long)c.x * N);
-            ldg_vec<T, V>(b1, bk + (long long)c.y * N);
-            ldg_vec<T, V>(b2, bk + (long long)c.z * N);
-            ldg_vec<T, V>(b3, bk + (long long)c.w * N);
+            ldg_vec<T, V>(b0, row_ptr(bk, c.x, N));
+            ldg_vec<T, V>(b1, row_ptr(bk, c.y, N));
+            ldg_vec<T, V>(b2, row_ptr(bk, c.z, N));
+            ldg_vec<T, V>(b3, row_ptr(bk, c.w, N));
             step(v.v[0], b0);
             step(v.v[1], b1);
             step(v.v[2], b2);
@@ -205,7 +205,7 @@ __device__ __forceinline__ Vec<double, V> rb_row_staged(const int *__restrict__ 
             Vec<T, V> b[U];
 #pragma unroll
             for (int u = 0; u < U; ++u)
-                gather_vec<T, V>(b[u], bk + (long long)__shfl_sync(kFull, c_l, (j + u) & 31) * N);
+                gather_vec<T, V>(b[u], row_ptr(bk, __shfl_sync(kFull, c_l, (j + u) & 31), N));
             if (j + U <= nv) {
 #pragma unroll
                 for (int u = 0; u < U; ++u) fma_vec<T, V>(acc, __shfl_sync(kFull, v_l, j + u), b[u]);
@@ -242,7 +242,7 @@ __device__ __forceinline__ Vec<T, V> rb_short_staged(const int *__restrict__ ci,
             Vec<T, V> b[U];
 #pragma unroll
             for (int u = 0; u < U; ++u)
-                gather_vec<T, V>(b[u], bk + (long long)__shfl_sync(kFull, c_l, (j + u) & 31) * N);
+                gather_vec<T, V>(b[u], row_ptr(bk, __shfl_sync(kFull, c_l, (j + u) & 31), N));
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const T v = __shfl_sync(kFull, v_l, (j + u) & 31);
@@ -484,7 +484,7 @@ k_nnz_one(const int *__restrict__ rowid, const int *__restrict__ ci, const T *__
                 if constexpr (R > 1) sl = seg_lanes<R, int>(row, in_grid);
                 Vec<T, V> bv;
                 bv.zero();
-                if (in_nnz && tok) ldg_vec<T, V>(bv, B + (long long)col * N + kcol);
+                if (in_nnz && tok) ldg_vec<T, V>(bv, row_ptr(B + kcol, col, N));
                 const bool writer = (R == 1 ? in_nnz : sl.tail) && tok;
                 // Warps that touch a float64-table row (hub rows) form exact
                 // float64 products and segment sums: float32 product rounding
@@ -543,20 +543,29 @@ template <typename T>
 struct GlobalA {
     const int *rowid, *ci;
     const T *av;
-    __device__ __forceinline__ int row(long long q) const { return __ldg(rowid + q); }
-    __device__ __forceinline__ int col(long long q) const { return __ldg(ci + q); }
-    __device__ __forceinline__ T val(long long q) const { return __ldg(av + q); }
+    // positions are < 2^31 (sgap_run checks nnz): 32-bit unsigned offsets
+    // give one IMAD.WIDE.U32 per address instead of 64-bit index arithmetic
+    template <typename I>
+    __device__ __forceinline__ int row(I q) const { return __ldg(rowid + (unsigned)q); }
+    template <typename I>
+    __device__ __forceinline__ int col(I q) const { return __ldg(ci + (unsigned)q); }
+    template <typename I>
+    __device__ __forceinline__ T val(I q) const { return __ldg(av + (unsigned)q); }
     // four consecutive positions, q % 4 == 0 (16-byte aligned)
-    __device__ __forceinline__ void load4(long long q, int4 &c, Vec<T, 4> &v, int4 &r) const {
-        c = __ldg(reinterpret_cast<const int4 *>(ci + q));
-        r = __ldg(reinterpret_cast<const int4 *>(rowid + q));
-        ldg_vec<T, 4>(v, av + q);
+    template <typename I>
+    __device__ __forceinline__ void load4(I q, int4 &c, Vec<T, 4> &v, int4 &r) const {
+        const unsigned u = (unsigned)q;
+        c = __ldg(reinterpret_cast<const int4 *>(ci + u));
+        r = __ldg(reinterpret_cast<const int4 *>(rowid + u));
+        ldg_vec<T, 4>(v, av + u);
     }
     // pull the A lines `ahead` positions further into L1 (one per 32 positions)
-    __device__ __forceinline__ void prefetch(long long q) const {
-        prefetch_l1(ci + q);
-        prefetch_l1(rowid + q);
-        prefetch_l1(av + q);
+    template <typename I>
+    __device__ __forceinline__ void prefetch(I q) const {
+        const unsigned u = (unsigned)q;
+        prefetch_l1(ci + u);
+        prefetch_l1(rowid + u);
+        prefetch_l1(av + u);
     }
 };
 
@@ -564,7 +573,8 @@ template <typename T>
 struct SharedA {
     const int *sr, *sc;
     const T *sv;
-    __device__ __forceinline__ void prefetch(long long) const {}
+    template <typename I>
+    __device__ __forceinline__ void prefetch(I) const {}
     __device__ __forceinline__ int row(long long q) const { return sr[q]; }
     __device__ __forceinline__ int col(long long q) const { return sc[q]; }
     __device__ __forceinline__ T val(long long q) const { return sv[q]; }
@@ -646,17 +656,18 @@ __device__ __forceinline__ void eb_walk4(const ASrc &A, long long q0, long long 
     tot.zero();
     int since_fold = 0;
     const T *bk = B + kcol;
-    long long q = q0;
-    for (; q + 4 <= qend; q += 4) {
-        if ((q & 31) == 0 && q + 64 < qend) A.prefetch(q + 64);  // A lines two ahead
+    unsigned q = (unsigned)q0;
+    const unsigned qe = (unsigned)qend;
+    for (; q + 4 <= qe; q += 4) {
+        if ((q & 31) == 0 && q + 64 < qe) A.prefetch(q + 64);  // A lines two ahead
         int4 c, r;
         Vec<T, 4> v;
         A.load4(q, c, v, r);
         Vec<T, V> b0, b1, b2, b3;
-        ldg_vec<T, V>(b0, bk + (long long)c.x * N);
-        ldg_vec<T, V>(b1, bk + (long long)c.y * N);
-        ldg_vec<T, V>(b2, bk + (long long)c.z * N);
-        ldg_vec<T, V>(b3, bk + (long long)c.w * N);
+        ldg_vec<T, V>(b0, row_ptr(bk, c.x, N));
+        ldg_vec<T, V>(b1, row_ptr(bk, c.y, N));
+        ldg_vec<T, V>(b2, row_ptr(bk, c.z, N));
+        ldg_vec<T, V>(b3, row_ptr(bk, c.w, N));
         if (r.w == cur) {
             fma_vec<T, V>(acc, v.v[0], b0);
             fma_vec<T, V>(acc, v.v[1], b1);
@@ -686,10 +697,10 @@ __device__ __forceinline__ void eb_walk4(const ASrc &A, long long q0, long long 
             since_fold = 0;
         }
     }
-    for (; q < qend; ++q) {  // < 4 tail positions
+    for (; q < qe; ++q) {  // < 4 tail positions
         const int rq = A.row(q);
         Vec<T, V> b;
-        ldg_vec<T, V>(b, bk + (long long)A.col(q) * N);
+        ldg_vec<T, V>(b, row_ptr(bk, A.col(q), N));
         if (rq != cur) {
             fold<T, V>(tot, acc);
             flush_owned<T, V>(C, N, cur, kcol, tot, lr, here);
@@ -727,10 +738,10 @@ __device__ __forceinline__ void eb_walk4_exact(const ASrc &A, long long q0, long
         Vec<T, 4> v;
         A.load4(q, c, v, r);
         Vec<T, V> b0, b1, b2, b3;
-        ldg_vec<T, V>(b0, bk + (long long)c.x * N);
-        ldg_vec<T, V>(b1, bk + (long long)c.y * N);
-        ldg_vec<T, V>(b2, bk + (long long)c.z * N);
-        ldg_vec<T, V>(b3, bk + (long long)c.w * N);
+        ldg_vec<T, V>(b0, row_ptr(bk, c.x, N));
+        ldg_vec<T, V>(b1, row_ptr(bk, c.y, N));
+        ldg_vec<T, V>(b2, row_ptr(bk, c.z, N));
+        ldg_vec<T, V>(b3, row_ptr(bk, c.w, N));
 #pragma unroll
         for (int x = 0; x < V; ++x) {
             tot.v[x] = fma((double)v.v[0], (double)b0.v[x], tot.v[x]);
@@ -741,7 +752,7 @@ __device__ __forceinline__ void eb_walk4_exact(const ASrc &A, long long q0, long
     }
     for (; q < qend; ++q) {
         Vec<T, V> b;
-        ldg_vec<T, V>(b, bk + (long long)A.col(q) * N);
+        ldg_vec<T, V>(b, row_ptr(bk, A.col(q), N));
         const double a = (double)A.val(q);
 #pragma unroll
         for (int x = 0; x < V; ++x) tot.v[x] = fma(a, (double)b.v[x], tot.v[x]);
@@ -884,10 +895,10 @@ k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
                         Vec<T, 4> v;
                         A.load4(q, c, v, r);
                         Vec<T, V> b0, b1, b2, b3;
-                        ldg_vec<T, V>(b0, bk + (long long)c.x * N);
-                        ldg_vec<T, V>(b1, bk + (long long)c.y * N);
-                        ldg_vec<T, V>(b2, bk + (long long)c.z * N);
-                        ldg_vec<T, V>(b3, bk + (long long)c.w * N);
+                        ldg_vec<T, V>(b0, row_ptr(bk, c.x, N));
+                        ldg_vec<T, V>(b1, row_ptr(bk, c.y, N));
+                        ldg_vec<T, V>(b2, row_ptr(bk, c.z, N));
+                        ldg_vec<T, V>(b3, row_ptr(bk, c.w, N));
 #pragma unroll
                         for (int x = 0; x < V; ++x) {
                             tot.v[x] = fma((double)v.v[0], (double)b0.v[x], tot.v[x]);
@@ -898,7 +909,7 @@ k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
                     }
                     for (; q < end; ++q) {
                         Vec<T, V> b;
-                        ldg_vec<T, V>(b, bk + (long long)A.col(q) * N);
+                        ldg_vec<T, V>(b, row_ptr(bk, A.col(q), N));
                         const double a = (double)A.val(q);
 #pragma unroll
                         for (int x = 0; x < V; ++x) tot.v[x] = fma(a, (double)b.v[x], tot.v[x]);
@@ -1036,7 +1047,7 @@ __device__ __forceinline__ void eb_walk_staged(const int *__restrict__ rowid,
             Vec<T, V> b[U];
 #pragma unroll
             for (int u = 0; u < U; ++u)
-                gather_vec<T, V>(b[u], bk + (long long)__shfl_sync(kFull, c_l, j + u) * N);
+                gather_vec<T, V>(b[u], row_ptr(bk, __shfl_sync(kFull, c_l, j + u), N));
             const unsigned gm = (chm >> j) & ((1u << U) - 1u);
             if (gm == 0u && j + U <= nval) {
 #pragma unroll
@@ -1064,7 +1075,7 @@ __device__ __forceinline__ void eb_walk_staged(const int *__restrict__ rowid,
                         here = own.on;
                     }
                     Vec<T, V> bb;
-                    ldg_vec<T, V>(bb, bk + (long long)c * N);
+                    ldg_vec<T, V>(bb, row_ptr(bk, c, N));
                     fma_vec<T, V>(acc, v, bb);
                 }
             }
