@@ -558,6 +558,7 @@ struct GlobalA {
         c = __ldg(reinterpret_cast<const int4 *>(ci + u));
         r = __ldg(reinterpret_cast<const int4 *>(rowid + u));
         ldg_vec<T, 4>(v, av + u);
+        // (evict-first A loads, __ldcs: 0.833 vs 0.700 ms on config 2)
     }
     // pull the A lines `ahead` positions further into L1 (one per 32 positions)
     template <typename I>
