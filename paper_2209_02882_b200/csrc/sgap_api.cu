@@ -509,10 +509,14 @@ int64_t sgap_long_row_threshold(const sgap_kernel_t *k, int32_t dtype) {
     // 1.1e-5; 4g cost config 3 6% in float64 atomics for no accuracy gain.
     // nnz-one flushes r-term segment sums: rows past 32r (min 128).
     if (k->family == SGAP_NNZ_MULTIPLE) {
-        // <= 32 flushes of short partials (small g), <= 16 of long ones
+        // <= 32 flushes of short partials (small g), <= 16 of long ones, and
+        // never above the error-free length: a row past kExactRow must be in
+        // the table to take the exact path (config 3 measured 9.1e-6 with
+        // its 4k-8k rows summed in float32 at g = 512)
         long long t = 16LL * k->g;
         if (t < 2048) t = 2048;
         if (t > 32LL * k->g) t = 32LL * k->g;
+        if (t > kExactRow) t = kExactRow;
         return t < 128 ? 128 : t;
     }
     if (k->family != SGAP_NNZ_ONE) return -1;  // row families own their rows
