@@ -25,6 +25,9 @@ namespace sgap {
 
 constexpr int kBatch = 4;     // independent gathers kept in flight per lane
 constexpr int kFoldEvery = 8;  // float32 partial sums fold into float64 every 8 terms
+#ifndef SGAP_EB_MINB
+#define SGAP_EB_MINB 4  // CTAs per SM the register EB walk is compiled for
+#endif
 
 // ===========================================================================
 // RB + serial reduction: row:g,col:c,r:1 (row-multiple).
@@ -852,8 +855,49 @@ __device__ __forceinline__ void eb_walk(const ASrc &A, long long q0, long long q
     if (own.on && own.end == own.nnz) zero_rows<T, V>(C, N, kcol, (cur & kRowMask) + 1, own.m);
 }
 
+// A chunk inside an exact-flagged (hub) row, walked by the register walk
+// itself: float64 products (exact for float32 inputs) summed in float64, one
+// flush into the float64 table.  Out of line (noinline) so its float64 state
+// does not count against the hot walk's register budget.
+template <typename T, int V>
+__device__ __noinline__ void eb_chunk_f64(const GlobalA<T> A, long long base, long long end,
+                                          const T *__restrict__ B, int N, long long kcol,
+                                          T *__restrict__ C, const LongRows lr, int r_first,
+                                          bool vec4) {
+    Vec<double, V> tot;
+    tot.zero();
+    const T *bk = B + kcol;
+    unsigned q = (unsigned)base;
+    const unsigned qe = (unsigned)end;
+    for (; vec4 && q + 4 <= qe; q += 4) {
+        int4 c, r;
+        Vec<T, 4> v;
+        A.load4(q, c, v, r);
+        Vec<T, V> b0, b1, b2, b3;
+        ldg_vec<T, V>(b0, row_ptr(bk, c.x, N));
+        ldg_vec<T, V>(b1, row_ptr(bk, c.y, N));
+        ldg_vec<T, V>(b2, row_ptr(bk, c.z, N));
+        ldg_vec<T, V>(b3, row_ptr(bk, c.w, N));
+#pragma unroll
+        for (int x = 0; x < V; ++x) {
+            tot.v[x] = fma((double)v.v[0], (double)b0.v[x], tot.v[x]);
+            tot.v[x] = fma((double)v.v[1], (double)b1.v[x], tot.v[x]);
+            tot.v[x] = fma((double)v.v[2], (double)b2.v[x], tot.v[x]);
+            tot.v[x] = fma((double)v.v[3], (double)b3.v[x], tot.v[x]);
+        }
+    }
+    for (; q < qe; ++q) {
+        Vec<T, V> b;
+        ldg_vec<T, V>(b, row_ptr(bk, A.col(q), N));
+        const double a = (double)A.val(q);
+#pragma unroll
+        for (int x = 0; x < V; ++x) tot.v[x] = fma(a, (double)b.v[x], tot.v[x]);
+    }
+    flush_row<T, V>(C, N, r_first, kcol, tot, lr);  // the float64 table
+}
+
 template <typename T, int V, int W, int U, bool PIPE>
-__global__ void __launch_bounds__(256, 4)
+__global__ void __launch_bounds__(256, SGAP_EB_MINB)
 k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
                const T *__restrict__ av, const T *__restrict__ B, T *__restrict__ C,
                const int *__restrict__ rp, int M, int N, long long nnz, int g,
@@ -888,40 +932,8 @@ k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
                 if (own.on && end == nnz)
                     zero_rows<T, V>(C, N, kcol, (r_first & kRowMask) + 1, M);
                 nwb += V;
-                if (exact_inline) {
-                    // a chunk inside an exact-flagged (hub) row: float64
-                    // products (exact for float32 inputs) summed in float64,
-                    // in this walk -- no separate error-free pass to launch
-                    Vec<double, V> tot;
-                    tot.zero();
-                    const T *bk = B + kcol;
-                    long long q = base;
-                    for (; VEC4 && q + 4 <= end; q += 4) {
-                        int4 c, r;
-                        Vec<T, 4> v;
-                        A.load4(q, c, v, r);
-                        Vec<T, V> b0, b1, b2, b3;
-                        ldg_vec<T, V>(b0, row_ptr(bk, c.x, N));
-                        ldg_vec<T, V>(b1, row_ptr(bk, c.y, N));
-                        ldg_vec<T, V>(b2, row_ptr(bk, c.z, N));
-                        ldg_vec<T, V>(b3, row_ptr(bk, c.w, N));
-#pragma unroll
-                        for (int x = 0; x < V; ++x) {
-                            tot.v[x] = fma((double)v.v[0], (double)b0.v[x], tot.v[x]);
-                            tot.v[x] = fma((double)v.v[1], (double)b1.v[x], tot.v[x]);
-                            tot.v[x] = fma((double)v.v[2], (double)b2.v[x], tot.v[x]);
-                            tot.v[x] = fma((double)v.v[3], (double)b3.v[x], tot.v[x]);
-                        }
-                    }
-                    for (; q < end; ++q) {
-                        Vec<T, V> b;
-                        ldg_vec<T, V>(b, row_ptr(bk, A.col(q), N));
-                        const double a = (double)A.val(q);
-#pragma unroll
-                        for (int x = 0; x < V; ++x) tot.v[x] = fma(a, (double)b.v[x], tot.v[x]);
-                    }
-                    flush_row<T, V>(C, N, r_first, kcol, tot, lr);  // the float64 table
-                }
+                if (exact_inline)  // a chunk inside an exact-flagged (hub) row
+                    eb_chunk_f64<T, V>(A, base, end, B, N, kcol, C, lr, r_first, VEC4);
                 continue;
             }
             if (VEC4)
