@@ -176,10 +176,10 @@ def test_config5_rmat_scale24_sampled_rows():
 
 
 def test_exact_rows_and_empty_row_gaps():
-    """Rows beyond the error-free threshold (> 65,536 nonzeros) next to empty
-    rows at the start, middle and end of the matrix: the owner-mode walk
+    """Rows beyond the error-free threshold (here > 65,536 nonzeros) next to
+    empty rows at the start, middle and end of the matrix: the owner-mode walk
     zero-fills every empty row itself, including around chunks that the
-    exact-row kernel takes over."""
+    exact-row path takes over."""
     rng = np.random.default_rng(11)
     m, k, n = 64, 100_000, 128
     lens = np.zeros(m, dtype=np.int64)
@@ -198,12 +198,21 @@ def test_exact_rows_and_empty_row_gaps():
     want = oracle.spmm_f64(a.row_ptr.cpu().numpy(), a.col_idx.cpu().numpy(), a.vals.cpu().numpy(),
                            b.cpu().numpy(), n)
     c = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    # every family and walk over the error-free rows: EB register walk
+    # (inline float64 chunks), TMA and lane-staged walks (k_nnz_multiple_exact
+    # overlapped by programmatic dependent launch), nnz-one (float64 table
+    # sums), RB walks (float64 products per row), row-reciprocal groups
     for text, p, variant in (("nnz:512,col:4,r:1", 256, 1), ("nnz:64,col:4,r:1", 1024, 2),
-                             ("nnz:32,col:4,r:1", 256, 1)):
+                             ("nnz:32,col:4,r:1", 256, 1), ("nnz:256,col:4,r:1", 256, 3),
+                             ("nnz:1,col:4,r:8", 1024, 0), ("nnz:1,col:4,r:1", 256, 0),
+                             ("row:1,col:4,r:1", 256, 0), ("row:4,col:4,r:1", 256, 2),
+                             ("row:4,col:4,r:1", 256, 4), ("row:1/8,col:4,r:8", 256, 0),
+                             ("row:1/32,col:1,r:32", 256, 0)):
         tpl = algorithm_template(parse_point(text), KernelConfig(n=n, p=p))
         kk = lower(tpl, _Rp(m, k, rp), compute_starts=False)
         aux = prepare_aux(kk, a)
-        assert aux.has_exact_rows == 1
+        if kk.family == "nnz-multiple":
+            assert aux.has_exact_rows == 1
         c.fill_(float("nan"))
         spmm(kk, a, b, c, aux=aux, hw_variant=variant)
         got = c.cpu().numpy()
