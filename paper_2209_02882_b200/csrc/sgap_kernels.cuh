@@ -274,8 +274,10 @@ k_row_staged(const int *__restrict__ rp, const int *__restrict__ ci, const T *__
     // Measured and not kept on config 4 (N=128, 3.26 ms here):
     // software-pipelining a warp's rows (next row's bounds and (col, val)
     // under this row's gathers): 3.41 ms; a 32-register walk for rows <= 32
-    // at 56 warps/SM plus a second launch for longer rows: 3.50 ms (more
-    // warps, more L1 thrash: the walk is L1-throughput- not occupancy-bound).
+    // at 56 warps/SM plus a second launch for longer rows: 3.50 ms; a warp
+    // per row PAIR gathering the B rows the two rows share once (1/3 fewer
+    // gathers on the stencil, columns matched by shuffle binary search):
+    // 3.13 ms, no gain -- the walk is latency-chained, not L1-bound.
     const int warps = (int)(blockDim.x >> 5);
     const int w = (int)(threadIdx.x >> 5);
     const long long kcol = (long long)lane_id() * V;
