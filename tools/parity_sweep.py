@@ -34,15 +34,18 @@ ap.add_argument("--n", type=int, default=0)
 ap.add_argument("--tol", type=float, default=1e-5)
 ap.add_argument("--out", default="")
 ap.add_argument("--sample-rows", type=int, default=2000)
+ap.add_argument("--dtype", default="f32", choices=["f32", "f64"],
+                help="f64: the reference's default precision (sim.run precision='double')")
 args = ap.parse_args()
 
 dev = torch.device("cuda", 0)
 n = args.n or bench.default_n(args.config)
 g, desc, _ = bench.build_workload(args.config, 1, 1, dev)
+dt = torch.float64 if args.dtype == "f64" else torch.float32
 a = DeviceCsr(g.num_rows, g.num_cols, g.row_ptr.to(torch.int32), g.col_idx.to(torch.int32),
-              g.vals.to(torch.float32))
-b = bench.dense_b(g.num_cols, n, 1, dev)
-c = torch.empty((a.num_rows, n), dtype=torch.float32, device=dev)
+              g.vals.to(dt))
+b = bench.dense_b(g.num_cols, n, 1, dev).to(dt)
+c = torch.empty((a.num_rows, n), dtype=dt, device=dev)
 rp = a.row_ptr.cpu().numpy().astype(np.int64)
 want = reference_spmm_f64(a, b, n)
 
@@ -55,7 +58,7 @@ ci = a.col_idx.cpu().numpy()
 av = a.vals.cpu().numpy()
 sub_rp = np.concatenate([[0], np.cumsum(lens[rows])]).astype(np.int32)
 sub_ci = np.concatenate([ci[rp[r]:rp[r + 1]] for r in rows]).astype(np.int32)
-sub_av = np.concatenate([av[rp[r]:rp[r + 1]] for r in rows]).astype(np.float32)
+sub_av = np.concatenate([av[rp[r]:rp[r + 1]] for r in rows])
 cpu = oracle.spmm_f64(sub_rp, sub_ci, sub_av, b.cpu().numpy(), n)
 dev_rows = want[torch.as_tensor(rows, device=dev)].cpu().numpy()
 pinned = bool(np.array_equal(cpu.reshape(dev_rows.shape), dev_rows))
@@ -92,7 +95,7 @@ for cand in candidates(n):
         fails.append(rows_out[-1])
         print("FAIL", cand.label(), err, flush=True)
     del aux
-summary = {"workload": desc, "n": n, "candidates": len(rows_out), "tol": args.tol,
+summary = {"workload": desc, "n": n, "dtype": args.dtype, "candidates": len(rows_out), "tol": args.tol,
            "failures": len(fails), "max_err": max(r["err"] for r in rows_out),
            "worst": max(rows_out, key=lambda r: r["err"]), "device_reference_pinned": pinned,
            "seconds": time.time() - t0}
