@@ -185,7 +185,7 @@ inline int tma_tile_for(int g) {
     return (int)((kTmaTile / l) * l);
 }
 
-template <typename T, int V, int W, int U, bool PIPE, int STAGES = 3, int MINB = 3>
+template <typename T, int V, int W, int U, int STAGES = 3, int MINB = 3>
 int launch_nnz_multiple(bool tma, int tile, int owner, const sgap_kernel_t &k,
                         const sgap_csr_t &a, const T *B, T *C, const int *rowid,
                         const LongRows &lr, unsigned long long *wb, cudaStream_t st, bool pdl,
@@ -193,7 +193,7 @@ int launch_nnz_multiple(bool tma, int tile, int owner, const sgap_kernel_t &k,
     const long long total_pos = k.grid_size * k.chunk;
     if (tma) {
         const size_t smem = tma_smem_bytes<T, STAGES>();
-        auto kern = k_nnz_multiple_tma<T, V, W, U, PIPE, STAGES, MINB>;
+        auto kern = k_nnz_multiple_tma<T, V, W, U, STAGES, MINB>;
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
             cudaSuccess)
             return SGAP_ERR_CUDA;
@@ -213,7 +213,7 @@ int launch_nnz_multiple(bool tma, int tile, int owner, const sgap_kernel_t &k,
     const int blk = k.hw_block > 0 ? k.hw_block : kHwBlock;
     const int vec4 = (k.g % 4 == 0) && aligned(rowid, 16) && aligned(a.d_col_idx, 16) &&
                      aligned(a.d_vals, 16);
-    return launch_k(k_nnz_multiple<T, V, W, U, PIPE>, dim3(grid_for(items, blk)), dim3(blk), 0, st,
+    return launch_k(k_nnz_multiple<T, V, W, U>, dim3(grid_for(items, blk)), dim3(blk), 0, st,
                     pdl, rowid, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, a.d_row_ptr,
                     (int)a.num_rows, k.n, a.nnz, k.g, total_pos, vec4, owner, lr, wb, exact_inline);
 }
@@ -278,7 +278,7 @@ int run_nnz_multiple_w(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, 
                         a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, a.d_row_ptr,
                         (int)a.num_rows, k.n, a.nnz, k.g, total_pos, owner, lr, wb);
     }
-    return launch_nnz_multiple<T, V, W, 4, false>(tma, tile, owner, k, a, B, C, rowid, lr, wb, st,
+    return launch_nnz_multiple<T, V, W, 4>(tma, tile, owner, k, a, B, C, rowid, lr, wb, st,
                                                    pdl, exact_inline ? 1 : 0);
 }
 

@@ -778,12 +778,13 @@ struct WalkBatch {
     Vec<T, V> b[U];
 };
 
-// The serial nnz walk of one chunk [q0, qend) for one column tile, software
-// pipelined: batch i+1's (col, val, row) and its U B-row gathers are issued
-// before batch i is consumed, so 2U gathers are in flight per lane.  A flush
-// (row change or chunk end) is one writeback; partial sums fold into float64
-// every 32 positions.
-template <typename T, int V, int U, bool PIPE, class ASrc>
+// The serial nnz walk of one chunk [q0, qend) for one column tile when the
+// chunk is not 4-aligned (g % 4 != 0 or unaligned A): U positions' (col, val,
+// row) and their U B-row gathers per step, then the serial flush logic.  A
+// flush (row change or chunk end) is one writeback; partial sums fold into
+// float64 every kFoldEvery positions.  (Software-pipelining batch i+1 under
+// batch i was measured slower: the registers cost more occupancy.)
+template <typename T, int V, int U, class ASrc>
 __device__ __forceinline__ void eb_walk(const ASrc &A, long long q0, long long qend,
                                         const T *__restrict__ B, int N, long long kcol,
                                         T *__restrict__ C, const LongRows &lr, const Owner &own,
@@ -831,25 +832,10 @@ __device__ __forceinline__ void eb_walk(const ASrc &A, long long q0, long long q
             since_fold = 0;
         }
     };
-    if constexpr (PIPE) {
-        WalkBatch<T, V, U> w0, w1;
-        fetch(q0, w0);
-        for (long long q = q0;;) {
-            if (q + U < qend) fetch(q + U, w1);
-            consume(q, w0);
-            q += U;
-            if (q >= qend) break;
-            if (q + U < qend) fetch(q + U, w0);
-            consume(q, w1);
-            q += U;
-            if (q >= qend) break;
-        }
-    } else {
-        WalkBatch<T, V, U> w0;
-        for (long long q = q0; q < qend; q += U) {
-            fetch(q, w0);
-            consume(q, w0);
-        }
+    WalkBatch<T, V, U> w0;
+    for (long long q = q0; q < qend; q += U) {
+        fetch(q, w0);
+        consume(q, w0);
     }
     fold<T, V>(tot, acc);
     const bool complete = here && __ldg(own.rp + (cur & kRowMask) + 1) == own.end;
@@ -899,7 +885,7 @@ __device__ __noinline__ void eb_chunk_f64(const GlobalA<T> A, long long base, lo
     flush_row<T, V>(C, N, r_first, kcol, tot, lr);  // the float64 table
 }
 
-template <typename T, int V, int W, int U, bool PIPE>
+template <typename T, int V, int W, int U>
 __global__ void __launch_bounds__(256, SGAP_EB_MINB)
 k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
                const T *__restrict__ av, const T *__restrict__ B, T *__restrict__ C,
@@ -942,7 +928,7 @@ k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
             if (VEC4)
                 eb_walk4<T, V>(A, base, end, B, N, (long long)tile * V, C, lr, own, nwb);
             else
-                eb_walk<T, V, U, PIPE>(A, base, end, B, N, (long long)tile * V, C, lr, own, nwb);
+                eb_walk<T, V, U>(A, base, end, B, N, (long long)tile * V, C, lr, own, nwb);
         }
     }
     flush_count(wb, nwb);
@@ -1171,7 +1157,7 @@ constexpr size_t tma_smem_bytes() {
            2 * STAGES * sizeof(unsigned long long);
 }
 
-template <typename T, int V, int W, int U, bool PIPE, int kTmaStages, int MINB>
+template <typename T, int V, int W, int U, int kTmaStages, int MINB>
 __global__ void __launch_bounds__(kTmaThreads, MINB)
 k_nnz_multiple_tma(const int *__restrict__ rowid, const int *__restrict__ ci,
                    const T *__restrict__ av, const T *__restrict__ B, T *__restrict__ C,
@@ -1265,7 +1251,7 @@ k_nnz_multiple_tma(const int *__restrict__ rowid, const int *__restrict__ ci,
                     if (VEC4)
                         eb_walk4<T, V>(SA, q0, qend, B, N, (long long)tc * V, C, lr, own, nwb);
                     else
-                        eb_walk<T, V, U, PIPE>(SA, q0, qend, B, N, (long long)tc * V, C, lr, own,
+                        eb_walk<T, V, U>(SA, q0, qend, B, N, (long long)tc * V, C, lr, own,
                                                nwb);
                 }
             }
