@@ -145,8 +145,9 @@ def heuristic(stats: MatrixStats, n: int) -> Candidate:
     * regular rows (cv < 1, max <= 8 x mean):
       - n >= 16: RB + serial, 4 rows per logical thread, interleaved CTA
         mapping, c = 4 (27-pt stencil at N=128);
-      - long rows (mean >= 32): RB + parallel group of 2 lanes, widest
-        vector (uniform 1%: flexible r=2 beats r=32 at every n);
+      - long rows (mean >= 32): RB + parallel group -- 8 lanes over single
+        columns for n <= 8, 2 lanes otherwise (uniform 1%: flexible small
+        groups beat r=32 at every n);
       - n < 16 and short rows: RB + serial, one lane per row with the widest
         vector (stencil at N=4/8);
     * skewed rows (power law, hub rows): EB + serial walk with the widest
@@ -158,7 +159,15 @@ def heuristic(stats: MatrixStats, n: int) -> Candidate:
     regular = stats.cv_row < 1.0 and stats.max_row <= 8 * max(stats.mean_row, 1.0)
     if regular:
         if stats.mean_row >= 32:
-            pt = f"row:1/2,col:{col(widest)},r:2"
+            # long regular rows: a small parallel group; narrow N wants a
+            # wider group over single columns (config 1 sweeps: n=4 best
+            # row:1/8,col:1,r:8, n=32 row:1/2,col:2,r:2)
+            if n <= 8:
+                pt = "row:1/8,col:1,r:8"
+            elif n <= 32:
+                pt = f"row:1/2,col:{col(min(widest, 2))},r:2"
+            else:
+                pt = f"row:1/2,col:{col(widest)},r:2"
             p = _first_p(pt, n)
             if p is not None:
                 return Candidate(pt, p)

@@ -24,7 +24,8 @@ def test_heuristic_matrix_classes():
     assert heuristic(RMAT20, 128).point.startswith("nnz:")      # power law -> EB walk
     assert heuristic(STENCIL160, 128).point.startswith("row:4")  # regular -> RB
     assert heuristic(STENCIL160, 4).point == "row:1,col:4,r:1"
-    assert heuristic(UNIFORM1, 4).point.startswith("row:1/2")    # flexible group beats r=32
+    assert heuristic(UNIFORM1, 4).point == "row:1/8,col:1,r:8"    # flexible group beats r=32
+    assert heuristic(UNIFORM1, 32).point == "row:1/2,col:2,r:2"
 
 
 def test_candidate_grid_covers_families_and_walks():
