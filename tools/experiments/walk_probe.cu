@@ -175,6 +175,67 @@ __global__ void __launch_bounds__(256, MINB) k_staged(const int *__restrict__ ri
     }
 }
 
+// ---- variant 2: B rows gathered by cp.async into a per-warp shared ring ------
+// D positions in flight per warp without holding them in registers.
+template <int D, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_ring(const int *__restrict__ rid, const int *__restrict__ ci,
+                                                    const float *__restrict__ av, long long nnz,
+                                                    const float *__restrict__ B, float *__restrict__ C) {
+    constexpr int G = 512;
+    extern __shared__ float4 ring[];  // [8 warps][D][32]
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    float4 *my = ring + (size_t)wib * D * 32;
+    const unsigned sbase = (unsigned)__cvta_generic_to_shared(my) + lane * 16;
+    const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    const long long nchunks = (nnz + G - 1) / G;
+    for (long long ch = warp; ch < nchunks; ch += nw) {
+        const long long base = ch * G;
+        const long long end = min(base + G, nnz);
+        const int n = (int)(end - base);
+        auto issue = [&](int p) {  // position p (relative) -> slot p % D
+            if (p < n) {
+                const int c = __ldg(ci + base + p);
+                const float *src = B + (size_t)(unsigned)c * 128 + lane * 4;
+                const unsigned dst = sbase + (unsigned)((p % D) * 32 * 16);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+            }
+        };
+        // prologue: D positions in flight, one commit group per 4
+        for (int p = 0; p < D; p += 4) {
+            issue(p); issue(p + 1); issue(p + 2); issue(p + 3);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+        int cur = __ldg(rid + base);
+        float4 acc = make_float4(0, 0, 0, 0);
+        for (int p = 0; p < n; p += 4) {
+            asm volatile("cp.async.wait_group %0;" ::"n"(D / 4 - 1) : "memory");
+            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (p + u < n) {
+                    const float4 b = my[((p + u) % D) * 32 + lane];
+                    const float v = __ldg(av + base + p + u);
+                    const int r = __ldg(rid + base + p + u);
+                    if (r != cur) {
+                        atomicAdd(reinterpret_cast<float4 *>(C + (long long)cur * 128) + lane, acc);
+                        acc = make_float4(0, 0, 0, 0);
+                        cur = r;
+                    }
+                    acc.x = fmaf(v, b.x, acc.x); acc.y = fmaf(v, b.y, acc.y);
+                    acc.z = fmaf(v, b.z, acc.z); acc.w = fmaf(v, b.w, acc.w);
+                }
+            }
+            __syncwarp();
+            issue(p + D); issue(p + D + 1); issue(p + D + 2); issue(p + D + 3);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        atomicAdd(reinterpret_cast<float4 *>(C + (long long)cur * 128) + lane, acc);
+        __syncwarp();
+    }
+}
+
 // ---- reference: one thread per (row, column), float64 ------------------------------
 __global__ void k_ref(const int *rp, const int *ci, const float *av, int M, const float *B, double *C) {
     long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -269,6 +330,21 @@ int main(int argc, char **argv) {
     STAGEDN(4, 256, 0, 4, 0) STAGEDN(4, 256, 0, 4, 1) STAGEDN(4, 256, 0, 4, 3)
     STAGEDN(8, 256, 0, 3, 0) STAGEDN(8, 256, 0, 3, 1) STAGEDN(8, 256, 0, 3, 3)
     STAGEDN(4, 256, 2, 4, 0) STAGEDN(4, 256, 2, 4, 1) STAGEDN(4, 256, 2, 4, 3)
+#define RING(D, MINB)                                                                              \
+    {                                                                                              \
+        const size_t smem = (size_t)8 * D * 32 * 16;                                               \
+        cudaFuncSetAttribute(k_ring<D, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ring<D, MINB>, 256, smem);           \
+        cudaMemsetAsync(C, 0, (size_t)M * N * 4);                                                  \
+        k_ring<D, MINB><<<sms * occ, 256, smem>>>(rid, ci, av, nnz, B, C);                         \
+        CK(cudaDeviceSynchronize());                                                               \
+        char nm[64]; snprintf(nm, 64, "ring D=%d occ=%d", D, occ);                                 \
+        float ms = timeit([&] { k_ring<D, MINB><<<sms * occ, 256, smem>>>(rid, ci, av, nnz, B, C); }); \
+        cudaMemsetAsync(C, 0, (size_t)M * N * 4);                                                  \
+        k_ring<D, MINB><<<sms * occ, 256, smem>>>(rid, ci, av, nnz, B, C);                         \
+        check(nm, ms);                                                                             \
+    }
+    RING(8, 4) RING(16, 3) RING(16, 4) RING(24, 2) RING(32, 2)
     float zms = timeit([&] { cudaMemsetAsync(C, 0, (size_t)M * N * 4); });
     printf("%-28s %.3f ms\n", "memset C alone", zms);
     return 0;
