@@ -101,6 +101,25 @@ def test_config1_every_templated_point(p):
             assert m.atomic_ops == pins[(str(pt), p)]["atomic_ops"]
 
 
+@pytest.mark.parametrize("n", [1, 3, 5, 6, 12])
+def test_odd_and_narrow_widths_every_templated_point(n):
+    """Widths that are not a multiple of 4 take the scalar/float2 tile paths
+    (store_vec narrower than 16 B); every templated point, both precisions."""
+    a = random_csr(1500, 900, 0.02, seed=11)
+    b = random_dense(900, n, seed=12)
+    want32 = oracle_f32(a, b, n)
+    want64 = oracle.spmm_f64(a.row_ptr, a.col_idx, a.vals, b.vals.reshape(900, n), n)
+    cfg = KernelConfig(n=n, p=256)
+    pts = templated(n, 256)
+    assert pts
+    for pt in pts:
+        k = build_kernel(pt, cfg, a)
+        got, _ = run(k, a, b, precision="single")
+        assert oracle.max_rel_error(got.vals, want32) <= F32_TOL, (n, str(pt))
+        got64, _ = run(k, a, b, precision="double")
+        assert oracle.max_rel_error(got64.vals, want64) <= F64_TOL, (n, str(pt))
+
+
 def test_device_block_starts_bit_exact():
     rng = np.random.default_rng(5)
     for trial in range(40):
