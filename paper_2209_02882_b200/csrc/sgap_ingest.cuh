@@ -63,11 +63,54 @@ __device__ __forceinline__ int mm_int(const unsigned char *s, const unsigned cha
     return 0;
 }
 
-// Strict decimal float; exact (correctly rounded) only on Clinger's fast
-// path: <= 19 significant digits, mantissa <= 2^53, |decimal exponent| <= 22,
-// where one IEEE multiply or divide of two exact doubles rounds once.
-// 0 ok; 1 plain decimal off the fast path (the host converts it); 2 anything
-// else (inf/nan/underscores/...: Python judges the whole line).
+#include "sgap_pow5.inc"
+
+// Eisel-Lemire (Lemire, "Number Parsing at a Gigabyte per Second", 2021):
+// w * 10^q correctly rounded to binary64 for w < 2^64 from the 128-bit
+// truncated 5^q (sgap_pow5.inc), one 64x64 product plus a second one when
+// the first leaves the rounding undecided.  Returns false (the host converts
+// the token) where the method cannot decide or the result is not a normal
+// finite double: |q| outside the table, a still-ambiguous product outside
+// q in [-27, 55], subnormal or overflowing results.
+__device__ __forceinline__ bool mm_eisel_lemire(unsigned long long w, int q, double &out) {
+    if (q < SGAP_POW5_MIN_Q || q > SGAP_POW5_MAX_Q) return false;
+    const int lz = __clzll((long long)w);
+    w <<= lz;
+    const unsigned long long *t = kPow5 + 2 * (q - SGAP_POW5_MIN_Q);
+    unsigned long long hi = __umul64hi(w, t[0]);
+    unsigned long long lo = w * t[0];
+    if ((hi & 0x1FFULL) == 0x1FFULL) {
+        const unsigned long long sh = __umul64hi(w, t[1]);
+        lo += sh;
+        if (sh > lo) ++hi;
+        if (lo == ~0ULL && (q < -27 || q > 55)) return false;
+    }
+    const int upper = (int)(hi >> 63);
+    const int shift = upper + 9;
+    unsigned long long mant = hi >> shift;
+    // floor(log2(10^q)) + 63 as (217706 q) >> 16, arithmetic shift
+    long long p2 = ((217706LL * q) >> 16) + 63 + upper - lz + 1023;
+    if (p2 <= 0) return false;
+    if (lo <= 1 && q >= -4 && q <= 23 && (mant & 3) == 1 && (mant << shift) == hi)
+        mant &= ~1ULL;  // exactly halfway: round to even
+    mant += mant & 1;
+    mant >>= 1;
+    if (mant >= (2ULL << 52)) {
+        mant = 1ULL << 52;
+        ++p2;
+    }
+    mant &= ~(1ULL << 52);
+    if (p2 >= 2047) return false;
+    out = __longlong_as_double((long long)(((unsigned long long)p2 << 52) | mant));
+    return true;
+}
+
+// Strict decimal float, correctly rounded: Clinger's fast path (mantissa
+// <= 2^53, |decimal exponent| <= 22: one IEEE multiply or divide of two
+// exact doubles) and Eisel-Lemire for the rest of <= 19 significant digits.
+// 0 ok; 1 plain decimal neither method takes (> 19 significant digits,
+// subnormal/overflowing, undecided: the host converts it); 2 anything else
+// (inf/nan/underscores/...: Python judges the whole line).
 __device__ __forceinline__ int mm_float(const unsigned char *s, const unsigned char *e, double &out) {
     const double p10[23] = {1e0,  1e1,  1e2,  1e3,  1e4,  1e5,  1e6,  1e7,  1e8,  1e9,  1e10, 1e11,
                             1e12, 1e13, 1e14, 1e15, 1e16, 1e17, 1e18, 1e19, 1e20, 1e21, 1e22};
@@ -108,8 +151,10 @@ __device__ __forceinline__ int mm_float(const unsigned char *s, const unsigned c
     if (w == 0) {
         v = 0.0;
     } else {
-        if (w > (1ULL << 53) || d < -22 || d > 22) return 1;
-        v = d >= 0 ? __dmul_rn((double)w, p10[d]) : __ddiv_rn((double)w, p10[-d]);
+        if (w <= (1ULL << 53) && d >= -22 && d <= 22)
+            v = d >= 0 ? __dmul_rn((double)w, p10[d]) : __ddiv_rn((double)w, p10[-d]);
+        else if (!mm_eisel_lemire(w, d, v))
+            return 1;
     }
     out = neg ? -v : v;
     return 0;

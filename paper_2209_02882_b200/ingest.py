@@ -11,8 +11,10 @@ per-entry work on the GPU:
   duplicate runs in np.add.reduceat order (``sgap_mm_sum_runs``) and build
   row_ptr;
 * host again, only where needed: lines whose tokens fall outside the strict
-  device grammar (underscores, inf/nan, > 19 significant digits, values off
-  Clinger's exact fast path) are converted with Python's own int()/float(),
+  device grammar (underscores, inf/nan) are converted with Python's own
+  int()/float(); plain decimals the device cannot convert exactly (> 19
+  significant digits, subnormal or overflowing: Clinger's fast path and
+  Eisel-Lemire cover the rest) in one numpy batch,
   and the first bad line (if any) is re-checked in Python for the reference's
   exact message and line number.
 
@@ -92,9 +94,11 @@ def _host_csr(text: str, device) -> DeviceCoo:
                      torch.as_tensor(m.vals, dtype=torch.float64, device=dev))
 
 
-def load_matrix_market_device(text: str | bytes, device="cuda") -> DeviceCoo:
+def load_matrix_market_device(text: str | bytes, device="cuda", stats: dict | None = None) -> DeviceCoo:
     """Coordinate Matrix Market (real, general|symmetric) -> CSR on ``device``;
-    same result and errors as ``matrices.loads_matrix_market``."""
+    same result and errors as ``matrices.loads_matrix_market``.  ``stats``
+    (optional dict) receives how many body lines were parsed and how many
+    values / lines the host had to convert or judge."""
     if isinstance(text, (bytes, bytearray)):
         text = bytes(text).decode()
     dev = torch.device(device)
@@ -141,6 +145,9 @@ def load_matrix_market_device(text: str | bytes, device="cuda") -> DeviceCoo:
     # converted in one batch by numpy's bytes -> float64 (correctly rounded,
     # bit-identical to float()), gathered from the host copy of the text
     fl_idx = torch.nonzero(status == FLOAT, as_tuple=True)[0]
+    if stats is not None:
+        stats.update(lines=nlines, host_floats=int(fl_idx.numel()),
+                     host_lines=int((status == HOST).sum().item()))
     if fl_idx.numel():
         off = tok_off[fl_idx].cpu().numpy()
         ln = tok_len[fl_idx].cpu().numpy().astype(np.int64)

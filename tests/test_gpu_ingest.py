@@ -61,7 +61,7 @@ def _mm(rng, rows, cols, n, sym, fmt, dup_heavy=False):
 
 
 FORMATS = [
-    lambda x, rng: repr(float(x)),                 # 17-digit repr: host batch conversion
+    lambda x, rng: repr(float(x)),                 # 17-digit repr: Eisel-Lemire on the device
     lambda x, rng: f"{x:.6e}",                     # fast path
     lambda x, rng: f"{x:.3f}",
     lambda x, rng: ["1_0.5", "inf", "-Infinity", "nan", "1e400", "4.9e-324", "+.5", "5.", "-0",
@@ -80,6 +80,46 @@ def test_duplicate_runs_sum_in_numpy_order():
     rng = np.random.default_rng(5)
     for n in (9, 17, 200, 1000):
         same(_mm(rng, 4, 4, n, False, FORMATS[0], dup_heavy=True))
+
+
+def _hard_decimals(rng, n):
+    """Decimal strings across the binary64 range that Clinger's fast path
+    cannot take: 17-digit round-trip reprs of random bit patterns, 16-19
+    digit mantissas with large exponents, exact halfway cases (2^53 + 1 and
+    its neighbours), subnormals and overflow (host), > 19 digits (host)."""
+    bits = rng.integers(0, 2**63 - 1, n, dtype=np.int64) & ~np.int64(0x7FF0000000000000) | \
+        (rng.integers(1, 2046, n, dtype=np.int64) << 52)
+    out = [repr(float(x)) for x in bits.view(np.float64)]
+    out += [f"{int(m)}e{int(e)}" for m, e in zip(rng.integers(10**15, 10**18, n),
+                                                  rng.integers(-340, 290, n))]
+    out += [f"{x:.16e}" for x in rng.standard_normal(n) * 10.0 ** rng.integers(-300, 300, n)]
+    out += ["9007199254740993", "9007199254740995", "9007199254740992.5", "18014398509481986",
+            "2.2250738585072014e-308", "1.7976931348623157e308", "4.9e-324", "2.5e-320", "1e309",
+            "8.98846567431158e307", "7.2057594037927933e16", "1e23", "0.1", "-1.5e-300",
+            "1.00000000000000011102230246251565404236316680908203125", "9999999999999999999",
+            "12345678901234567890e-10"]
+    return out
+
+
+def test_correctly_rounded_decimals_on_device():
+    """Every value bit-identical to float(); normal finite results of <= 19
+    significant digits are converted on the device (Eisel-Lemire), only
+    subnormal / overflowing / > 19-digit tokens reach the host."""
+    rng = np.random.default_rng(17)
+    vals = _hard_decimals(rng, 4000)
+    n = len(vals)
+    text = f"%%MatrixMarket matrix coordinate real general\n{n} 1 {n}\n" + \
+        "\n".join(f"{i + 1} 1 {v}" for i, v in enumerate(vals)) + "\n"
+    stats = {}
+    got = load_matrix_market_device(text, stats=stats)
+    want = np.array([float(v) for v in vals])
+    gv = got.vals.cpu().numpy()
+    assert np.array_equal(got.row_ptr.cpu().numpy(), np.arange(n + 1))
+    assert np.array_equal(gv.view(np.int64), want.view(np.int64))
+    host = sum(1 for v in vals if len(v.lstrip("-").split("e")[0].replace(".", "").lstrip("0")) > 19
+               or not (2.2250738585072014e-308 <= abs(float(v)) < float("inf")))
+    assert stats["lines"] == n
+    assert stats["host_floats"] + stats["host_lines"] <= host, (stats, host)
 
 
 def test_crlf_and_header_comments():
