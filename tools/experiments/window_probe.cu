@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(256) k_gather(const int *rp, const int *ci, co
 
 // (b) window-staged: CTA = (line, slice of S columns); smem [9 * SIDE][S]
 template <int S>
-__global__ void __launch_bounds__(SIDE * S / 4) k_window(const int *rp, const unsigned short *slot,
+__global__ void __launch_bounds__(640) k_window(const int *rp, const unsigned short *slot,
                                                          const float *av, const float *B, float *C) {
     extern __shared__ float4 sm[];
     constexpr int LPR = S / 4;  // lanes per row
@@ -76,17 +76,19 @@ __global__ void __launch_bounds__(SIDE * S / 4) k_window(const int *rp, const un
         sm[(w * SIDE + x) * LPR + part] = v;
     }
     __syncthreads();
-    const int x = threadIdx.x / LPR, part = threadIdx.x % LPR;
-    const int i = line * SIDE + x;
-    const int beg = __ldg(rp + i), end = __ldg(rp + i + 1);
-    float4 acc = make_float4(0, 0, 0, 0);
-    for (int p = beg; p < end; ++p) {
-        const float v = __ldg(av + p);
-        const float4 b = sm[(int)__ldg(slot + p) * LPR + part];
-        acc.x = fmaf(v, b.x, acc.x); acc.y = fmaf(v, b.y, acc.y);
-        acc.z = fmaf(v, b.z, acc.z); acc.w = fmaf(v, b.w, acc.w);
+    for (int t = threadIdx.x; t < SIDE * LPR; t += blockDim.x) {  // S = 32: two rows per thread
+        const int x = t / LPR, part = t % LPR;
+        const int i = line * SIDE + x;
+        const int beg = __ldg(rp + i), end = __ldg(rp + i + 1);
+        float4 acc = make_float4(0, 0, 0, 0);
+        for (int p = beg; p < end; ++p) {
+            const float v = __ldg(av + p);
+            const float4 b = sm[(int)__ldg(slot + p) * LPR + part];
+            acc.x = fmaf(v, b.x, acc.x); acc.y = fmaf(v, b.y, acc.y);
+            acc.z = fmaf(v, b.z, acc.z); acc.w = fmaf(v, b.w, acc.w);
+        }
+        reinterpret_cast<float4 *>(C + (size_t)i * N + col0)[part] = acc;
     }
-    reinterpret_cast<float4 *>(C + (size_t)i * N + col0)[part] = acc;
 }
 
 int main() {
@@ -163,7 +165,7 @@ int main() {
         const int smem = 9 * SIDE * S * 4;
         CK(cudaFuncSetAttribute(k_window<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         timeit("(b) window-staged S=16 (92 KB smem)", [&] {
-            k_window<S><<<SIDE * SIDE * (N / S), SIDE * S / 4, smem>>>(d_rp, d_slot, d_av, d_b, d_c2);
+            k_window<S><<<SIDE * SIDE * (N / S), (SIDE * S / 4 > 640 ? 640 : SIDE * S / 4), smem>>>(d_rp, d_slot, d_av, d_b, d_c2);
         });
         CK(cudaGetLastError());
         check("S=16");
@@ -173,7 +175,7 @@ int main() {
         const int smem = 9 * SIDE * S * 4;
         CK(cudaFuncSetAttribute(k_window<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         timeit("(b) window-staged S=8 (46 KB smem)", [&] {
-            k_window<S><<<SIDE * SIDE * (N / S), SIDE * S / 4, smem>>>(d_rp, d_slot, d_av, d_b, d_c2);
+            k_window<S><<<SIDE * SIDE * (N / S), (SIDE * S / 4 > 640 ? 640 : SIDE * S / 4), smem>>>(d_rp, d_slot, d_av, d_b, d_c2);
         });
         CK(cudaGetLastError());
         check("S=8");
@@ -182,8 +184,8 @@ int main() {
         constexpr int S = 32;
         const int smem = 9 * SIDE * S * 4;
         CK(cudaFuncSetAttribute(k_window<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        timeit("(b) window-staged S=32 (184 KB smem; fails to launch here)", [&] {
-            k_window<S><<<SIDE * SIDE * (N / S), SIDE * S / 4, smem>>>(d_rp, d_slot, d_av, d_b, d_c2);
+        timeit("(b) window-staged S=32 (184 KB smem, 640 threads)", [&] {
+            k_window<S><<<SIDE * SIDE * (N / S), (SIDE * S / 4 > 640 ? 640 : SIDE * S / 4), smem>>>(d_rp, d_slot, d_av, d_b, d_c2);
         });
         CK(cudaGetLastError());
         check("S=32");
