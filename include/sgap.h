@@ -234,7 +234,9 @@ int sgap_reference_spmm_f64(const sgap_csr_t *a, const void *d_b, int32_t n,
  *     tokens, 3 non-numeric, 4 coordinate out of range, 5 the host checks
  *     the line, 6 entry whose plain-decimal value the host converts) and, for
  *     status 1 and 6, zero-based row/col, the value token's byte offset and
- *     length; for status 1 the value (correctly rounded: Clinger's fast path).
+ *     length; for status 1 the value (correctly rounded: Clinger's fast path
+ *     or Eisel-Lemire).  rows, cols <= INT32_MAX (SGAP_ERR_SHAPE otherwise:
+ *     the sort keys pack row<<32|col).
  *   sgap_mm_expand: COO in the reference's append order at d_pos (exclusive
  *     scan of 1 per entry, 2 for symmetric off-diagonals), key = row<<32|col.
  *   sgap_mm_sum_runs: per run of equal keys in the stably sorted COO, the

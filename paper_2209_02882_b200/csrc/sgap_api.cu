@@ -691,6 +691,7 @@ int sgap_mm_parse(const uint8_t *d_text, int64_t len, const int64_t *d_starts, i
                   int64_t rows, int64_t cols, uint8_t *d_status, int64_t *d_r, int64_t *d_c,
                   double *d_v, int64_t *d_tok_off, int32_t *d_tok_len, void *stream) {
     if (len < 0 || nlines < 0 || rows < 0 || cols < 0) return SGAP_ERR_ARG;
+    if (rows > INT_MAX || cols > INT_MAX) return SGAP_ERR_SHAPE;  // (row << 32 | col) sort keys
     if (nlines == 0) return SGAP_OK;
     if (!d_text || !d_starts || !d_status || !d_r || !d_c || !d_v || !d_tok_off || !d_tok_len)
         return SGAP_ERR_ARG;

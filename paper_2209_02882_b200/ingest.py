@@ -120,6 +120,8 @@ def load_matrix_market_device(text: str | bytes, device="cuda", stats: dict | No
     first_line = start  # 0-based index of the body's first line in text.splitlines()
     if len(body) >= 2**31:
         return _host_csr(text, dev)  # the line index uses 32-bit selection
+    if rows >= 2**31 or cols >= 2**31:
+        return _host_csr(text, dev)  # COO sort keys pack (row << 32 | col)
     st = torch.cuda.current_stream(dev).cuda_stream
     d_text = torch.frombuffer(bytearray(body), dtype=torch.uint8).to(dev) if body else \
         torch.empty(0, dtype=torch.uint8, device=dev)

@@ -122,6 +122,12 @@ def test_correctly_rounded_decimals_on_device():
     assert stats["host_floats"] + stats["host_lines"] <= host, (stats, host)
 
 
+def test_shapes_beyond_32_bit_keys_stay_exact():
+    # (row << 32 | col) keys need 31-bit shapes; larger ones take the host parser
+    same("%%MatrixMarket matrix coordinate real general\n5 4294967300 3\n"
+         "1 4294967299 1.5\n1 2 2.5\n5 4294967300 -1\n")
+
+
 def test_crlf_and_header_comments():
     text = "%%MatrixMarket matrix coordinate real general\r\n%c\r\n\r\n2 2 2\r\n1 1 0.5\r\n2 2 -3\r\n"
     same(text)
