@@ -703,7 +703,8 @@ __device__ __forceinline__ void eb_walk4(const ASrc &A, long long q0, long long 
     // (Four per trip: more spills, 0.709 vs 0.702 ms on config 2; loading the
     // next batch's A under this batch's gathers: spills, 0.846 ms; storing a
     // row's float32 partial directly when no fold happened since it began,
-    // skipping the float64 round trip: 0.710 vs 0.704 ms.)
+    // skipping the float64 round trip: 0.710 vs 0.704 ms; B gathers with
+    // ld.global.nc.L1::no_allocate: 0.874 ms -- hub-row L1 hits matter.)
     for (; q + 8 <= qe; q += 8) {
         if ((q & 31) == 0 && q + 64 < qe) A.prefetch(q + 64);  // A lines two ahead
         batch4(q);
