@@ -68,6 +68,15 @@ def test_argument_validation_without_device():
     assert L.sgap_block_starts(None, 4, 0, 1, None, None) == _native.ERR_ARG
     assert L.sgap_seg_reduce_group(None, None, None, 5, 4, None, 0, 0, None, None, None) == _native.ERR_ARG
     assert L.sgap_atomic_add_group(None, None, None, 8, 3, None, 0, 0, None, None, None) == _native.ERR_ARG
+    # Matrix Market ingest entry points
+    assert L.sgap_mm_line_flags(None, -1, None, None, None) == _native.ERR_ARG
+    assert L.sgap_mm_line_flags(None, 0, None, None, None) == _native.OK
+    assert L.sgap_mm_parse(None, 10, None, 1, 2**31, 4, None, None, None, None, None, None,
+                           None) == _native.ERR_SHAPE
+    assert L.sgap_mm_parse(None, 10, None, 1, 4, 4, None, None, None, None, None, None,
+                           None) == _native.ERR_ARG
+    assert L.sgap_mm_expand(-1, None, None, None, None, None, 0, None, None, None) == _native.ERR_ARG
+    assert L.sgap_mm_sum_runs(0, None, None, None, 0, None, None, None, None) == _native.OK
 
 
 def test_missing_library_fails_loudly(monkeypatch, tmp_path):
