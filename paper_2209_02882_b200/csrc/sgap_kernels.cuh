@@ -28,7 +28,8 @@ constexpr int kFoldEvery = 8;  // float32 partial sums fold into float64 every 8
 #ifndef SGAP_EB_MINB
 #define SGAP_EB_MINB 4  // CTAs per SM the register EB walk is compiled for
 // (5 / 6: 48 / 40 registers with 450-900 B of spills; config 2 1.03 / 1.36 ms,
-// config 3 3.30 / 4.22 ms, against 0.711 / 2.13 ms at 4 and 64 registers)
+// config 3 3.30 / 4.22 ms, against 0.711 / 2.13 ms at 4 and 64 registers;
+// 3: 0.827 / 2.53 ms -- fewer warps lose more than the extra registers give)
 #endif
 
 // ===========================================================================
