@@ -709,7 +709,9 @@ __device__ __forceinline__ void eb_walk4(const ASrc &A, long long q0, long long 
     // skipping the float64 round trip: 0.710 vs 0.704 ms; B gathers with
     // ld.global.nc.L1::no_allocate: 0.874 ms -- hub-row L1 hits matter; an
     // L2 evict_last policy on them (createpolicy, fraction 0.25/0.5/1.0):
-    // 0.723/0.715/0.715 ms; the max-L1 carveout: unchanged, already chosen.)
+    // 0.723/0.715/0.715 ms; the max-L1 carveout: unchanged, already chosen;
+    // L1::evict_last on the B gathers: 0.709 ms, L1::evict_first on the
+    // col/row-id loads: 0.799 ms.)
     for (; q + 8 <= qe; q += 8) {
         if ((q & 31) == 0 && q + 64 < qe) A.prefetch(q + 64);  // A lines two ahead
         batch4(q);
