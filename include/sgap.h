@@ -92,8 +92,9 @@ typedef struct {
     int64_t grid_size;      /* == LoweredKernel.grid_size                    */
     int64_t block_size;     /* == LoweredKernel.block_size                   */
     int32_t has_block_starts; /* == (LoweredKernel.block_starts is not None) */
-    int32_t hw_block;       /* CTA size override: 0 = auto (256), else a warp
-                               multiple in [32, 256]                        */
+    int32_t hw_block;       /* CTA size override: 0 = auto (256; 128 for the
+                               register EB walk), else a warp multiple in
+                               [32, 256]                                    */
     int32_t hw_variant;     /* nnz-multiple walk: 0 auto, 1 register-staged,
                                2 TMA-staged (cp.async.bulk + mbarrier ring),
                                3/4 lane-staged (warp per chunk, 4/8 B-row

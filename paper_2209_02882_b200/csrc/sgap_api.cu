@@ -20,6 +20,11 @@ extern "C" int64_t sgap_long_row_capacity(int64_t nnz, int64_t threshold, int64_
 namespace {
 
 constexpr int kHwBlock = 256;
+// CTA size of the register EB walk (hw variant 1): same 32 warps/SM at 64
+// registers, finer blocks balance the long-chunk tail better -- config 2
+// 0.693 ms at 128 vs 0.701 at 256 (96: 0.732, 160-192: 0.745); config 3
+// 2.037 vs 2.108 ms (64: 2.015).
+constexpr int kEbWalkBlock = 128;
 
 inline long long ceil_div(long long a, long long b) { return (a + b - 1) / b; }
 
@@ -210,7 +215,7 @@ int launch_nnz_multiple(bool tma, int tile, int owner, const sgap_kernel_t &k,
                         (int)a.num_rows, k.n, a.nnz, k.g, total_pos, tile, owner, lr, wb);
     }
     const long long items = ceil_div(total_pos / k.g, 32 / W);
-    const int blk = k.hw_block > 0 ? k.hw_block : kHwBlock;
+    const int blk = k.hw_block > 0 ? k.hw_block : kEbWalkBlock;
     const int vec4 = (k.g % 4 == 0) && aligned(rowid, 16) && aligned(a.d_col_idx, 16) &&
                      aligned(a.d_vals, 16);
     return launch_k(k_nnz_multiple<T, V, W, U>, dim3(grid_for(items, blk)), dim3(blk), 0, st,
