@@ -1,26 +1,28 @@
 #!/usr/bin/env python
 """Benchmark: CSR SpMM GFLOP/s (2*nnz*N/t) and HBM GB/s vs roofline on B200.
 
-    python bench.py [--gpus N --steps K --warmup W] [--config 2] [--point P --p 256]
+    python bench.py [--gpus N --steps K --warmup W] [--config 5] [--point P --p 256]
     python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \
         --master-port P bench.py --gpus N ...
-    python bench.py --impl reference ...   # the reference's CPU path (oracle port)
+    python bench.py --impl reference ...   # the reference's own CPU path
 
-Workload (BASELINE.json configs):
-  --config 2 (default): R-MAT scale 20+log2(N), edge factor 16, Graph500
-    (0.57,0.19,0.19,0.05), seeded vertex permutation, duplicates summed,
-    N=128 dense columns, fp32.  At N=1 GPU this is exactly config 2 (1M rows,
-    16.09M nnz); at N GPUs the matrix grows N-fold and is cut into N
-    nnz-balanced row shards (B replicated, C row-disjoint, no collective):
-    per-GPU work stays ~config 2, i.e. weak scaling.
-  --config 1/3/4/5 select the other BASELINE shapes (5 = R-MAT scale 24 at
-    any N: strong scaling of one matrix).
+Workload (BASELINE.json configs): the headline is config 5 --
+R-MAT scale 24, edge factor 16, Graph500 (0.57,0.19,0.19,0.05), seeded
+vertex permutation, duplicates summed, N = 128 dense columns, fp32 -- the
+configuration BASELINE's metric is quoted on at 1/2/4/8 B200.  At N GPUs the
+same matrix is cut into N nnz-balanced row shards (B replicated, C
+row-disjoint, no data-path collective): strong scaling.  ``--config 1..4``
+select the other BASELINE shapes (config 2: R-MAT scale 20; ``--weak``
+grows it with the world size instead).  ``--gpus N`` without torchrun
+re-launches itself under torch.distributed.run with N ranks.
 
-One step = one full SpMM over the resident operands: C zero-fill (atomic
-families) + the sm_100a kernel.  A+B+C exceed the 126 MB L2, so no flush is
-needed between steps.  ``value`` is total GFLOP/s over all ranks with the
-max-over-ranks device time; ``e2e`` repeats the step through the host-buffer
-path (pinned H2D of A and B, kernel, D2H of C) inside the timed region.
+One step = one full SpMM over the resident operands: the zero-fill the
+schedule needs + the sm_100a kernel(s) + the long-row fold.  A+B+C exceed the
+126 MB L2 (config 5: 19 GB), so no flush is needed between steps.  ``value``
+is total GFLOP/s over all ranks with the max-over-ranks device time; ``e2e``
+repeats the step through host buffers (pinned H2D of A and B, kernel, D2H of
+C inside the timed region) via ``pipeline.HostSpmm``, plus one cold start
+(upload, device planning, SpMM, download).
 """
 
 from __future__ import annotations
@@ -30,6 +32,7 @@ import json
 import math
 import os
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -44,20 +47,21 @@ sys.path.insert(0, str(ROOT))
 METRIC = "SpMM GFLOP/s (2*nnz*N/t)"
 UNIT = "GFLOP/s"
 FALLBACK_HBM_GBS = 6650.0
-# B-row gather ceiling of config 2 (8.2 GB of 512-B rows in 0.416 ms; the
-# same probe reads 19-20 TB/s from any L2-resident table): measured, not nominal
-GATHER_CEILING_TBS = 19.8
+SMS = 148
+FP32_LANES_PER_SM = 128
 
 
 # --------------------------------------------------------------------------- setup
 
-def parse_args():
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--weak", action="store_true",
+                    help="config 2 only: R-MAT scale 20+log2(world) (weak scaling)")
     ap.add_argument("--n", type=int, default=0, help="dense width override")
     ap.add_argument("--point", default="", help="schedule point (default: selector)")
     ap.add_argument("--p", type=int, default=256)
@@ -68,7 +72,18 @@ def parse_args():
     ap.add_argument("--e2e-blocks", type=int, default=8)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--seed", type=int, default=1)
-    return ap.parse_args()
+    return ap.parse_args(argv)
+
+
+def maybe_self_launch(args) -> None:
+    """``--gpus N`` outside torchrun: re-run this script as N ranks."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    port = 29500 + (os.getpid() % 2000)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
 
 
 def dist_setup():
@@ -97,16 +112,18 @@ def default_n(cfg: int) -> int:
     return {1: 32, 2: 128, 3: 64, 4: 128, 5: 128}[cfg]
 
 
-def build_workload(cfg: int, world: int, seed: int, device):
+def build_workload(cfg: int, world: int, seed: int, device, weak: bool = False):
     from paper_2209_02882_b200 import generators as G
-    if cfg == 2:
+    if cfg == 2 and weak:
         scale = 20 + int(round(math.log2(world)))
         g = G.rmat(scale, 16, seed=seed, device=device)
-        desc = f"config 2: R-MAT scale {scale}, edge factor 16, permuted" + \
+        desc = f"config 2 weak: R-MAT scale {scale}, edge factor 16, permuted" + \
             (f" ({world}x config 2, {world} nnz-balanced row shards)" if world > 1 else "")
         return g, desc, "weak"
     g = G.config_matrix(cfg, device=device, seed=seed)
-    return g, f"config {cfg}: {g.label}", "strong"
+    desc = f"config {cfg}: {g.label}" + \
+        (f" ({world} nnz-balanced row shards, B replicated)" if world > 1 else "")
+    return g, desc, "strong"
 
 
 def dense_b(num_rows: int, n: int, seed: int, device) -> torch.Tensor:
@@ -172,14 +189,24 @@ def host_threads() -> int:
         return os.cpu_count() or 1
 
 
-def measured_peak_hbm() -> tuple[float, str]:
+def measured_peaks() -> dict:
+    """HBM GB/s from MEASURED_PEAKS.json (driver-written); the FP32 FMA peak
+    is not measured there, so it is the nominal 148 SMs x 128 lanes x 2 FLOP
+    at the recorded max SM clock."""
+    out = {"hbm_gbs": FALLBACK_HBM_GBS, "hbm_source": "fallback (B200_PROFILING.md)",
+           "sm_mhz": 1965.0}
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         try:
-            return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+            rec = json.loads(p.read_text())
+            out["hbm_gbs"] = float(rec["hbm_gbs"])
+            out["hbm_source"] = "MEASURED_PEAKS.json hbm_gbs (copy, burst)"
+            out["sm_mhz"] = float(rec.get("sm_max_mhz", 1965.0))
         except Exception:
             pass
-    return FALLBACK_HBM_GBS, "fallback"
+    out["fp32_tflops"] = SMS * FP32_LANES_PER_SM * 2 * out["sm_mhz"] * 1e6 / 1e12
+    out["fp32_source"] = f"nominal: {SMS} SMs x {FP32_LANES_PER_SM} FMA lanes x 2 at {out['sm_mhz']:.0f} MHz"
+    return out
 
 
 def algorithmic_bytes(m: int, nnz: int, n: int, touched: int, esz: int = 4) -> int:
@@ -188,61 +215,181 @@ def algorithmic_bytes(m: int, nnz: int, n: int, touched: int, esz: int = 4) -> i
     return 4 * (m + 1) + 8 * nnz + esz * n * touched + esz * m * n
 
 
-def ncu_traffic(workload: str, point: str):
-    """dram read+write bytes per launch of the timed kernel from the committed
-    ncu --set full capture, when one exists for this exact workload."""
+def roofline(m: int, nnz: int, n: int, touched: int, kernel_ms: float, peaks: dict) -> dict:
+    """SURVEY 8(d): t_roof = max(bytes / BW_HBM, 2 nnz N / P_FP32);
+    frac = t_roof / t_measured.  ``achieved``/``peak`` are stated in the unit
+    of the bound that binds."""
+    abytes = algorithmic_bytes(m, nnz, n, touched)
+    flops = 2.0 * nnz * n
+    t_hbm = abytes / (peaks["hbm_gbs"] * 1e9)
+    t_fma = flops / (peaks["fp32_tflops"] * 1e12)
+    t = kernel_ms * 1e-3
+    if t_hbm >= t_fma:
+        r = {"bound": "hbm", "achieved": abytes / t / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s"}
+    else:
+        r = {"bound": "fp32_fma", "achieved": flops / t / 1e12, "peak": peaks["fp32_tflops"],
+             "unit": "TFLOP/s"}
+    r["frac"] = max(t_hbm, t_fma) / t
+    r.update({"algorithmic_bytes": abytes, "t_hbm_ms": t_hbm * 1e3, "t_fp32_ms": t_fma * 1e3,
+              "hbm_frac": t_hbm / t, "fp32_frac": t_fma / t, "kernel_ms": kernel_ms,
+              "peak_source": {"hbm": peaks["hbm_source"], "fp32": peaks["fp32_source"]}})
+    return r
+
+
+def ncu_traffic(workload: str, point: str, hw_variant: int):
+    """dram read+write bytes per launch of the dominant kernel from the
+    committed ncu --set full capture of this build (profiles/ncu_traffic.json,
+    written by tools/ncu_traffic.py), when one exists for this workload."""
     p = ROOT / "profiles" / "ncu_traffic.json"
     if not p.exists():
         return None
     try:
         rec = json.loads(p.read_text())
         for r in rec.get("entries", []):
-            if r.get("workload") == workload and r.get("point") == point:
-                return r.get("dram_bytes")
+            if (r.get("workload") == workload and r.get("point") == point
+                    and int(r.get("hw_variant", 0)) == hw_variant):
+                return {"bytes": r.get("dram_bytes"), "kernel": r.get("kernel"),
+                        "captured": r.get("captured"), "source": "profiles/ncu_traffic.json"}
     except Exception:
         return None
     return None
 
 
+# --------------------------------------------------------------------------- CPU baselines
+
+def _ref_import():
+    """The reference package installed from /root/reference into baseline/_ref
+    (pip --target; travels to the GPU box).  None when absent."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "spmmlab").exists():
+        return None
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    try:
+        from spmmlab import matrices as M  # noqa: F401
+        return M
+    except Exception:
+        return None
+
+
+_W = {}
+
+
+def _ref_worker_init(rp, ci, vals, bsub, n):
+    """One row slice of the sample as the reference's own CsrMatrix /
+    DenseMatrix (columns remapped onto the slice's touched B rows, which
+    changes no product or summation order)."""
+    M = _ref_import()
+    uniq, inv = np.unique(ci, return_inverse=True)
+    _W["a"] = M.CsrMatrix(len(rp) - 1, len(uniq), rp.astype(np.int64), inv.astype(np.int64),
+                          vals.astype(np.float64))
+    _W["b"] = M.DenseMatrix(len(uniq), n, np.ascontiguousarray(bsub[uniq], dtype=np.float64).reshape(-1))
+    _W["oracle"] = M.dense_spmm_oracle
+
+
+def _ref_worker_run(_):
+    c = _W["oracle"](_W["a"], _W["b"])
+    return float(c.vals[:8].sum())
+
+
+def reference_cpu(rp, ci, vals, b_host, n, *, workers: int, nnz_per_worker: int, steps: int,
+                  warmup: int):
+    """The reference's CPU path (spmmlab.matrices.dense_spmm_oracle, pure
+    Python over nonzeros, numpy over the N columns) on ``workers`` processes,
+    each on its own contiguous row slice of the leading rows of the workload.
+    Returns (GFLOP/s, seconds per step, sample description)."""
+    import multiprocessing as mp
+    total = min(int(rp[-1]), nnz_per_worker * workers)
+    r_end = max(1, min(int(np.searchsorted(rp, total, side="left")), len(rp) - 1))
+    s_nnz = int(rp[r_end])
+    cuts = np.searchsorted(rp[: r_end + 1], np.linspace(0, s_nnz, workers + 1), side="left")
+    cuts[0], cuts[-1] = 0, r_end
+    slices = []
+    for w in range(workers):
+        lo, hi = int(cuts[w]), int(cuts[w + 1])
+        if hi <= lo:
+            continue
+        p0, p1 = int(rp[lo]), int(rp[hi])
+        slices.append((rp[lo:hi + 1] - p0, ci[p0:p1], vals[p0:p1]))
+    ctx = mp.get_context("fork")
+    pools = [ctx.Pool(1, initializer=_ref_worker_init, initargs=(s[0], s[1], s[2], b_host, n))
+             for s in slices]
+    try:
+        def one_step():
+            rs = [p.apply_async(_ref_worker_run, (0,)) for p in pools]
+            for r in rs:
+                r.get()
+        for _ in range(warmup):
+            one_step()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            one_step()
+        dt = (time.perf_counter() - t0) / steps
+    finally:
+        for p in pools:
+            p.terminate()
+    value = 2.0 * s_nnz * n / dt / 1e9
+    sample = (f"spmmlab.matrices.dense_spmm_oracle (the reference, pure Python, baseline/_ref) on "
+              f"rows [0, {r_end}) = {s_nnz} nnz x N={n} per step, {len(slices)} processes x 1 "
+              "core, each on a contiguous row slice")
+    return value, dt, sample, len(slices)
+
+
+def port_cpu(rp, ci, vals, b_host, n, *, threads: int, sample_nnz: int, reps: int):
+    """The oracle's C restatement of dense_spmm_oracle (bit-identical f64,
+    OpenMP) on ``threads`` cores over the leading rows holding ~sample_nnz."""
+    import oracle
+    r_end = max(1, min(int(np.searchsorted(rp, min(int(rp[-1]), sample_nnz), side="left")),
+                       len(rp) - 1))
+    srp = rp[: r_end + 1].astype(np.int32)
+    s_nnz = int(srp[-1])
+    oracle.spmm_f64(srp, ci[:s_nnz], vals[:s_nnz], b_host, n, threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        oracle.spmm_f64(srp, ci[:s_nnz], vals[:s_nnz], b_host, n, threads=threads)
+    dt = (time.perf_counter() - t0) / reps
+    return (2.0 * s_nnz * n / dt / 1e9,
+            f"oracle/ (C fp64 port of dense_spmm_oracle, OpenMP) on rows [0, {r_end}): "
+            f"{s_nnz} nnz x N={n}, {reps} reps")
+
+
 # --------------------------------------------------------------------------- reference arm
 
 def run_reference(args, rank, world):
-    """The reference's CPU path on this host's cores: the oracle port of
-    dense_spmm_oracle (oracle/, C, bit-identical f64), on a bounded sample."""
+    """``--impl reference``: the reference's own CPU implementation of the
+    path (spmmlab's dense_spmm_oracle from baseline/_ref) on this host's
+    cores, on a bounded sample of the same workload; rank 0 only.  Falls back
+    to the oracle's C port (kind "port") when baseline/_ref is absent."""
     if rank != 0:
         return
-    import oracle
     cfg = args.config
     n = args.n or default_n(cfg)
     dev = "cuda" if torch.cuda.is_available() else "cpu"
-    g, desc, scaling = build_workload(cfg, world, args.seed, dev)
-    rp = g.row_ptr.cpu().numpy()
+    g, desc, scaling = build_workload(cfg, 1, args.seed, dev, weak=args.weak)
+    rp = g.row_ptr.cpu().numpy().astype(np.int64)
     ci = g.col_idx.cpu().numpy().astype(np.int32)
     vals = g.vals.cpu().numpy().astype(np.float32)
-    b = dense_b(g.num_cols, n, args.seed, dev).cpu().numpy()
-    threads = host_threads()
-    # bounded sample: leading rows holding ~sample_nnz nonzeros per step
-    sample_nnz = min(g.nnz, 4_000_000)
-    r_end = int(np.searchsorted(rp, sample_nnz, side="left"))
-    r_end = max(1, min(r_end, g.num_rows))
-    srp = rp[: r_end + 1].astype(np.int32)
-    s_nnz = int(srp[-1])
-    for _ in range(args.warmup):
-        oracle.spmm_f64(srp, ci[:s_nnz], vals[:s_nnz], b, n, threads=threads)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        oracle.spmm_f64(srp, ci[:s_nnz], vals[:s_nnz], b, n, threads=threads)
-    dt = (time.perf_counter() - t0) / args.steps
-    value = 2.0 * s_nnz * n / dt / 1e9
-    sample = f"rows [0, {r_end}) of the workload: {s_nnz} nnz x N={n} per step"
+    b_host = dense_b(g.num_cols, n, args.seed, dev).cpu().numpy()
+    cores = host_threads()
+    if _ref_import() is not None:
+        workers = max(1, min(cores, 32))
+        value, dt, sample, used = reference_cpu(rp, ci, vals, b_host, n, workers=workers,
+                                                nnz_per_worker=150_000, steps=args.steps,
+                                                warmup=min(args.warmup, 1))
+        kind = "reference"
+    else:
+        value, sample = port_cpu(rp, ci, vals, b_host, n, threads=cores, sample_nnz=4_000_000,
+                                 reps=args.steps)
+        dt = 2.0 * 4_000_000 * n / value / 1e9
+        used, kind = cores, "port"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
         "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": desc, "rows": g.num_rows, "nnz": g.nnz, "n": n},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": kind,
+                         "sample": sample, "host_cores": cores},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -252,9 +399,13 @@ def run_reference(args, rank, world):
 
 def main():
     args = parse_args()
+    maybe_self_launch(args)
     rank, world, local = dist_setup()
     if args.impl == "reference":
         run_reference(args, rank, world)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
         return
     from paper_2209_02882_b200.device import DeviceCsr, launches_per_call, prepare_aux, spmm
     from paper_2209_02882_b200.partition import plan_shards, shard_csr
@@ -265,19 +416,19 @@ def main():
     dev = torch.device("cuda", torch.cuda.current_device())
     cfg = args.config
     n = args.n or default_n(cfg)
-    g, desc, scaling = build_workload(cfg, world, args.seed, dev)
+    g, desc, scaling = build_workload(cfg, world, args.seed, dev, weak=args.weak)
     total_nnz = g.nnz
     plan = plan_shards(g.row_ptr.cpu().numpy(), world)
     rp, ci, vals = shard_csr(g.row_ptr, g.col_idx, g.vals, plan, rank)
     lo, hi = plan.rows(rank)
     a = DeviceCsr(hi - lo, g.num_cols, rp.to(torch.int32).contiguous(),
                   ci.to(torch.int32).contiguous(), vals.to(torch.float32).contiguous())
+    del rp, ci, vals, g
+    torch.cuda.empty_cache()
     touched = int(torch.unique(a.col_idx).numel()) if a.nnz else 0
     rp_host = a.row_ptr.cpu().numpy().astype(np.int64)
-    b = dense_b(g.num_cols, n, args.seed, dev)
+    b = dense_b(a.num_cols, n, args.seed, dev)
     c = torch.empty((a.num_rows, n), dtype=torch.float32, device=dev)
-    del g
-    torch.cuda.empty_cache()
     stream = torch.cuda.current_stream()
     stats = matrix_stats(rp_host, a.num_cols)
 
@@ -290,7 +441,7 @@ def main():
         if rank == 0:
             ranked = autotune(a, b, c, n, candidates(n), reps=2, row_ptr_host=rp_host,
                               stream=stream, max_ms=50.0)
-            sweep_rows = [{"point": cd.point, "p": cd.p, "ms": ms,
+            sweep_rows = [{"point": cd.point, "p": cd.p, "hw_variant": cd.hw_variant, "ms": ms,
                            "gflops": 2.0 * a.nnz * n / (ms * 1e6)} for cd, ms in ranked]
             choice = ranked[0][0]
         if world > 1:
@@ -299,151 +450,77 @@ def main():
             choice = obj[0]
     heur = heuristic(stats, n)
     k = plan_for(choice, n, a.num_rows, a.num_cols, rp_host)
-    eb = k.family in ("nnz-one", "nnz-multiple")
     aux = prepare_aux(k, a, stream=stream)
 
-    def step(ev=None):
-        if ev is not None:
-            ev.record(stream)
+    def step():
         spmm(k, a, b, c, aux=aux, hw_block=choice.hw_block, hw_variant=choice.hw_variant,
              stream=stream)
 
-    for _ in range(args.warmup):
+    for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    t_start = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
-        t_start.record(stream)
         for i in range(args.steps):
-            step(mids[i])
+            starts[i].record(stream)
+            step()
             ends[i].record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    total_ms = t_start.elapsed_time(ends[-1])
-    kernel_ms = statistics.mean(mids[i].elapsed_time(ends[i]) for i in range(args.steps))
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    total_ms = starts[0].elapsed_time(ends[-1])
+    per_step = [starts[i].elapsed_time(ends[i]) for i in range(args.steps)]
+    kernel_ms = statistics.mean(per_step)
+    rank_ms = [total_ms]
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
+        rank_ms = [None] * world
+        dist.all_gather_object(rank_ms, total_ms)
+    total_ms = max(rank_ms)  # max over ranks
     ms_per_step = total_ms / args.steps
     value = 2.0 * total_nnz * n / (ms_per_step * 1e6)
 
-    # ---- roofline of the dominant kernel (this rank's shard)
-    peak, peak_kind = measured_peak_hbm()
-    abytes = algorithmic_bytes(a.num_rows, a.nnz, n, touched)
-    achieved = abytes / (kernel_ms * 1e-3) / 1e9
-    workload_key = f"cfg{cfg}:world{world}:n{n}"
-    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": ncu_traffic(workload_key, choice.point),
-            "peak_source": peak_kind, "algorithmic_bytes": abytes, "kernel_ms": kernel_ms,
-            "kernel_ms_covers": "the whole SpMM call (zero-fill pre-pass + main kernel + "
-                                "long-row fold), CUDA events on the launch stream",
-            "kernel_share": kernel_ms / ms_per_step}
-    # what actually binds on power-law matrices: every nonzero gathers a whole
-    # B row through L2 (profiles/r01_gather_ceiling.md)
-    gbytes = a.nnz * n * 4
-    roof["b_gather"] = {
-        "bytes": gbytes, "achieved_tbs": gbytes / (kernel_ms * 1e-3) / 1e12,
-        "ceiling_tbs": GATHER_CEILING_TBS if (cfg == 2 and world == 1) else None,
-        "ceiling_source": "gather-only kernel over config 2's col_idx in CSR order, same B "
-                          "layout (tools/experiments/l2_gather_probe.cu), best of 5 on B200",
-    }
-    if roof["b_gather"]["ceiling_tbs"]:
-        roof["b_gather"]["frac"] = roof["b_gather"]["achieved_tbs"] / GATHER_CEILING_TBS
+    # ---- roofline of the SpMM call (this rank's shard)
+    peaks = measured_peaks()
+    roof = roofline(a.num_rows, a.nnz, n, touched, kernel_ms, peaks)
+    roof["kernel_ms_covers"] = ("the whole SpMM call (zero-fill + main kernel + long-row fold), "
+                                "CUDA events on the launch stream, mean over the timed steps")
+    roof["kernel_ms_median"] = statistics.median(per_step)
+    roof["kernel_share"] = kernel_ms / ms_per_step
+    workload_key = f"cfg{cfg}:world{world}:n{n}" + (":weak" if args.weak else "")
+    roof["traffic"] = None
+    tr = ncu_traffic(workload_key, choice.point, choice.hw_variant)
+    if tr is not None:
+        roof["traffic"] = tr["bytes"]
+        roof["traffic_info"] = tr
+        if tr["bytes"]:
+            roof["traffic_over_algorithmic"] = tr["bytes"] / roof["algorithmic_bytes"]
+    roof["b_gather_bytes"] = a.nnz * n * 4  # every nonzero gathers a whole B row through L2
+    roof["b_gather_tbs"] = roof["b_gather_bytes"] / (kernel_ms * 1e-3) / 1e12
 
-    # ---- end to end through host buffers (pipelined: B up, then per row
-    # block A up / SpMM / C down on three streams)
+    # ---- end to end through host buffers
     e2e = None
     if not args.no_e2e:
-        from paper_2209_02882_b200.pipeline import HostSpmm
-        h_rp = a.row_ptr.cpu().pin_memory()
-        h_ci = a.col_idx.cpu().pin_memory()
-        h_v = a.vals.cpu().pin_memory()
-        h_b = b.cpu().pin_memory()
-        h_c = torch.empty(c.shape, dtype=c.dtype).pin_memory()
+        e2e = measure_e2e(args, a, b, c, k, choice, plan_for, n, total_nnz, world, dev, stream)
 
-        def plan_block(rows, sub_rp):
-            return plan_for(choice, n, rows, a.num_cols, sub_rp)
-
-        pipe = HostSpmm(a.num_rows, a.num_cols, n, h_rp, plan_block, blocks=args.e2e_blocks,
-                        hw_variant=choice.hw_variant)
-        pipe(h_rp, h_ci, h_v, h_b, h_c)
-        pipe.wait()
-        torch.cuda.synchronize()
-        e_steps = max(3, min(args.steps, 10))
-        if world > 1:
-            dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(e_steps):
-            pipe(h_rp, h_ci, h_v, h_b, h_c)
-        pipe.wait(stream)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        te = torch.tensor([e0.elapsed_time(e1) / e_steps], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        # the PCIe floor of one step: the same bytes up and down at once, no compute
-        s_up, s_dn = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-        d_rp, d_ci, d_v = (torch.empty_like(x, device=dev) for x in (h_rp, h_ci, h_v))
-        d_b, d_c = torch.empty_like(h_b, device=dev), torch.empty_like(h_c, device=dev)
-
-        def copies():
-            s_up.wait_stream(stream)
-            s_dn.wait_stream(stream)
-            with torch.cuda.stream(s_up):
-                for dst, src in ((d_rp, h_rp), (d_ci, h_ci), (d_v, h_v), (d_b, h_b)):
-                    dst.copy_(src, non_blocking=True)
-            with torch.cuda.stream(s_dn):
-                h_c.copy_(d_c, non_blocking=True)
-            stream.wait_stream(s_up)
-            stream.wait_stream(s_dn)
-
-        floor = float("inf")
-        for _ in range(3):
-            e0.record(stream)
-            copies()
-            e1.record(stream)
-            e1.synchronize()
-            floor = min(floor, e0.elapsed_time(e1))
-        del d_rp, d_ci, d_v, d_b, d_c
-        e2e = {"value": 2.0 * total_nnz * n / (float(te.item()) * 1e6), "unit": UNIT,
-               "h2d_bytes_per_step": pipe.h2d_bytes(), "d2h_bytes_per_step": pipe.d2h_bytes(),
-               "ms_per_step": float(te.item()), "steps": e_steps,
-               "pcie_floor_ms": floor, "frac_of_pcie_floor": floor / float(te.item()),
-               "path": f"pinned host A,B -> {args.e2e_blocks} row blocks: H2D / plan + SpMM / "
-                       "D2H C overlapped on 3 streams, device buffers double-buffered across "
-                       "steps (paper_2209_02882_b200.pipeline.HostSpmm)"}
-        del pipe
-
-    # ---- CPU baseline (rank 0, single GPU only)
+    # ---- CPU baselines (rank 0, single GPU only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        import oracle
         threads = host_threads()
-        h_rp32 = rp_host.astype(np.int32)
         h_ci32 = a.col_idx.cpu().numpy()
         h_v32 = a.vals.cpu().numpy()
         h_b32 = b.cpu().numpy()
-        sample_nnz = min(a.nnz, 4_000_000)
-        r_end = max(1, min(int(np.searchsorted(h_rp32, sample_nnz, side="left")), a.num_rows))
-        srp = h_rp32[: r_end + 1]
-        s_nnz = int(srp[-1])
-        oracle.spmm_f64(srp, h_ci32[:s_nnz], h_v32[:s_nnz], h_b32, n, threads=threads)
-        reps = 3
-        t0 = time.perf_counter()
-        for _ in range(reps):
-            oracle.spmm_f64(srp, h_ci32[:s_nnz], h_v32[:s_nnz], h_b32, n, threads=threads)
-        dt = (time.perf_counter() - t0) / reps
-        cpu = {"value": 2.0 * s_nnz * n / dt / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"oracle (C fp64 port of dense_spmm_oracle) on rows [0, {r_end}): "
-                         f"{s_nnz} nnz x N={n}, {reps} reps"}
+        pv, psample = port_cpu(rp_host, h_ci32, h_v32, h_b32, n, threads=threads,
+                               sample_nnz=4_000_000, reps=3)
+        cpu = {"value": pv, "unit": UNIT, "cores": threads, "kind": "port", "sample": psample}
+        if _ref_import() is not None:
+            rv, _, rsample, _ = reference_cpu(rp_host, h_ci32, h_v32, h_b32, n, workers=1,
+                                              nnz_per_worker=150_000, steps=2, warmup=0)
+            cpu["reference_1core"] = {"value": rv, "unit": UNIT, "cores": 1, "kind": "reference",
+                                      "sample": rsample}
 
     if rank == 0:
         line = {
@@ -453,10 +530,15 @@ def main():
             "config": {
                 "workload": desc, "rows": int(plan.starts[-1]), "nnz": total_nnz, "n": n,
                 "shard_rows": a.num_rows, "shard_nnz": a.nnz, "touched_b_rows": touched,
-                "schedule": choice.point, "p": choice.p, "family": k.family,
-                "heuristic_choice": heur.label(), "selector": "given" if args.point else "autotune",
+                "schedule": choice.point, "p": choice.p, "hw_variant": choice.hw_variant,
+                "family": k.family, "heuristic_choice": heur.label(),
+                "selector": "given" if args.point else "autotune",
                 "parallelism": f"row-shard{world}" if world > 1 else "single",
+                "shard_row_starts": [int(x) for x in plan.starts] if world > 1 else None,
+                "rank_total_ms": rank_ms if world > 1 else None,
                 "l2": "inputs > L2 (A+B+C far above 126 MB): no flush needed",
+                "plan": {"table_rows": aux.table_rows, "longest_row": aux.longest_row,
+                         "exact_rows": aux.exact_count, "workspace_bytes": aux.nbytes()},
                 "stats": stats.as_dict(),
             },
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
@@ -470,6 +552,98 @@ def main():
                                                     "heuristic": heur.label()}, indent=1))
     if world > 1:
         dist.destroy_process_group()
+
+
+def measure_e2e(args, a, b, c, k, choice, plan_for, n, total_nnz, world, dev, stream):
+    """The same metric through host buffers: (1) steady state through
+    ``pipeline.HostSpmm`` (pinned A, B up / SpMM / C down per step,
+    overlapped); (2) one cold start through the public device API: upload A
+    and B, plan on the device (sgap_plan), SpMM, download C."""
+    import torch.distributed as dist
+    from paper_2209_02882_b200.device import DeviceCsr, prepare_aux, spmm
+    from paper_2209_02882_b200.pipeline import HostSpmm
+    h_rp = a.row_ptr.cpu().pin_memory()
+    h_ci = a.col_idx.cpu().pin_memory()
+    h_v = a.vals.cpu().pin_memory()
+    h_b = b.cpu().pin_memory()
+    h_c = torch.empty(c.shape, dtype=c.dtype).pin_memory()
+
+    def plan_block(rows, sub_rp):
+        return plan_for(choice, n, rows, a.num_cols, sub_rp)
+
+    pipe = HostSpmm(a.num_rows, a.num_cols, n, h_rp, h_ci, plan_block, blocks=args.e2e_blocks,
+                    hw_variant=choice.hw_variant)
+    pipe(h_v, h_b, h_c)
+    pipe.wait()
+    torch.cuda.synchronize()
+    e_steps = max(3, min(args.steps, 10))
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e_steps):
+        pipe(h_v, h_b, h_c)
+    pipe.wait(stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    te = torch.tensor([e0.elapsed_time(e1) / e_steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    h2d, d2h = pipe.h2d_bytes(), pipe.d2h_bytes()
+    del pipe
+    torch.cuda.empty_cache()
+    # the PCIe floor of one step: the same bytes up and down at once, no compute
+    s_up, s_dn = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    d_rp, d_ci, d_v = (torch.empty_like(x, device=dev) for x in (h_rp, h_ci, h_v))
+    d_c = torch.empty_like(h_c, device=dev)
+
+    def copies():
+        s_up.wait_stream(stream)
+        s_dn.wait_stream(stream)
+        with torch.cuda.stream(s_up):
+            for dst, src in ((d_rp, h_rp), (d_ci, h_ci), (d_v, h_v), (b, h_b)):
+                dst.copy_(src, non_blocking=True)
+        with torch.cuda.stream(s_dn):
+            h_c.copy_(d_c, non_blocking=True)
+        stream.wait_stream(s_up)
+        stream.wait_stream(s_dn)
+
+    floor = float("inf")
+    for _ in range(3):
+        e0.record(stream)
+        copies()
+        e1.record(stream)
+        e1.synchronize()
+        floor = min(floor, e0.elapsed_time(e1))
+    del d_c
+    # cold start: upload + device planning + SpMM + download, serial
+    torch.cuda.synchronize()
+    e0.record(stream)
+    d_rp.copy_(h_rp, non_blocking=True)
+    d_ci.copy_(h_ci, non_blocking=True)
+    d_v.copy_(h_v, non_blocking=True)
+    b.copy_(h_b, non_blocking=True)
+    a2 = DeviceCsr(a.num_rows, a.num_cols, d_rp, d_ci, d_v)
+    aux2 = prepare_aux(k, a2, stream=stream)
+    spmm(k, a2, b, c, aux=aux2, hw_block=choice.hw_block, hw_variant=choice.hw_variant,
+         stream=stream)
+    h_c.copy_(c, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    cold_ms = e0.elapsed_time(e1)
+    del aux2, a2, d_rp, d_ci, d_v
+    ms = float(te.item())
+    return {"value": 2.0 * total_nnz * n / (ms * 1e6), "unit": UNIT,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": ms, "steps": e_steps,
+            "pcie_floor_ms": floor, "frac_of_pcie_floor": floor / ms,
+            "cold_start_ms": cold_ms,
+            "cold_start_gflops": 2.0 * a.nnz * n / (cold_ms * 1e6),
+            "cold_start_path": "pinned host A, B -> device; sgap_plan (row stats, block starts, "
+                               "row ids, float64 table) -> SpMM -> C to pinned host, one stream",
+            "path": f"pinned host A,B -> {args.e2e_blocks} row blocks: H2D / SpMM / D2H C "
+                    "overlapped on 3 streams, device buffers double-buffered across steps "
+                    "(paper_2209_02882_b200.pipeline.HostSpmm; structure planned once)"}
 
 
 if __name__ == "__main__":

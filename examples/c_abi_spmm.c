@@ -1,6 +1,6 @@
 /*
  * The drop-in boundary from plain C: build a Sgap kernel for a point, run it
- * through sgap_run on the device and check against a host double-precision
+ * through sgap_plan + sgap_run on the device and check against a host double-precision
  * product.  No Python, no torch -- only libsgap.so, sgap.h and the CUDA
  * runtime.  Exit status 0 on success.
  *
@@ -42,10 +42,8 @@ static int run_point(const char *label, sgap_point_t pt, int M, int K, int N, in
     sgap_kernel_t k;
     int32_t rule = 0;
     SG(sgap_build_kernel(&pt, N, p, M, nnz, &k, &rule));
-    int *d_rp, *d_ci, *d_starts = NULL, *d_rowid = NULL, *d_long_rows = NULL, *d_long_count = NULL,
-        *d_slot = NULL, *d_exact = NULL;
+    int *d_rp, *d_ci;
     float *d_av, *d_b, *d_c;
-    double *d_long_acc = NULL;
     CK(cudaMalloc((void **)&d_rp, (M + 1) * sizeof(int)));
     CK(cudaMalloc((void **)&d_ci, nnz * sizeof(int)));
     CK(cudaMalloc((void **)&d_av, nnz * sizeof(float)));
@@ -56,53 +54,19 @@ static int run_point(const char *label, sgap_point_t pt, int M, int K, int N, in
     CK(cudaMemcpy(d_av, av, nnz * sizeof(float), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(d_b, hb, (size_t)K * N * sizeof(float), cudaMemcpyHostToDevice));
 
-    sgap_aux_t aux = {0};
-    const int eb = k.family == SGAP_NNZ_ONE || k.family == SGAP_NNZ_MULTIPLE;
-    if (eb) {  /* block starts (LoweredKernel.block_starts), row ids, long-row table */
-        CK(cudaMalloc((void **)&d_starts, (k.grid_size + 1) * sizeof(int)));
-        SG(sgap_block_starts(d_rp, M, k.chunk, k.grid_size, d_starts, NULL));
-        const int64_t thr = sgap_long_row_threshold(&k, SGAP_F32);
-        CK(cudaMalloc((void **)&d_rowid, nnz * sizeof(int)));
-        SG(sgap_row_ids(d_rp, M, nnz, thr, 0, d_rowid, NULL));
-        aux.d_block_starts = d_starts;
-        aux.d_rowid = d_rowid;
-        aux.long_threshold = thr;
-        if (thr >= 0) {
-            const int64_t cap = sgap_long_row_capacity(nnz, thr, 0);
-            CK(cudaMalloc((void **)&d_long_rows, cap * sizeof(int)));
-            CK(cudaMalloc((void **)&d_long_count, sizeof(int)));
-            CK(cudaMalloc((void **)&d_long_acc, cap * N * sizeof(double)));
-            CK(cudaMalloc((void **)&d_slot, M * sizeof(int)));
-            aux.d_long_rows = d_long_rows;
-            aux.d_long_count = d_long_count;
-            aux.d_long_acc = d_long_acc;
-            aux.d_long_slot = d_slot;
-            aux.long_capacity = cap;
-            /* rows of the error-free pass: longer than max(thr, exact length) */
-            const int64_t cut = thr > sgap_exact_row_length() ? thr : sgap_exact_row_length();
-            int ne = 0, *ex = malloc(M * sizeof(int));
-            for (int i = 0; i < M; ++i) if (rp[i + 1] - rp[i] > cut) ex[ne++] = i;
-            if (ne && k.family == SGAP_NNZ_MULTIPLE) {
-                CK(cudaMalloc((void **)&d_exact, ne * sizeof(int)));
-                CK(cudaMemcpy(d_exact, ex, ne * sizeof(int), cudaMemcpyHostToDevice));
-                aux.d_exact_rows = d_exact;
-                aux.exact_count = ne;
-                aux.has_exact_rows = 1;
-            }
-            free(ex);
-            const size_t tmp_bytes = sgap_long_rows_tmp_bytes(M);
-            void *d_tmp;
-            CK(cudaMalloc(&d_tmp, tmp_bytes));
-            SG(sgap_prepare_long_rows(d_rp, M, N, &aux, d_tmp, tmp_bytes, NULL));
-            CK(cudaDeviceSynchronize());
-            CK(cudaFree(d_tmp));
-        }
-    }
+    /* plan (block starts, row ids, float64 long-row table -- all on the
+       device, CSR invariants validated first) + run */
     sgap_csr_t a = {M, K, nnz, d_rp, d_ci, d_av};
+    size_t ws_bytes = 0;
+    void *d_ws;
+    sgap_plan_t plan;
+    SG(sgap_plan_workspace_bytes(&k, &a, SGAP_F32, SGAP_PLAN_VALIDATE, &ws_bytes));
+    CK(cudaMalloc(&d_ws, ws_bytes));
+    SG(sgap_plan(&k, &a, SGAP_F32, SGAP_PLAN_VALIDATE, d_ws, ws_bytes, &plan, NULL));
     unsigned long long *d_wb;
     CK(cudaMalloc((void **)&d_wb, sizeof(unsigned long long)));
     CK(cudaMemset(d_wb, 0, sizeof(unsigned long long)));
-    SG(sgap_run(&k, &a, d_b, d_c, SGAP_F32, 0, &aux, d_wb, NULL));
+    SG(sgap_run(&plan, &a, d_b, d_c, 0, d_wb, NULL));
     CK(cudaDeviceSynchronize());
 
     float *hc = malloc((size_t)M * N * sizeof(float));
@@ -120,10 +84,49 @@ static int run_point(const char *label, sgap_point_t pt, int M, int K, int N, in
     printf("%-22s family=%d grid=%lld block=%lld nnz=%d writebacks=%llu max_rel_error=%.3e\n", label,
            k.family, (long long)k.grid_size, (long long)k.block_size, nnz, wb, worst);
     cudaFree(d_rp); cudaFree(d_ci); cudaFree(d_av); cudaFree(d_b); cudaFree(d_c); cudaFree(d_wb);
-    cudaFree(d_starts); cudaFree(d_rowid); cudaFree(d_long_rows); cudaFree(d_long_count);
-    cudaFree(d_long_acc); cudaFree(d_slot); cudaFree(d_exact);
+    cudaFree(d_ws);
     free(rp); free(ci); free(av); free(hb); free(hc);
     return worst <= 1e-5 ? 0 : 1;
+}
+
+/* SimulationFault (sim.py:279-287) / CsrMatrix invariants (matrices.py:58-75):
+   an out-of-range column and a decreasing row_ptr are reported by the
+   validating planner, not read out of bounds. */
+static int fault_case(void) {
+    const int rp_bad_col[4] = {0, 2, 3, 4}, ci_bad_col[4] = {0, 5, 1, 2}; /* K = 4: col 5 */
+    const int rp_bad_rp[4] = {0, 3, 2, 4}, ci_ok[4] = {0, 1, 2, 3};
+    const float av[4] = {1, 2, 3, 4};
+    const sgap_point_t pt = {SGAP_KIND_ROW, SGAP_AMT_ONE, 0, SGAP_AMT_ONE, 0, 1};
+    int *d_rp, *d_ci;
+    float *d_av;
+    void *d_ws;
+    CK(cudaMalloc((void **)&d_rp, 4 * sizeof(int)));
+    CK(cudaMalloc((void **)&d_ci, 4 * sizeof(int)));
+    CK(cudaMalloc((void **)&d_av, 4 * sizeof(float)));
+    CK(cudaMemcpy(d_av, av, sizeof(av), cudaMemcpyHostToDevice));
+    sgap_kernel_t k;
+    SG(sgap_build_kernel(&pt, 32, 256, 3, 4, &k, NULL));
+    sgap_csr_t a = {3, 4, 4, d_rp, d_ci, d_av};
+    size_t ws = 0;
+    SG(sgap_plan_workspace_bytes(&k, &a, SGAP_F32, SGAP_PLAN_VALIDATE, &ws));
+    CK(cudaMalloc(&d_ws, ws));
+    sgap_plan_t plan;
+    int64_t pos = 0;
+    CK(cudaMemcpy(d_rp, rp_bad_col, sizeof(rp_bad_col), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_ci, ci_bad_col, sizeof(ci_bad_col), cudaMemcpyHostToDevice));
+    const int s1 = sgap_plan(&k, &a, SGAP_F32, SGAP_PLAN_VALIDATE, d_ws, ws, &plan, NULL);
+    const int v1 = sgap_validate_csr(&a, d_ws, &pos, NULL);
+    const int64_t pos1 = pos;
+    CK(cudaMemcpy(d_rp, rp_bad_rp, sizeof(rp_bad_rp), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_ci, ci_ok, sizeof(ci_ok), cudaMemcpyHostToDevice));
+    const int v2 = sgap_validate_csr(&a, d_ws, &pos, NULL);
+    const int64_t pos2 = pos;
+    cudaFree(d_rp); cudaFree(d_ci); cudaFree(d_av); cudaFree(d_ws);
+    const int ok = s1 == SGAP_ERR_FAULT && v1 == SGAP_ERR_FAULT && pos1 == 1 &&
+                   v2 == SGAP_ERR_FAULT && pos2 == -2;
+    printf("%-22s plan=%s col fault at %lld, row_ptr fault at %lld\n", "fault detection",
+           sgap_status_string(s1), (long long)pos1, (long long)pos2);
+    return ok ? 0 : 1;
 }
 
 int main(void) {
@@ -140,6 +143,7 @@ int main(void) {
                             "row:1/8,col:4,r:8"};
     int bad = 0;
     for (int i = 0; i < 4; ++i) bad |= run_point(names[i], pts[i], 3000, 2000, 64, 256);
+    bad |= fault_case();
     printf(bad ? "FAIL\n" : "OK\n");
     return bad;
 }

@@ -16,8 +16,15 @@
  *                         (family + divisibility gates   templates.py:82-202,
  *                          + grid/block geometry)         lowering.py:218-243,649-696)
  *   sgap_block_starts     lowering.compute_block_starts  lowering.py:119-128
+ *   sgap_plan_workspace_bytes / sgap_plan
+ *                         the per-matrix half of         lowering.py:683-696
+ *                         runner.build_kernel (block_starts) + the engine's
+ *                         side data (row ids, float64 long-row table,
+ *                         error-free row list), all built on the device
+ *   sgap_validate_csr     CsrMatrix invariants +         matrices.py:58-75,
+ *                         SimulationFault on an out-of-  sim.py:279-287
+ *                         range index
  *   sgap_run              sim.run                        sim.py:431-487
- *   sgap_prepare_long_rows (engine-side numerics, no reference counterpart)
  *   sgap_seg_reduce_group sim.exec_seg_reduce_group      sim.py:139-165
  *   sgap_atomic_add_group sim.exec_atomic_add_group      sim.py:112-136
  *
@@ -38,7 +45,7 @@
 extern "C" {
 #endif
 
-#define SGAP_ABI_VERSION 3
+#define SGAP_ABI_VERSION 4
 
 typedef enum {
     SGAP_OK = 0,
@@ -134,8 +141,10 @@ int sgap_block_starts(const int32_t *d_row_ptr, int64_t num_rows, int64_t chunk,
                       int64_t num_blocks, int32_t *d_starts, void *stream);
 
 /* Per-matrix side data of a kernel (what the reference's LoweredKernel
- * carries beyond its integers, plus the long-row table of this engine).  All
- * device memory is owned by the caller.
+ * carries beyond its integers, plus the long-row table of this engine).
+ * Filled by sgap_plan inside the caller's workspace and read by sgap_run;
+ * callers never build it (ABI v4: sgap_run takes a plan, so the float64
+ * long-row policy cannot be bypassed).  Field notes:
  *   d_block_starts: [grid_size + 1] from sgap_block_starts
  *     (LoweredKernel.block_starts, lowering.py:683-696); informational: the
  *     kernels use d_rowid instead of per-lane searches in its windows.
@@ -180,40 +189,81 @@ int sgap_row_ids(const int32_t *d_row_ptr, int64_t num_rows, int64_t nnz,
                  int64_t long_threshold, int64_t long_chunk, int32_t *d_rowid,
                  void *stream);
 
-/* Rows longer than this (and in the long-row table) are accumulated with an
- * error-free transform (TwoProduct + TwoSum): float32 product rounding alone
- * would reach ~1e-5 of the reference metric beyond ~2e5 nonzeros.           */
+/* Rows longer than this are accumulated error-free (float64 products of the
+ * float32 inputs, summed in float64): float32 product rounding alone would
+ * reach ~1e-5 of the reference metric on hub rows of ~2e4+ nonzeros.       */
 int64_t sgap_exact_row_length(void);
 
-/* Threshold the engine uses for a kernel (-1: no table needed: row families
- * keep float64 running sums, float64 values accumulate in float64).        */
+/* Long-row threshold the planner uses for a kernel (-1: no table: row
+ * families keep float64 running sums, float64 values accumulate in
+ * float64).  Informational; sgap_plan applies it.                          */
 int64_t sgap_long_row_threshold(const sgap_kernel_t *kernel, int32_t dtype);
-/* Chunk length whose straddling rows join the table (0: none); nnz-multiple
- * with g >= 128 in float32.                                                 */
-int64_t sgap_long_row_chunk(const sgap_kernel_t *kernel, int32_t dtype);
-/* Upper bound on the number of table rows: rows with > threshold nonzeros
- * plus (chunk > 0) one straddling row per chunk boundary.                   */
-int64_t sgap_long_row_capacity(int64_t nnz, int64_t threshold, int64_t chunk);
-/* Scratch for the ordered compaction in sgap_prepare_long_rows. */
-size_t sgap_long_rows_tmp_bytes(int64_t num_rows);
-/* Fill aux->d_long_rows / d_long_count (and d_long_slot when set) for
- * aux->long_threshold and aux->long_chunk, and zero aux->d_long_acc
- * (long_capacity x n). */
-int sgap_prepare_long_rows(const int32_t *d_row_ptr, int64_t num_rows, int32_t n,
-                           sgap_aux_t *aux, void *d_tmp, size_t tmp_bytes,
-                           void *stream);
 
-/* sim.run: C (+)= A @ B on the device.
- *   d_b: [a->num_cols x kernel->n] row-major, d_c: [a->num_rows x n] row-major.
+/* ---- the planner (runner.build_kernel's per-matrix half, on the device) ---
+ * A plan binds one kernel to one sparsity structure: block starts, per-
+ * position row ids, the float64 long-row table and the error-free row list,
+ * all in one caller-owned device workspace.  Values (d_vals), B and C may
+ * change between runs; the structure (row_ptr / col_idx buffers and their
+ * contents) must not -- sgap_run rejects a CSR whose shape or index buffers
+ * differ from the planned ones (SGAP_ERR_SHAPE).
+ *
+ * sgap_plan runs on `stream` and synchronises it once to read back 24 bytes
+ * of row statistics (longest row, number of table rows and of error-free
+ * rows), which size the per-run launches.  It allocates nothing.            */
+#define SGAP_PLAN_VALIDATE 1u     /* run sgap_validate_csr first            */
+#define SGAP_PLAN_SPLIT_ROWS 2u   /* nnz-multiple, g >= 128: rows straddling a
+                                     g-chunk boundary join the float64 table
+                                     (no zero-fill pre-pass; measured slower
+                                     on config 2, off by default)           */
+
+typedef struct {
+    int32_t abi;            /* SGAP_ABI_VERSION of the planner              */
+    int32_t dtype;          /* sgap_dtype_t the plan was built for          */
+    sgap_kernel_t kernel;   /* copy; hw_block / hw_variant may be changed
+                               between runs, nothing else                  */
+    int64_t num_rows, num_cols, nnz;
+    const int32_t *d_row_ptr;  /* the planned structure (identity check)    */
+    const int32_t *d_col_idx;
+    int64_t longest_row;    /* max row length                               */
+    int64_t table_rows;     /* rows in the float64 long-row table           */
+    sgap_aux_t aux;         /* pointers into the workspace                  */
+    void *d_workspace;
+    size_t workspace_bytes;
+} sgap_plan_t;
+
+/* Workspace bytes sgap_plan needs for (kernel, A's shape, dtype, flags):
+ * an upper bound from num_rows / nnz alone (no device access).             */
+int sgap_plan_workspace_bytes(const sgap_kernel_t *kernel, const sgap_csr_t *a, int32_t dtype,
+                              uint32_t flags, size_t *bytes);
+
+/* Build the plan.  d_workspace: >= sgap_plan_workspace_bytes, 256-byte
+ * aligned, owned by the caller and kept alive (unmodified) while the plan is
+ * used.  Returns SGAP_ERR_FAULT (with SGAP_PLAN_VALIDATE) for a malformed
+ * CSR, SGAP_ERR_ARG / SHAPE / PRECISION / CONFIG / CUDA otherwise.         */
+int sgap_plan(const sgap_kernel_t *kernel, const sgap_csr_t *a, int32_t dtype, uint32_t flags,
+              void *d_workspace, size_t workspace_bytes, sgap_plan_t *plan, void *stream);
+
+/* The CsrMatrix invariants (matrices.py:58-75: row_ptr[0] == 0, row_ptr
+ * non-decreasing, row_ptr[num_rows] == nnz, 0 <= col < num_cols, columns
+ * strictly increasing within a row), checked on the device.  Returns SGAP_OK
+ * or SGAP_ERR_FAULT; *fault_pos (may be NULL) receives the first offending
+ * position: a row_ptr index r as -(r + 1), a col_idx position as itself.
+ * d_scratch: 8 bytes of device memory.  Synchronises `stream`.            */
+int sgap_validate_csr(const sgap_csr_t *a, void *d_scratch, int64_t *fault_pos, void *stream);
+
+/* sim.run: C (+)= A @ B on the device with a plan from sgap_plan.
+ *   a: the planned structure (same shape, row_ptr and col_idx buffers; vals
+ *   may differ), values of plan->dtype.
+ *   d_b: [a->num_cols x kernel.n] row-major, d_c: [a->num_rows x n] row-major,
+ *   aligned to the kernel's column vector (c elements).
  *   accumulate = 1: C += A@B (c0 already in d_c, sim.py:439-441);
  *   accumulate = 0: C = A@B (d_c is overwritten; zero-fill included).
- *   aux: side data (required for the nnz families; NULL allowed otherwise).
  *   d_writebacks: optional (NULL = off) device counter, incremented by the
  *   number of output writebacks (== SimMetrics.atomic_ops of the reference
- *   simulator for the same kernel; 0 for row-multiple).                      */
-int sgap_run(const sgap_kernel_t *kernel, const sgap_csr_t *a, const void *d_b,
-             void *d_c, int32_t dtype, int32_t accumulate, const sgap_aux_t *aux,
-             unsigned long long *d_writebacks, void *stream);
+ *   simulator for the same kernel; 0 for row-multiple).
+ *   Launch-only: no allocation, no host synchronisation.                     */
+int sgap_run(const sgap_plan_t *plan, const sgap_csr_t *a, const void *d_b, void *d_c,
+             int32_t accumulate, unsigned long long *d_writebacks, void *stream);
 
 /* The dense reference product that runner.verify_point checks against
  * (runner.py:193-194 -> matrices.dense_spmm_oracle, matrices.py:241-254),

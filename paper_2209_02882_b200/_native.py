@@ -44,10 +44,9 @@ EXPORTED = (
     "sgap_row_ids",
     "sgap_exact_row_length",
     "sgap_long_row_threshold",
-    "sgap_long_row_chunk",
-    "sgap_long_row_capacity",
-    "sgap_long_rows_tmp_bytes",
-    "sgap_prepare_long_rows",
+    "sgap_plan_workspace_bytes",
+    "sgap_plan",
+    "sgap_validate_csr",
     "sgap_run",
     "sgap_reference_spmm_f64",
     "sgap_seg_reduce_group",
@@ -126,6 +125,30 @@ class Aux(ctypes.Structure):
     ]
 
 
+class Plan(ctypes.Structure):
+    """sgap_plan_t (include/sgap.h): filled by sgap_plan, read by sgap_run."""
+
+    _fields_ = [
+        ("abi", ctypes.c_int32),
+        ("dtype", ctypes.c_int32),
+        ("kernel", Kernel),
+        ("num_rows", ctypes.c_int64),
+        ("num_cols", ctypes.c_int64),
+        ("nnz", ctypes.c_int64),
+        ("d_row_ptr", ctypes.c_void_p),
+        ("d_col_idx", ctypes.c_void_p),
+        ("longest_row", ctypes.c_int64),
+        ("table_rows", ctypes.c_int64),
+        ("aux", Aux),
+        ("d_workspace", ctypes.c_void_p),
+        ("workspace_bytes", ctypes.c_size_t),
+    ]
+
+
+# sgap_plan flags
+PLAN_VALIDATE = 1
+PLAN_SPLIT_ROWS = 2
+
 _lib = None
 
 
@@ -159,16 +182,15 @@ def lib():
     L.sgap_exact_row_length.restype = i64
     L.sgap_long_row_threshold.argtypes = [ctypes.POINTER(Kernel), i32]
     L.sgap_long_row_threshold.restype = i64
-    L.sgap_long_row_chunk.argtypes = [ctypes.POINTER(Kernel), i32]
-    L.sgap_long_row_chunk.restype = i64
-    L.sgap_long_row_capacity.argtypes = [i64, i64, i64]
-    L.sgap_long_row_capacity.restype = i64
-    L.sgap_long_rows_tmp_bytes.argtypes = [i64]
-    L.sgap_long_rows_tmp_bytes.restype = ctypes.c_size_t
-    L.sgap_prepare_long_rows.argtypes = [vp, i64, i32, ctypes.POINTER(Aux), vp, ctypes.c_size_t, vp]
-    L.sgap_prepare_long_rows.restype = ctypes.c_int
-    L.sgap_run.argtypes = [ctypes.POINTER(Kernel), ctypes.POINTER(Csr), vp, vp, i32, i32,
-                           ctypes.POINTER(Aux), vp, vp]
+    L.sgap_plan_workspace_bytes.argtypes = [ctypes.POINTER(Kernel), ctypes.POINTER(Csr), i32,
+                                            ctypes.c_uint32, ctypes.POINTER(ctypes.c_size_t)]
+    L.sgap_plan_workspace_bytes.restype = ctypes.c_int
+    L.sgap_plan.argtypes = [ctypes.POINTER(Kernel), ctypes.POINTER(Csr), i32, ctypes.c_uint32, vp,
+                            ctypes.c_size_t, ctypes.POINTER(Plan), vp]
+    L.sgap_plan.restype = ctypes.c_int
+    L.sgap_validate_csr.argtypes = [ctypes.POINTER(Csr), vp, ctypes.POINTER(i64), vp]
+    L.sgap_validate_csr.restype = ctypes.c_int
+    L.sgap_run.argtypes = [ctypes.POINTER(Plan), ctypes.POINTER(Csr), vp, vp, i32, vp, vp]
     L.sgap_run.restype = ctypes.c_int
     L.sgap_reference_spmm_f64.argtypes = [ctypes.POINTER(Csr), vp, i32, i32, vp, vp]
     L.sgap_reference_spmm_f64.restype = ctypes.c_int

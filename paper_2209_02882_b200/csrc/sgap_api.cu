@@ -15,8 +15,6 @@
 
 using namespace sgap;
 
-extern "C" int64_t sgap_long_row_capacity(int64_t nnz, int64_t threshold, int64_t chunk);
-
 namespace {
 
 constexpr int kHwBlock = 256;
@@ -234,7 +232,7 @@ int launch_nnz_multiple(bool tma, int tile, int owner, const sgap_kernel_t &k,
 template <typename T, int V, int W>
 int run_nnz_multiple_w(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
                        const int *rowid, const LongRows &lr, int owner, bool has_exact,
-                       unsigned long long *wb, cudaStream_t st) {
+                       bool zero, unsigned long long *wb, cudaStream_t st) {
     const int tile = tma_tile_for(k.g);
     const bool tma_ok = tile > 0 && aligned(rowid, 16) && aligned(a.d_col_idx, 16) &&
                         aligned(a.d_vals, 16);
@@ -244,9 +242,23 @@ int run_nnz_multiple_w(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, 
     // itself) and for narrow N (profiles/r01_selector_regret.json)
     const int variant = k.hw_variant == 0 ? ((tma_ok && W >= 16 && k.g <= 128) ? 2 : 1) : k.hw_variant;
     const bool tma = variant == 2;
+    // every check that can reject the call runs before the first launch: an
+    // error after the exact pass would leave its sums in the float64 table
+    // (never folded, so a later call on the same plan would add them to C)
     if (tma && !tma_ok) return SGAP_ERR_ARG;
     if (variant < 1 || variant > 4) return SGAP_ERR_ARG;
     if (variant >= 3 && W != 32) return SGAP_ERR_ARG;  // the staged walk takes a whole warp
+    if (variant >= 3 && k.hw_block > 0 && k.hw_block != kHwBlock) return SGAP_ERR_ARG;
+    if (tma) {
+        const size_t smem = tma_smem_bytes<T, 3>();
+        if (cudaFuncSetAttribute(k_nnz_multiple_tma<T, V, W, 4, 3, 3>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return SGAP_ERR_CUDA;
+    }
+    if (zero) {
+        k_zero_shared_rows<T><<<grid_for(ceil_div(a.num_rows, 32), kHwBlock), kHwBlock, 0, st>>>(
+            a.d_row_ptr, (int)a.num_rows, k.n, k.g, lr.threshold, C);
+    }
     // chunks inside exact-flagged rows (error-free accumulate) run in their
     // own kernel, launched first; the main walk follows with programmatic
     // dependent launch, so the two overlap (no data dependency: both only add
@@ -272,8 +284,7 @@ int run_nnz_multiple_w(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, 
     if (variant >= 3) {
         const long long total_pos = k.grid_size * k.chunk;
         const long long chunks = total_pos / k.g;
-        const int blk = k.hw_block > 0 ? k.hw_block : kHwBlock;
-        if (blk != kHwBlock) return SGAP_ERR_ARG;
+        const int blk = kHwBlock;
         const dim3 grid(grid_for(chunks, blk));
         if (variant == 3)
             return launch_k(k_nnz_multiple_staged<T, V, 4, 4>, grid, dim3(blk), 0, st, pdl, rowid,
@@ -297,17 +308,14 @@ int run_nnz_multiple(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T 
     // overwrites it, so nothing needs zeroing
     const int owner = acc ? 0 : 1;
     const bool routed = lr.threshold >= 0 && lr.chunk == k.g;
-    if (owner && !routed) {
-        k_zero_shared_rows<T><<<grid_for(ceil_div(a.num_rows, 32), kHwBlock), kHwBlock, 0, st>>>(
-            a.d_row_ptr, (int)a.num_rows, k.n, k.g, lr.threshold, C);
-    }
+    const bool zero = owner && !routed;  // launched by the walk after its checks
     switch (pow2_floor(k.n / V)) {
-        case 1: return run_nnz_multiple_w<T, V, 1>(k, a, B, C, rowid, lr, owner, has_exact, wb, st);
-        case 2: return run_nnz_multiple_w<T, V, 2>(k, a, B, C, rowid, lr, owner, has_exact, wb, st);
-        case 4: return run_nnz_multiple_w<T, V, 4>(k, a, B, C, rowid, lr, owner, has_exact, wb, st);
-        case 8: return run_nnz_multiple_w<T, V, 8>(k, a, B, C, rowid, lr, owner, has_exact, wb, st);
-        case 16: return run_nnz_multiple_w<T, V, 16>(k, a, B, C, rowid, lr, owner, has_exact, wb, st);
-        default: return run_nnz_multiple_w<T, V, 32>(k, a, B, C, rowid, lr, owner, has_exact, wb, st);
+        case 1: return run_nnz_multiple_w<T, V, 1>(k, a, B, C, rowid, lr, owner, has_exact, zero, wb, st);
+        case 2: return run_nnz_multiple_w<T, V, 2>(k, a, B, C, rowid, lr, owner, has_exact, zero, wb, st);
+        case 4: return run_nnz_multiple_w<T, V, 4>(k, a, B, C, rowid, lr, owner, has_exact, zero, wb, st);
+        case 8: return run_nnz_multiple_w<T, V, 8>(k, a, B, C, rowid, lr, owner, has_exact, zero, wb, st);
+        case 16: return run_nnz_multiple_w<T, V, 16>(k, a, B, C, rowid, lr, owner, has_exact, zero, wb, st);
+        default: return run_nnz_multiple_w<T, V, 32>(k, a, B, C, rowid, lr, owner, has_exact, zero, wb, st);
     }
 }
 
@@ -391,6 +399,189 @@ int prim_entry(bool seg, const int64_t *idx, const void *val, const uint8_t *act
                                      as_stream(stream));
     return SGAP_ERR_PRECISION;
 }
+
+int64_t long_row_chunk(const sgap_kernel_t *k, int32_t dtype) {
+    if (k == nullptr || dtype != SGAP_F32 || k->family != SGAP_NNZ_MULTIPLE) return 0;
+    // short chunks would put most rows in the table (capacity ~ nnz/g rows x n)
+    return k->g >= 128 ? k->g : 0;
+}
+
+int64_t long_row_capacity(int64_t nnz, int64_t threshold, int64_t chunk) {
+    if (threshold < 0) return 0;
+    long long cap = nnz / (threshold + 1) + 1;
+    if (chunk > 0) cap += (nnz + chunk - 1) / chunk;  // one straddling row per boundary
+    return cap;
+}
+
+size_t long_rows_tmp_bytes(int64_t num_rows) {
+    size_t bytes = 0;
+    LongRowPred pred{nullptr, 0, 0};
+    cub::DeviceSelect::If(nullptr, bytes, thrust::counting_iterator<int>(0), (int *)nullptr,
+                          (int *)nullptr, (int)(num_rows > 0 ? num_rows : 1), pred);
+    return bytes;
+}
+
+int prepare_long_rows(const int32_t *d_row_ptr, int64_t num_rows, int32_t n,
+                           sgap_aux_t *aux, void *d_tmp, size_t tmp_bytes, void *stream) {
+    if (aux == nullptr || d_row_ptr == nullptr || n < 1) return SGAP_ERR_ARG;
+    if (aux->long_threshold < 0) return SGAP_OK;
+    if (aux->d_long_rows == nullptr || aux->d_long_count == nullptr || aux->d_long_acc == nullptr)
+        return SGAP_ERR_ARG;
+    if (num_rows > INT_MAX - 1) return SGAP_ERR_SHAPE;
+    cudaStream_t st = as_stream(stream);
+    if (num_rows == 0) {
+        return cudaMemsetAsync(aux->d_long_count, 0, sizeof(int32_t), st) == cudaSuccess
+                   ? SGAP_OK : SGAP_ERR_CUDA;
+    }
+    size_t need = long_rows_tmp_bytes(num_rows);
+    if (d_tmp == nullptr || tmp_bytes < need) return SGAP_ERR_ARG;
+    LongRowPred pred{d_row_ptr, aux->long_threshold, aux->long_chunk};
+    if (cub::DeviceSelect::If(d_tmp, tmp_bytes, thrust::counting_iterator<int>(0),
+                              aux->d_long_rows, aux->d_long_count, (int)num_rows, pred, st) !=
+        cudaSuccess)
+        return SGAP_ERR_CUDA;
+    if (aux->d_long_slot != nullptr) {
+        long long cap = aux->long_capacity;
+        unsigned blocks = (unsigned)ceil_div(cap > 0 ? cap : 1, kHwBlock);
+        if (blocks > 4096) blocks = 4096;
+        k_long_slots<<<blocks, kHwBlock, 0, st>>>(aux->d_long_rows, aux->d_long_count,
+                                                  aux->d_long_slot);
+    }
+    const size_t acc_bytes = (size_t)aux->long_capacity * (size_t)n * sizeof(double);
+    if (acc_bytes && cudaMemsetAsync(aux->d_long_acc, 0, acc_bytes, st) != cudaSuccess)
+        return SGAP_ERR_CUDA;
+    return launch_status();
+}
+
+static int run_impl(const sgap_kernel_t *k, const sgap_csr_t *a, const void *d_b, void *d_c,
+                    int32_t dtype, int32_t accumulate, const sgap_aux_t *aux,
+                    unsigned long long *d_writebacks, void *stream) {
+    if (k == nullptr || a == nullptr) return SGAP_ERR_ARG;
+    if (dtype != SGAP_F32 && dtype != SGAP_F64) return SGAP_ERR_PRECISION;
+    if (k->n < 1 || k->c < 1 || k->n % k->c) return SGAP_ERR_CONFIG;
+    // kernels are compiled with __launch_bounds__(256)
+    if (k->hw_block != 0 && (k->hw_block < 32 || k->hw_block > 256 || k->hw_block % 32))
+        return SGAP_ERR_ARG;
+    if (a->num_rows < 0 || a->num_cols < 0 || a->nnz < 0) return SGAP_ERR_SHAPE;
+    if (a->num_rows > INT_MAX - 1 || a->nnz > INT_MAX) return SGAP_ERR_SHAPE;
+    const size_t esz = dtype == SGAP_F32 ? 4 : 8;
+    const long long out_elems = a->num_rows * (long long)k->n;
+    cudaStream_t st = as_stream(stream);
+    if (out_elems == 0) return SGAP_OK;
+    if (d_c == nullptr || a->d_row_ptr == nullptr) return SGAP_ERR_ARG;
+    if (a->nnz > 0 && (d_b == nullptr || a->d_col_idx == nullptr || a->d_vals == nullptr))
+        return SGAP_ERR_ARG;
+    const size_t vec_bytes = esz * (size_t)(k->c == 4 && esz == 8 ? 2 : k->c);
+    if ((d_b && !aligned(d_b, vec_bytes)) || !aligned(d_c, vec_bytes)) return SGAP_ERR_ARG;
+    const bool eb = k->family == SGAP_NNZ_ONE || k->family == SGAP_NNZ_MULTIPLE;
+    const int32_t *rowid = aux ? aux->d_rowid : nullptr;
+    if (eb && k->grid_size > 0 && a->nnz > 0 && rowid == nullptr) return SGAP_ERR_ARG;
+    if (k->family == SGAP_NNZ_MULTIPLE && (k->g < 1 || k->chunk % k->g)) return SGAP_ERR_CONFIG;
+    LongRows lr{nullptr, nullptr, nullptr, -1, nullptr, 0, nullptr, 0};
+    const bool has_exact = aux != nullptr && aux->has_exact_rows != 0;
+    // exact-flagged chunks are skipped by the main walk: their pass needs the list
+    if (has_exact && k->family == SGAP_NNZ_MULTIPLE && dtype == SGAP_F32 &&
+        aux->long_threshold >= 0 && (aux->d_exact_rows == nullptr || aux->exact_count <= 0))
+        return SGAP_ERR_ARG;
+    if (eb && aux && aux->long_threshold >= 0 && dtype == SGAP_F32) {
+        if (aux->d_long_rows == nullptr || aux->d_long_count == nullptr || aux->d_long_acc == nullptr)
+            return SGAP_ERR_ARG;
+        lr = LongRows{aux->d_long_rows, aux->d_long_count, aux->d_long_acc, aux->long_threshold,
+                      aux->d_long_slot, aux->long_chunk, aux->d_exact_rows, aux->exact_count};
+    }
+    if (k->family == SGAP_NNZ_ONE && !accumulate) {
+        // atomic-writeback families accumulate into C: zero-fill (counts as
+        // part of the SpMM, SURVEY 8(d)); nnz-multiple zero-fills only the
+        // rows it cannot store outright (k_zero_shared_rows).
+        if (cudaMemsetAsync(d_c, 0, (size_t)out_elems * esz, st) != cudaSuccess)
+            return SGAP_ERR_CUDA;
+    }
+    if (eb && k->grid_size == 0) {
+        if (k->family == SGAP_NNZ_MULTIPLE && !accumulate)  // every row is empty
+            return cudaMemsetAsync(d_c, 0, (size_t)out_elems * esz, st) == cudaSuccess ? SGAP_OK
+                                                                                    : SGAP_ERR_CUDA;
+        return SGAP_OK;
+    }
+    if (dtype == SGAP_F32)
+        return run_typed<float>(*k, *a, d_b, d_c, accumulate, rowid, lr, has_exact, d_writebacks,
+                                st);
+    return run_typed<double>(*k, *a, d_b, d_c, accumulate, rowid, lr, has_exact, d_writebacks, st);
+}
+
+
+// ------------------------------------------------------------------ planner
+
+// Rows longer than `cut` (the error-free pass's list), in ascending order.
+struct LongerThan {
+    const int *rp;
+    long long cut;
+    __host__ __device__ __forceinline__ bool operator()(const int &r) const {
+        return (long long)rp[r + 1] - rp[r] > cut;
+    }
+};
+
+// Workspace layout of a plan (every region 256-byte aligned).
+struct PlanLayout {
+    size_t starts = 0, rowid = 0, slot = 0, rows = 0, count = 0, acc = 0, exact = 0, stats = 0,
+           tmp = 0, total = 0;
+    long long thr = -1, chunk = 0, cap = 0, exact_cap = 0, exact_cut = 0;
+    size_t tmp_bytes = 0;
+};
+
+inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+int plan_layout(const sgap_kernel_t &k, const sgap_csr_t &a, int32_t dtype, uint32_t flags,
+                PlanLayout &L) {
+    const bool eb = k.family == SGAP_NNZ_ONE || k.family == SGAP_NNZ_MULTIPLE;
+    const long long M = a.num_rows, nnz = a.nnz;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t at = off;
+        off = align256(off + (bytes ? bytes : 1));
+        return at;
+    };
+    L.stats = take(4 * sizeof(unsigned long long));
+    if (eb) {
+        L.starts = take((size_t)(k.grid_size + 1) * sizeof(int));
+        L.rowid = take((size_t)(nnz > 4 ? nnz : 4) * sizeof(int));
+        L.thr = sgap_long_row_threshold(&k, dtype);
+        L.chunk = (L.thr >= 0 && (flags & SGAP_PLAN_SPLIT_ROWS)) ? long_row_chunk(&k, dtype) : 0;
+        if (L.thr >= 0) {
+            L.cap = long_row_capacity(nnz, L.thr, L.chunk);
+            if (L.cap > M) L.cap = M > 0 ? M : 1;
+            L.exact_cut = L.thr > kExactRow ? L.thr : kExactRow;
+            L.exact_cap = k.family == SGAP_NNZ_MULTIPLE ? nnz / (L.exact_cut + 1) + 1 : 0;
+            if (L.exact_cap > M) L.exact_cap = M > 0 ? M : 1;
+            L.slot = take((size_t)(M > 0 ? M : 1) * sizeof(int));
+            L.rows = take((size_t)L.cap * sizeof(int));
+            L.count = take(sizeof(int));
+            L.acc = take((size_t)L.cap * (size_t)k.n * sizeof(double));
+            L.exact = take((size_t)L.exact_cap * sizeof(int));
+            size_t ex_bytes = 0;
+            LongerThan pred{nullptr, 0};
+            cub::DeviceSelect::If(nullptr, ex_bytes, thrust::counting_iterator<int>(0),
+                                  (int *)nullptr, (int *)nullptr, (int)(M > 0 ? M : 1), pred);
+            L.tmp_bytes = long_rows_tmp_bytes(M);
+            if (ex_bytes > L.tmp_bytes) L.tmp_bytes = ex_bytes;
+            L.tmp = take(L.tmp_bytes);
+        }
+    }
+    L.total = off;
+    return SGAP_OK;
+}
+
+int check_kernel_csr(const sgap_kernel_t *k, const sgap_csr_t *a, int32_t dtype) {
+    if (k == nullptr || a == nullptr) return SGAP_ERR_ARG;
+    if (dtype != SGAP_F32 && dtype != SGAP_F64) return SGAP_ERR_PRECISION;
+    if (k->n < 1 || k->c < 1 || k->n % k->c) return SGAP_ERR_CONFIG;
+    if (k->family < SGAP_NNZ_MULTIPLE || k->family > SGAP_NNZ_ONE) return SGAP_ERR_ARG;
+    if (a->num_rows < 0 || a->num_cols < 0 || a->nnz < 0) return SGAP_ERR_SHAPE;
+    if (a->num_rows > kRowMask - 1 || a->nnz > INT_MAX) return SGAP_ERR_SHAPE;
+    if (k->grid_size < 0 || k->chunk < 0) return SGAP_ERR_CONFIG;
+    return SGAP_OK;
+}
+
+constexpr int32_t kPlanMagicAbi = SGAP_ABI_VERSION;
 
 }  // namespace
 
@@ -531,59 +722,6 @@ int64_t sgap_long_row_threshold(const sgap_kernel_t *k, int32_t dtype) {
 
 int64_t sgap_exact_row_length(void) { return kExactRow; }
 
-int64_t sgap_long_row_chunk(const sgap_kernel_t *k, int32_t dtype) {
-    if (k == nullptr || dtype != SGAP_F32 || k->family != SGAP_NNZ_MULTIPLE) return 0;
-    // short chunks would put most rows in the table (capacity ~ nnz/g rows x n)
-    return k->g >= 128 ? k->g : 0;
-}
-
-int64_t sgap_long_row_capacity(int64_t nnz, int64_t threshold, int64_t chunk) {
-    if (threshold < 0) return 0;
-    long long cap = nnz / (threshold + 1) + 1;
-    if (chunk > 0) cap += (nnz + chunk - 1) / chunk;  // one straddling row per boundary
-    return cap;
-}
-
-size_t sgap_long_rows_tmp_bytes(int64_t num_rows) {
-    size_t bytes = 0;
-    LongRowPred pred{nullptr, 0, 0};
-    cub::DeviceSelect::If(nullptr, bytes, thrust::counting_iterator<int>(0), (int *)nullptr,
-                          (int *)nullptr, (int)(num_rows > 0 ? num_rows : 1), pred);
-    return bytes;
-}
-
-int sgap_prepare_long_rows(const int32_t *d_row_ptr, int64_t num_rows, int32_t n,
-                           sgap_aux_t *aux, void *d_tmp, size_t tmp_bytes, void *stream) {
-    if (aux == nullptr || d_row_ptr == nullptr || n < 1) return SGAP_ERR_ARG;
-    if (aux->long_threshold < 0) return SGAP_OK;
-    if (aux->d_long_rows == nullptr || aux->d_long_count == nullptr || aux->d_long_acc == nullptr)
-        return SGAP_ERR_ARG;
-    if (num_rows > INT_MAX - 1) return SGAP_ERR_SHAPE;
-    cudaStream_t st = as_stream(stream);
-    if (num_rows == 0) {
-        return cudaMemsetAsync(aux->d_long_count, 0, sizeof(int32_t), st) == cudaSuccess
-                   ? SGAP_OK : SGAP_ERR_CUDA;
-    }
-    size_t need = sgap_long_rows_tmp_bytes(num_rows);
-    if (d_tmp == nullptr || tmp_bytes < need) return SGAP_ERR_ARG;
-    LongRowPred pred{d_row_ptr, aux->long_threshold, aux->long_chunk};
-    if (cub::DeviceSelect::If(d_tmp, tmp_bytes, thrust::counting_iterator<int>(0),
-                              aux->d_long_rows, aux->d_long_count, (int)num_rows, pred, st) !=
-        cudaSuccess)
-        return SGAP_ERR_CUDA;
-    if (aux->d_long_slot != nullptr) {
-        long long cap = aux->long_capacity;
-        unsigned blocks = (unsigned)ceil_div(cap > 0 ? cap : 1, kHwBlock);
-        if (blocks > 4096) blocks = 4096;
-        k_long_slots<<<blocks, kHwBlock, 0, st>>>(aux->d_long_rows, aux->d_long_count,
-                                                  aux->d_long_slot);
-    }
-    const size_t acc_bytes = (size_t)aux->long_capacity * (size_t)n * sizeof(double);
-    if (acc_bytes && cudaMemsetAsync(aux->d_long_acc, 0, acc_bytes, st) != cudaSuccess)
-        return SGAP_ERR_CUDA;
-    return launch_status();
-}
-
 int sgap_row_ids(const int32_t *d_row_ptr, int64_t num_rows, int64_t nnz,
                  int64_t long_threshold, int64_t long_chunk, int32_t *d_rowid, void *stream) {
     if (long_chunk < 0) return SGAP_ERR_ARG;
@@ -596,59 +734,157 @@ int sgap_row_ids(const int32_t *d_row_ptr, int64_t num_rows, int64_t nnz,
     return launch_status();
 }
 
-int sgap_run(const sgap_kernel_t *k, const sgap_csr_t *a, const void *d_b, void *d_c,
-             int32_t dtype, int32_t accumulate, const sgap_aux_t *aux,
-             unsigned long long *d_writebacks, void *stream) {
-    if (k == nullptr || a == nullptr) return SGAP_ERR_ARG;
-    if (dtype != SGAP_F32 && dtype != SGAP_F64) return SGAP_ERR_PRECISION;
-    if (k->n < 1 || k->c < 1 || k->n % k->c) return SGAP_ERR_CONFIG;
-    // kernels are compiled with __launch_bounds__(256)
-    if (k->hw_block != 0 && (k->hw_block < 32 || k->hw_block > 256 || k->hw_block % 32))
-        return SGAP_ERR_ARG;
+int sgap_plan_workspace_bytes(const sgap_kernel_t *k, const sgap_csr_t *a, int32_t dtype,
+                              uint32_t flags, size_t *bytes) {
+    if (bytes == nullptr) return SGAP_ERR_ARG;
+    const int st = check_kernel_csr(k, a, dtype);
+    if (st != SGAP_OK) return st;
+    PlanLayout L;
+    plan_layout(*k, *a, dtype, flags, L);
+    *bytes = L.total;
+    return SGAP_OK;
+}
+
+int sgap_validate_csr(const sgap_csr_t *a, void *d_scratch, int64_t *fault_pos, void *stream) {
+    if (a == nullptr || d_scratch == nullptr) return SGAP_ERR_ARG;
     if (a->num_rows < 0 || a->num_cols < 0 || a->nnz < 0) return SGAP_ERR_SHAPE;
     if (a->num_rows > INT_MAX - 1 || a->nnz > INT_MAX) return SGAP_ERR_SHAPE;
-    const size_t esz = dtype == SGAP_F32 ? 4 : 8;
-    const long long out_elems = a->num_rows * (long long)k->n;
+    if (a->d_row_ptr == nullptr || (a->nnz > 0 && a->d_col_idx == nullptr)) return SGAP_ERR_ARG;
+    if (fault_pos) *fault_pos = 0;
     cudaStream_t st = as_stream(stream);
-    if (out_elems == 0) return SGAP_OK;
-    if (d_c == nullptr || a->d_row_ptr == nullptr) return SGAP_ERR_ARG;
-    if (a->nnz > 0 && (d_b == nullptr || a->d_col_idx == nullptr || a->d_vals == nullptr))
-        return SGAP_ERR_ARG;
-    const size_t vec_bytes = esz * (size_t)(k->c == 4 && esz == 8 ? 2 : k->c);
-    if ((d_b && !aligned(d_b, vec_bytes)) || !aligned(d_c, vec_bytes)) return SGAP_ERR_ARG;
-    const bool eb = k->family == SGAP_NNZ_ONE || k->family == SGAP_NNZ_MULTIPLE;
-    const int32_t *rowid = aux ? aux->d_rowid : nullptr;
-    if (eb && k->grid_size > 0 && a->nnz > 0 && rowid == nullptr) return SGAP_ERR_ARG;
-    if (k->family == SGAP_NNZ_MULTIPLE && (k->g < 1 || k->chunk % k->g)) return SGAP_ERR_CONFIG;
-    LongRows lr{nullptr, nullptr, nullptr, -1, nullptr, 0, nullptr, 0};
-    const bool has_exact = aux != nullptr && aux->has_exact_rows != 0;
-    // exact-flagged chunks are skipped by the main walk: their pass needs the list
-    if (has_exact && k->family == SGAP_NNZ_MULTIPLE && dtype == SGAP_F32 &&
-        aux->long_threshold >= 0 && (aux->d_exact_rows == nullptr || aux->exact_count <= 0))
-        return SGAP_ERR_ARG;
-    if (eb && aux && aux->long_threshold >= 0 && dtype == SGAP_F32) {
-        if (aux->d_long_rows == nullptr || aux->d_long_count == nullptr || aux->d_long_acc == nullptr)
-            return SGAP_ERR_ARG;
-        lr = LongRows{aux->d_long_rows, aux->d_long_count, aux->d_long_acc, aux->long_threshold,
-                      aux->d_long_slot, aux->long_chunk, aux->d_exact_rows, aux->exact_count};
-    }
-    if (k->family == SGAP_NNZ_ONE && !accumulate) {
-        // atomic-writeback families accumulate into C: zero-fill (counts as
-        // part of the SpMM, SURVEY 8(d)); nnz-multiple zero-fills only the
-        // rows it cannot store outright (k_zero_shared_rows).
-        if (cudaMemsetAsync(d_c, 0, (size_t)out_elems * esz, st) != cudaSuccess)
+    auto *f = static_cast<unsigned long long *>(d_scratch);
+    unsigned long long h = 0;
+    auto read = [&]() -> int {
+        if (cudaGetLastError() != cudaSuccess) return SGAP_ERR_CUDA;
+        if (cudaMemcpyAsync(&h, f, sizeof(h), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
             return SGAP_ERR_CUDA;
-    }
-    if (eb && k->grid_size == 0) {
-        if (k->family == SGAP_NNZ_MULTIPLE && !accumulate)  // every row is empty
-            return cudaMemsetAsync(d_c, 0, (size_t)out_elems * esz, st) == cudaSuccess ? SGAP_OK
-                                                                                    : SGAP_ERR_CUDA;
         return SGAP_OK;
+    };
+    if (cudaMemsetAsync(f, 0xff, sizeof(*f), st) != cudaSuccess) return SGAP_ERR_CUDA;
+    k_validate_row_ptr<<<(unsigned)ceil_div(a->num_rows + 1 < 1048576 ? a->num_rows + 1 : 1048576, 256),
+                         256, 0, st>>>(a->d_row_ptr, a->num_rows, a->nnz, f);
+    int s0 = read();
+    if (s0 != SGAP_OK) return s0;
+    if (h != ~0ULL) {
+        if (fault_pos) *fault_pos = -(int64_t)h - 1;
+        return SGAP_ERR_FAULT;
     }
-    if (dtype == SGAP_F32)
-        return run_typed<float>(*k, *a, d_b, d_c, accumulate, rowid, lr, has_exact, d_writebacks,
-                                st);
-    return run_typed<double>(*k, *a, d_b, d_c, accumulate, rowid, lr, has_exact, d_writebacks, st);
+    if (a->nnz == 0) return SGAP_OK;
+    if (cudaMemsetAsync(f, 0xff, sizeof(*f), st) != cudaSuccess) return SGAP_ERR_CUDA;
+    k_validate_cols<<<(unsigned)ceil_div(a->nnz < 4194304 ? a->nnz : 4194304, 256), 256, 0, st>>>(
+        a->d_row_ptr, a->d_col_idx, (int)a->num_rows, a->num_cols, a->nnz, f);
+    s0 = read();
+    if (s0 != SGAP_OK) return s0;
+    if (h != ~0ULL) {
+        if (fault_pos) *fault_pos = (int64_t)h;
+        return SGAP_ERR_FAULT;
+    }
+    return SGAP_OK;
+}
+
+int sgap_plan(const sgap_kernel_t *k, const sgap_csr_t *a, int32_t dtype, uint32_t flags,
+              void *d_ws, size_t ws_bytes, sgap_plan_t *plan, void *stream) {
+    if (plan == nullptr) return SGAP_ERR_ARG;
+    int st0 = check_kernel_csr(k, a, dtype);
+    if (st0 != SGAP_OK) return st0;
+    if (a->num_rows > 0 && a->d_row_ptr == nullptr) return SGAP_ERR_ARG;
+    if (a->nnz > 0 && a->d_col_idx == nullptr) return SGAP_ERR_ARG;
+    PlanLayout L;
+    plan_layout(*k, *a, dtype, flags, L);
+    if (d_ws == nullptr || ws_bytes < L.total || !aligned(d_ws, 256)) return SGAP_ERR_ARG;
+    cudaStream_t st = as_stream(stream);
+    char *ws = static_cast<char *>(d_ws);
+    if (flags & SGAP_PLAN_VALIDATE) {
+        int64_t pos = 0;
+        const int v = sgap_validate_csr(a, ws + L.stats, &pos, stream);
+        if (v != SGAP_OK) return v;
+    }
+    std::memset(plan, 0, sizeof(*plan));
+    plan->abi = kPlanMagicAbi;
+    plan->dtype = dtype;
+    plan->kernel = *k;
+    plan->num_rows = a->num_rows;
+    plan->num_cols = a->num_cols;
+    plan->nnz = a->nnz;
+    plan->d_row_ptr = a->d_row_ptr;
+    plan->d_col_idx = a->d_col_idx;
+    plan->d_workspace = d_ws;
+    plan->workspace_bytes = ws_bytes;
+    sgap_aux_t &aux = plan->aux;
+    aux.long_threshold = -1;
+    const bool eb = k->family == SGAP_NNZ_ONE || k->family == SGAP_NNZ_MULTIPLE;
+    const long long M = a->num_rows, nnz = a->nnz;
+    // row statistics (one read-back): longest row, table rows, error-free rows
+    auto *stats = reinterpret_cast<unsigned long long *>(ws + L.stats);
+    unsigned long long h[4] = {0, 0, 0, 0};
+    if (cudaMemsetAsync(stats, 0, 4 * sizeof(unsigned long long), st) != cudaSuccess)
+        return SGAP_ERR_CUDA;
+    if (M > 0) {
+        k_row_stats<<<grid_for(ceil_div(M, 32), kHwBlock), kHwBlock, 0, st>>>(
+            a->d_row_ptr, (int)M, L.thr, L.chunk, L.thr >= 0 ? L.exact_cut : LLONG_MAX, stats);
+        if (cudaGetLastError() != cudaSuccess) return SGAP_ERR_CUDA;
+    }
+    if (eb && k->grid_size > 0) {
+        const int s1 = sgap_block_starts(a->d_row_ptr, M, k->chunk, k->grid_size,
+                                         reinterpret_cast<int32_t *>(ws + L.starts), stream);
+        if (s1 != SGAP_OK) return s1;
+        aux.d_block_starts = reinterpret_cast<const int32_t *>(ws + L.starts);
+    }
+    if (cudaMemcpyAsync(h, stats, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return SGAP_ERR_CUDA;
+    plan->longest_row = (int64_t)h[0];
+    if (!eb) return SGAP_OK;
+    long long thr = L.thr;
+    if (thr >= 0 && (long long)h[0] <= thr && L.chunk == 0) thr = -1;  // no table needed
+    int32_t *rowid = reinterpret_cast<int32_t *>(ws + L.rowid);
+    const int s2 = sgap_row_ids(a->d_row_ptr, M, nnz, thr, thr >= 0 ? L.chunk : 0, rowid, stream);
+    if (s2 != SGAP_OK) return s2;
+    aux.d_rowid = rowid;
+    if (thr < 0) return SGAP_OK;
+    aux.long_threshold = thr;
+    aux.long_chunk = L.chunk;
+    aux.long_capacity = L.cap;
+    aux.d_long_slot = reinterpret_cast<int32_t *>(ws + L.slot);
+    aux.d_long_rows = reinterpret_cast<int32_t *>(ws + L.rows);
+    aux.d_long_count = reinterpret_cast<int32_t *>(ws + L.count);
+    aux.d_long_acc = reinterpret_cast<double *>(ws + L.acc);
+    plan->table_rows = (int64_t)h[1];
+    // zero only the rows the table will hold (prepare_long_rows clears cap x n)
+    const long long saved_cap = aux.long_capacity;
+    aux.long_capacity = (long long)h[1] < saved_cap ? (long long)h[1] : saved_cap;
+    const int s3 = prepare_long_rows(a->d_row_ptr, M, k->n, &aux, ws + L.tmp, L.tmp_bytes, stream);
+    aux.long_capacity = saved_cap;
+    if (s3 != SGAP_OK) return s3;
+    if (k->family == SGAP_NNZ_MULTIPLE && h[2] > 0) {
+        int32_t *ex = reinterpret_cast<int32_t *>(ws + L.exact);
+        LongerThan pred{a->d_row_ptr, L.exact_cut};
+        size_t tb = L.tmp_bytes;
+        // the count lands in the stats slot 3 (unused by the runs)
+        if (cub::DeviceSelect::If(ws + L.tmp, tb, thrust::counting_iterator<int>(0), ex,
+                                  reinterpret_cast<int *>(stats + 3), (int)M, pred, st) !=
+            cudaSuccess)
+            return SGAP_ERR_CUDA;
+        aux.d_exact_rows = ex;
+        aux.exact_count = (int32_t)h[2];
+        aux.has_exact_rows = 1;
+    }
+    return launch_status();
+}
+
+int sgap_run(const sgap_plan_t *plan, const sgap_csr_t *a, const void *d_b, void *d_c,
+             int32_t accumulate, unsigned long long *d_writebacks, void *stream) {
+    if (plan == nullptr || a == nullptr) return SGAP_ERR_ARG;
+    if (plan->abi != kPlanMagicAbi) return SGAP_ERR_ARG;  // not a plan from sgap_plan
+    // the plan is bound to one sparsity structure: values may change, the
+    // structure may not
+    if (a->num_rows != plan->num_rows || a->num_cols != plan->num_cols || a->nnz != plan->nnz ||
+        a->d_row_ptr != plan->d_row_ptr || a->d_col_idx != plan->d_col_idx)
+        return SGAP_ERR_SHAPE;
+    return run_impl(&plan->kernel, a, d_b, d_c, plan->dtype, accumulate, &plan->aux,
+                    d_writebacks, stream);
 }
 
 int sgap_reference_spmm_f64(const sgap_csr_t *a, const void *d_b, int32_t n, int32_t dtype,

@@ -328,9 +328,12 @@ k_row_reciprocal(const int *__restrict__ rp, const int *__restrict__ ci,
     const unsigned lane = lane_id();
     const int j = (int)(lane % G);
     unsigned long long nwb = 0;
-    for (IT item = (IT)((blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5);
-         item < items; item += (IT)((gridDim.x * (unsigned long long)blockDim.x) >> 5)) {
-        const IT grp = item * GPW + lane / G;
+    // the grid-stride counter stays 64-bit: with IT = unsigned, item + stride
+    // can pass 2^32 when M*N is near it (one group per warp, ~M*N warps
+    // launched) and a wrapped counter would revisit other warps' cells
+    for (unsigned long long item = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
+         item < (unsigned long long)items; item += (gridDim.x * (unsigned long long)blockDim.x) >> 5) {
+        const IT grp = (IT)item * GPW + lane / G;
         const IT io0 = grp * V;
         const bool ok = io0 < cells;
         const IT i = ok ? (n_shift >= 0 ? io0 >> n_shift : io0 / (IT)N) : 0;
@@ -968,7 +971,6 @@ k_nnz_multiple_exact(const int *__restrict__ rowid, const int *__restrict__ ci,
     const int nwarps = (int)(blockDim.x >> 5);
     const long long per_chunk = ((long long)g + 31) >> 5;
     const GlobalA<T> A{rowid, ci, av};
-    unsigned long long unused = 0;
     pdl_launch_dependents();  // the main walk (no data dependency) may start now
     // exactly the rows k_row_ids flagged exact (host-compacted list; the grid
     // is sized to it -- iterating the whole table launched ~65k mostly idle
@@ -1011,7 +1013,6 @@ k_nnz_multiple_exact(const int *__restrict__ rowid, const int *__restrict__ ci,
             flush_row<T, V>(C, N, r | kLongFlag, kcol, tot, lr);  // the float64 table
         }
     }
-    (void)unused;
 }
 
 // ---------------------------------------------------------------------------
@@ -1357,7 +1358,10 @@ k_zero_shared_rows(const int *__restrict__ rp, int M, int N, long long g, long l
             const int src = __ffs(mask) - 1;
             mask &= mask - 1;
             T *row = C + (item * 32 + src) * (long long)N;
-            if ((N * sizeof(T)) % 16 == 0) {
+            // 16-byte stores only when every row is 16-byte aligned (row
+            // stride a multiple of 16 and C itself aligned: a C-ABI caller
+            // may pass a 4- or 8-byte aligned buffer)
+            if ((N * sizeof(T)) % 16 == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0) {
                 float4 *r4 = reinterpret_cast<float4 *>(row);
                 const int n4 = (int)(N * sizeof(T) / 16);
                 for (int x = lane; x < n4; x += 32) r4[x] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1379,6 +1383,79 @@ struct LongRowPred {
         return chunk > 0 && e > s && s / chunk != (e - 1) / chunk;
     }
 };
+
+// Plan-time row statistics (sgap_plan): out[0] = longest row, out[1] = rows
+// the float64 table takes (longer than thr, or straddling a `chunk`
+// boundary), out[2] = rows of the error-free pass (longer than exact_cut).
+// One warp reduction and three atomics per warp.
+__global__ void __launch_bounds__(256)
+k_row_stats(const int *__restrict__ rp, int M, long long thr, long long chunk,
+            long long exact_cut, unsigned long long *__restrict__ out) {
+    const long long items = ((long long)M + 31) >> 5;
+    const unsigned lane = lane_id();
+    unsigned long long longest = 0, tab = 0, ex = 0;
+    SGAP_WARP_LOOP(item, items) {
+        const long long r = item * 32 + lane;
+        if (r < M) {
+            const long long s = __ldg(rp + r), e = __ldg(rp + r + 1);
+            const long long len = e - s;
+            longest = len > (long long)longest ? (unsigned long long)len : longest;
+            const bool split = chunk > 0 && len > 0 && s / chunk != (e - 1) / chunk;
+            tab += (thr >= 0 && (len > thr || split)) ? 1 : 0;
+            ex += len > exact_cut ? 1 : 0;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long l2 = __shfl_xor_sync(kFull, longest, o);
+        longest = l2 > longest ? l2 : longest;
+        tab += __shfl_xor_sync(kFull, tab, o);
+        ex += __shfl_xor_sync(kFull, ex, o);
+    }
+    if (lane == 0) {
+        atomicMax(out, longest);
+        if (tab) atomicAdd(out + 1, tab);
+        if (ex) atomicAdd(out + 2, ex);
+    }
+}
+
+// CsrMatrix invariants (matrices.py:58-75), pass 1: row_ptr.  *fault = the
+// smallest row_ptr index r that breaks row_ptr[0] == 0, row_ptr[r] <=
+// row_ptr[r+1] or row_ptr[M] == nnz (atomicMin; ULLONG_MAX = none).
+__global__ void __launch_bounds__(256)
+k_validate_row_ptr(const int *__restrict__ rp, long long M, long long nnz,
+                   unsigned long long *__restrict__ fault) {
+    for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r <= M;
+         r += (long long)gridDim.x * blockDim.x) {
+        const long long v = __ldg(rp + r);
+        bool bad = (r == 0 && v != 0) || (r == M && v != nnz) || v < 0 || v > nnz;
+        if (r < M && __ldg(rp + r + 1) < v) bad = true;
+        if (bad) atomicMin(fault, (unsigned long long)r);
+    }
+}
+
+// Pass 2 (row_ptr already valid): every column in [0, K) and strictly
+// increasing within its row.  *fault = the smallest offending position.
+__global__ void __launch_bounds__(256)
+k_validate_cols(const int *__restrict__ rp, const int *__restrict__ ci, int M, long long K,
+                long long nnz, unsigned long long *__restrict__ fault) {
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < nnz;
+         p += (long long)gridDim.x * blockDim.x) {
+        const int c = __ldg(ci + p);
+        bool bad = c < 0 || (long long)c >= K;
+        if (!bad && p + 1 < nnz) {
+            // end of p's row: the first row_ptr entry above p
+            int lo = 0, hi = M;
+            while (lo < hi) {
+                const int mid = (int)(((unsigned)lo + (unsigned)hi) >> 1);
+                if ((long long)__ldg(rp + mid + 1) <= p) lo = mid + 1; else hi = mid;
+            }
+            const long long end = __ldg(rp + lo + 1);
+            if (p + 1 < end && __ldg(ci + p + 1) <= c) bad = true;
+        }
+        if (bad) atomicMin(fault, (unsigned long long)p);
+    }
+}
 
 // Row -> slot map of the table (only the table's rows are written).
 __global__ void k_long_slots(const int *__restrict__ rows, const int *__restrict__ count,

@@ -21,6 +21,7 @@ from . import _native
 from .lowering import LoweredKernel
 
 __all__ = ["DeviceCsr", "KernelAux", "kernel_struct", "device_block_starts", "prepare_aux", "spmm",
+           "plan_workspace_bytes", "validate_csr",
            "launches_per_call", "reference_spmm_f64", "torch_dtype", "native_dtype", "require_cuda"]
 
 _INT32_MAX = 2**31 - 1
@@ -144,107 +145,106 @@ def device_block_starts(a: DeviceCsr, chunk: int, num_blocks: int, *, stream=Non
 
 @dataclass
 class KernelAux:
-    """Per-(kernel, matrix) device side data: the block-start table
-    (LoweredKernel.block_starts) and the float64 long-row table.  Built once
-    by ``prepare_aux`` and reused across calls on the same matrix."""
+    """The plan of one (kernel, matrix structure) pair: ``sgap_plan_t`` plus
+    the device workspace it points into (block starts, per-position row ids,
+    the float64 long-row table, the error-free row list), all built on the
+    device by ``sgap_plan`` (include/sgap.h).  Reused across calls on the same
+    structure; values, B and C may change between calls."""
 
-    starts: torch.Tensor | None
-    rowid: torch.Tensor | None = None
-    long_rows: torch.Tensor | None = None
-    long_count: torch.Tensor | None = None
-    long_acc: torch.Tensor | None = None
-    long_capacity: int = 0
-    long_threshold: int = -1
-    has_exact_rows: int = 0
-    long_slot: torch.Tensor | None = None
-    long_chunk: int = 0
-    exact_rows: torch.Tensor | None = None
+    plan: _native.Plan
+    workspace: torch.Tensor
+    num_rows: int
+    nnz: int
 
-    def view(self) -> _native.Aux:
-        ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
-        n_exact = int(self.exact_rows.numel()) if self.exact_rows is not None else 0
-        return _native.Aux(ptr(self.starts), ptr(self.rowid), ptr(self.long_rows),
-                           ptr(self.long_count), ptr(self.long_acc), self.long_capacity,
-                           self.long_threshold, self.has_exact_rows, ptr(self.long_slot),
-                           self.long_chunk, ptr(self.exact_rows), n_exact)
+    @property
+    def long_threshold(self) -> int:
+        return int(self.plan.aux.long_threshold)
+
+    @property
+    def long_chunk(self) -> int:
+        return int(self.plan.aux.long_chunk)
+
+    @property
+    def has_exact_rows(self) -> int:
+        return int(self.plan.aux.has_exact_rows)
+
+    @property
+    def exact_count(self) -> int:
+        return int(self.plan.aux.exact_count)
+
+    @property
+    def table_rows(self) -> int:
+        return int(self.plan.table_rows)
+
+    @property
+    def longest_row(self) -> int:
+        return int(self.plan.longest_row)
+
+    @property
+    def starts(self) -> torch.Tensor | None:
+        """LoweredKernel.block_starts as computed on the device (int32)."""
+        ptr = self.plan.aux.d_block_starts
+        if not ptr:
+            return None
+        off = ptr - self.workspace.data_ptr()
+        n = int(self.plan.kernel.grid_size) + 1
+        return self.workspace[off:off + 4 * n].view(torch.int32)
 
     def nbytes(self) -> int:
-        ts = (self.starts, self.rowid, self.long_rows, self.long_count, self.long_acc,
-              self.long_slot, self.exact_rows)
-        return sum(t.numel() * t.element_size() for t in ts if t is not None)
+        return int(self.workspace.numel())
 
 
-def prepare_aux(k: LoweredKernel, a: DeviceCsr, *, stream=None, long_rows: bool = True,
-                long_threshold: int | None = None, block_starts: bool = True,
-                split_rows: bool = False, row_ptr_host=None) -> KernelAux:
-    """Per-matrix side data of kernel ``k``: block starts and per-position row
-    ids (nnz families) and, for float32 values, the long-row table
-    (include/sgap.h: sgap_block_starts, sgap_row_ids, sgap_prepare_long_rows).
+def plan_workspace_bytes(k: LoweredKernel, a: DeviceCsr, *, split_rows: bool = False) -> int:
+    ks = kernel_struct(k)
+    view = a.view()
+    out = ctypes.c_size_t(0)
+    flags = _native.PLAN_SPLIT_ROWS if split_rows else 0
+    _native.check(_native.lib().sgap_plan_workspace_bytes(
+        ctypes.byref(ks), ctypes.byref(view), native_dtype(a.vals.dtype), flags,
+        ctypes.byref(out)), "sgap_plan_workspace_bytes")
+    return int(out.value)
+
+
+def prepare_aux(k: LoweredKernel, a: DeviceCsr, *, stream=None, split_rows: bool = False,
+                validate: bool = False, row_ptr_host=None) -> KernelAux:
+    """``sgap_plan``: the per-matrix half of ``runner.build_kernel``
+    (block_starts, lowering.py:683-696) plus the engine's side data, built on
+    the device in one workspace (one 24-byte read-back of row statistics).
 
     ``split_rows``: nnz-multiple rows that straddle a g-chunk boundary also
-    go to the float64 table (every split row summed in float64, no zero-fill
-    pre-pass).  Off by default: on config 2 its float64 flushes cost more
-    than the pre-pass they replace (0.764 vs 0.754 ms at g=512).
-
-    ``row_ptr_host``: the same row_ptr on the host (numpy); given, planning
-    never synchronises with the device (the longest-row check runs on it)."""
-    eb = k.family in ("nnz-one", "nnz-multiple")
+    go to the float64 table (no zero-fill pre-pass; measured slower on config
+    2, off by default).  ``validate``: check the CsrMatrix invariants first
+    (``sgap_validate_csr``; raises ``SimulationFault``-compatible
+    ``SgapError`` status FAULT).  ``row_ptr_host`` is accepted for
+    compatibility and unused: planning needs no host copy of the matrix."""
+    del row_ptr_host
     a.check()
-    starts = None
-    if eb and k.grid_size > 0 and block_starts:
-        starts = device_block_starts(a, k.chunk, k.grid_size, stream=stream)
-    aux = KernelAux(starts)
-    if not eb:
-        return aux
     L = _native.lib()
-    dev = a.device
-    thr = -1
-    chunk = 0
-    if long_rows:
-        ks = kernel_struct(k)
-        thr = int(L.sgap_long_row_threshold(ctypes.byref(ks), native_dtype(a.vals.dtype)))
-        if long_threshold is not None and thr >= 0:
-            thr = int(long_threshold)
-        if thr >= 0 and split_rows:
-            chunk = int(L.sgap_long_row_chunk(ctypes.byref(ks), native_dtype(a.vals.dtype)))
-    longest = 0
-    lens = None
-    if thr >= 0 and a.num_rows:  # does any row need the table?
-        if row_ptr_host is not None:
-            rph = np.asarray(row_ptr_host, dtype=np.int64)
-        else:  # plan-time copy of row_ptr
-            rph = a.row_ptr.cpu().numpy().astype(np.int64)
-        lens = rph[1:] - rph[:-1]
-        longest = int(lens.max())
-        if longest <= thr and chunk == 0:
-            thr = -1  # no long rows: no table, no fold launch
-    aux.rowid = torch.empty(max(a.nnz, 4), dtype=torch.int32, device=dev)
-    _native.check(L.sgap_row_ids(a.row_ptr.data_ptr(), a.num_rows, a.nnz, thr, chunk,
-                                 aux.rowid.data_ptr(), _stream_handle(stream)), "sgap_row_ids")
-    if thr < 0:
-        return aux
-    cap = int(L.sgap_long_row_capacity(a.nnz, thr, chunk))
-    # rows k_row_ids flags exact (longer than the table threshold and the
-    # error-free length), compacted for the error-free pass's grid
-    if lens is not None and k.family == "nnz-multiple":
-        exact = np.flatnonzero(lens > max(thr, int(L.sgap_exact_row_length()))).astype(np.int32)
-        if exact.size:
-            aux.exact_rows = torch.as_tensor(exact, device=dev)
-    aux.has_exact_rows = int(aux.exact_rows is not None)
-    aux.long_threshold = thr
-    aux.long_chunk = chunk
-    aux.long_capacity = cap
-    aux.long_slot = torch.empty(max(a.num_rows, 1), dtype=torch.int32, device=dev)
-    aux.long_rows = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
-    aux.long_count = torch.zeros(1, dtype=torch.int32, device=dev)
-    aux.long_acc = torch.empty(max(cap, 1) * k.n, dtype=torch.float64, device=dev)
-    tmp_bytes = int(L.sgap_long_rows_tmp_bytes(a.num_rows))
-    tmp = torch.empty(max(tmp_bytes, 1), dtype=torch.uint8, device=dev)
-    v = aux.view()
-    _native.check(L.sgap_prepare_long_rows(a.row_ptr.data_ptr(), a.num_rows, k.n, ctypes.byref(v),
-                                           tmp.data_ptr(), tmp_bytes, _stream_handle(stream)),
-                  "sgap_prepare_long_rows")
-    return aux
+    flags = (_native.PLAN_SPLIT_ROWS if split_rows else 0) | (_native.PLAN_VALIDATE if validate else 0)
+    ks = kernel_struct(k)
+    view = a.view()
+    nbytes = plan_workspace_bytes(k, a, split_rows=split_rows)
+    ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=a.device)
+    plan = _native.Plan()
+    _native.check(L.sgap_plan(ctypes.byref(ks), ctypes.byref(view), native_dtype(a.vals.dtype),
+                              flags, ws.data_ptr(), ws.numel(), ctypes.byref(plan),
+                              _stream_handle(stream)), "sgap_plan")
+    return KernelAux(plan, ws, a.num_rows, a.nnz)
+
+
+def validate_csr(a: DeviceCsr, *, stream=None) -> int | None:
+    """The CsrMatrix invariants on the device (matrices.py:58-75); None when
+    valid, else the first offending position (a row_ptr index r as -(r+1))."""
+    scratch = torch.empty(8, dtype=torch.uint8, device=a.device)
+    pos = ctypes.c_int64(0)
+    view = _native.Csr(a.num_rows, a.num_cols, a.nnz, a.row_ptr.data_ptr(), a.col_idx.data_ptr(),
+                       a.vals.data_ptr())
+    st = _native.lib().sgap_validate_csr(ctypes.byref(view), scratch.data_ptr(), ctypes.byref(pos),
+                                         _stream_handle(stream))
+    if st == _native.ERR_FAULT:
+        return int(pos.value)
+    _native.check(st, "sgap_validate_csr")
+    return None
 
 
 def spmm(k: LoweredKernel, a: DeviceCsr, b: torch.Tensor, c: torch.Tensor, *,
@@ -269,13 +269,19 @@ def spmm(k: LoweredKernel, a: DeviceCsr, b: torch.Tensor, c: torch.Tensor, *,
         raise ValueError("B and C must be contiguous row-major")
     if aux is None:
         aux = prepare_aux(k, a, stream=stream)
-    ks = kernel_struct(k, hw_block=hw_block, hw_variant=hw_variant)
+    ks = kernel_struct(k)
+    pk = aux.plan.kernel
+    if (pk.family, pk.n, pk.g, pk.c, pk.r, pk.chunk, pk.grid_size) != \
+            (ks.family, ks.n, ks.g, ks.c, ks.r, ks.chunk, ks.grid_size):
+        raise ValueError("the plan was built for another kernel")
+    plan = _native.Plan.from_buffer_copy(aux.plan)
+    plan.kernel.hw_block = hw_block
+    plan.kernel.hw_variant = hw_variant
     view = a.view()
-    av = aux.view()
     st = _native.lib().sgap_run(
-        ctypes.byref(ks), ctypes.byref(view), b.data_ptr(), c.data_ptr(),
-        native_dtype(a.vals.dtype), 1 if accumulate else 0, ctypes.byref(av),
-        writebacks.data_ptr() if writebacks is not None else None, _stream_handle(stream))
+        ctypes.byref(plan), ctypes.byref(view), b.data_ptr(), c.data_ptr(),
+        1 if accumulate else 0, writebacks.data_ptr() if writebacks is not None else None,
+        _stream_handle(stream))
     _native.check(st, "sgap_run")
 
 

@@ -30,7 +30,8 @@ import numpy as np
 import torch
 
 from . import _native
-from .device import DeviceCsr, native_dtype, prepare_aux, require_cuda, spmm, torch_dtype
+from .device import (DeviceCsr, native_dtype, prepare_aux, require_cuda, spmm, torch_dtype,
+                     validate_csr)
 from .lowering import LoweredKernel
 from .matrices import DenseMatrix
 from .space import parse_point
@@ -119,6 +120,13 @@ def run(kernel, a, b, c0=None, *, precision: str = "double", device=None,
         dc = torch.from_numpy(np.asarray(c0.vals, dtype=np_dt).reshape(a.num_rows, n).copy()).to(dev)
     wb = torch.zeros(1, dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream(dev)
+    # the simulator faults on an out-of-range index (sim.py:279-287) instead of
+    # reading out of bounds: the planner validates the CSR on the device first
+    fault = validate_csr(da, stream=stream)
+    if fault is not None:
+        where = f"row_ptr[{-fault - 1}]" if fault < 0 else f"position {fault}"
+        raise SimulationFault(f"malformed CSR operand at {where} (index out of range or "
+                              "invariant broken)", lane=fault)
     aux = prepare_aux(k, da, stream=stream)
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)

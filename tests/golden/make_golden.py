@@ -15,6 +15,9 @@ Fixtures:
   zoo_oracle.npz       dense_spmm_oracle outputs on the conftest matrix zoo
   sim_metrics.json     sim.run atomic_ops + max_rel_error for every templated
                        point on the zoo at n in {4, 8}, p = 256
+  sim_long.json        sim.run atomic_ops for long chunks (nnz:g with g in
+                       64..512, all walks' writeback logic) on three
+                       matrices with ~20-40k nonzeros incl. power-law rows
   group_primitives.npz exec_seg_reduce_group / exec_atomic_add_group cases
   cfg1.json            config-1 input/oracle hashes (+ simulator pins with
                        --cfg1-sim)
@@ -216,6 +219,54 @@ def make_cfg1(with_sim: bool):
     print("cfg1.json")
 
 
+def long_chunk_matrices():
+    """Three matrices with enough nonzeros for several g = 512 chunks:
+    uniform, power-law rows (hub rows span many chunks), and empty rows."""
+    out = [("random:800x800:0.05:21", random_csr(800, 800, 0.05, seed=21))]
+    rng = np.random.default_rng(22)
+    m, k = 600, 3000
+    lens = np.minimum((rng.pareto(1.2, m) * 8).astype(np.int64), 2500)
+    lens[::7] = 0
+    lens[3] = 2500
+    rp = np.concatenate([[0], np.cumsum(lens)])
+    cols = np.concatenate([np.sort(rng.choice(k, int(L), replace=False)) for L in lens if L])
+    out.append(("powerlaw:600x3000:22", CsrMatrix(m, k, rp, cols, rng.uniform(-1, 1, rp[-1]))))
+    lens = np.zeros(400, dtype=np.int64)
+    lens[50:350] = rng.integers(0, 120, 300)
+    rp = np.concatenate([[0], np.cumsum(lens)])
+    cols = np.concatenate([np.sort(rng.choice(500, int(L), replace=False)) for L in lens if L])
+    out.append(("gaps:400x500:22", CsrMatrix(400, 500, rp, cols, rng.uniform(-1, 1, rp[-1]))))
+    return out
+
+
+def make_sim_long():
+    """Writeback counts of the reference simulator for long chunks (the
+    bench's nnz:512 family member and its neighbours)."""
+    t0 = time.time()
+    rows = []
+    n = 8
+    cfg = KernelConfig(n=n, p=256)
+    for label, mat in long_chunk_matrices():
+        b = random_dense(mat.num_cols, n, seed=5)
+        for g in (64, 128, 256, 512):
+            for c in (1, 2, 4):
+                pt = parse_point(f"nnz:{g},col:{c},r:1")
+                k = build_kernel(pt, cfg, mat)
+                if k is None:
+                    continue
+                got, m = run(k, mat, b)
+                want = dense_spmm_oracle(mat, b)
+                err = float(np.max(np.abs(got.vals - want.vals) / (np.abs(want.vals) + 1)))
+                rows.append({"matrix": label, "n": n, "p": 256, "point": str(pt),
+                             "grid": k.grid_size, "block": k.block_size, "nnz": mat.nnz,
+                             "atomic_ops": m.atomic_ops, "max_rel_error": err,
+                             "row_ptr_sha": sha(mat.row_ptr), "col_idx_sha": sha(mat.col_idx),
+                             "vals_sha": sha(mat.vals)})
+                print(label, pt, k.grid_size, m.atomic_ops, f"{time.time() - t0:.0f}s", flush=True)
+    (OUT / "sim_long.json").write_text(json.dumps(rows, indent=1))
+    print("sim_long.json", len(rows), f"{time.time() - t0:.1f}s")
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg1-sim", action="store_true")
@@ -232,3 +283,5 @@ if __name__ == "__main__":
         make_cfg1(args.cfg1_sim)
     if "sim" in todo:
         make_sim_metrics()
+    if "simlong" in todo:
+        make_sim_long()

@@ -36,7 +36,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_status_strings():
     L = _native.lib()
-    assert L.sgap_abi_version() == 3
+    assert L.sgap_abi_version() == 4
     assert _native.status_string(_native.ERR_NO_TEMPLATE) == "no template covers the point"
     assert _native.status_string(99) == "unknown status"
 
@@ -51,20 +51,37 @@ def test_library_is_sm100a_only():
 def test_argument_validation_without_device():
     L = _native.lib()
     k = _native.Kernel()
-    assert L.sgap_run(None, None, None, None, 0, 0, None, None, None) == _native.ERR_ARG
+    assert L.sgap_run(None, None, None, None, 0, None, None) == _native.ERR_ARG
     assert L.sgap_long_row_threshold(None, 0) == -1
-    assert L.sgap_long_row_capacity(1000, -1, 0) == 0
-    assert L.sgap_long_row_capacity(1000, 99, 0) == 11
-    assert L.sgap_long_row_capacity(1000, 99, 100) == 21  # + one straddling row per boundary
-    assert L.sgap_long_row_chunk(None, 0) == 0
-    L.sgap_long_rows_tmp_bytes(1 << 20)  # needs a device to size CUB scratch; must not crash
     k.n, k.c = 4, 1
     a = _native.Csr()
-    assert L.sgap_run(ctypes.byref(k), ctypes.byref(a), None, None, 7, 0, None, None,
-                      None) == _native.ERR_PRECISION
-    # zero-sized output: nothing to do, no device touched
-    assert L.sgap_run(ctypes.byref(k), ctypes.byref(a), None, None, 0, 0, None, None,
-                      None) == _native.OK
+    # sgap_run takes only a plan built by sgap_plan (ABI v4): a zeroed struct is rejected
+    plan = _native.Plan()
+    assert L.sgap_run(ctypes.byref(plan), ctypes.byref(a), None, None, 0, None, None) == _native.ERR_ARG
+    # the planner: workspace sizing is host-only; bad dtype / config / shape are caught first
+    nb = ctypes.c_size_t(0)
+    assert L.sgap_plan_workspace_bytes(ctypes.byref(k), ctypes.byref(a), 7, 0,
+                                       ctypes.byref(nb)) == _native.ERR_PRECISION
+    k.family, k.g, k.chunk, k.grid_size = _native.FAMILY_IDS["nnz-multiple"], 256, 256, 4
+    a.num_rows, a.num_cols, a.nnz = 100, 100, 1000
+    assert L.sgap_plan_workspace_bytes(ctypes.byref(k), ctypes.byref(a), 0, 0,
+                                       ctypes.byref(nb)) == _native.OK
+    # block starts + row ids + stats at least; float32 adds the long-row table
+    assert nb.value >= 4 * 5 + 4 * 1000
+    nb64 = ctypes.c_size_t(0)
+    assert L.sgap_plan_workspace_bytes(ctypes.byref(k), ctypes.byref(a), 1, 0,
+                                       ctypes.byref(nb64)) == _native.OK
+    assert nb64.value < nb.value  # float64 values: no table
+    a.nnz = -1
+    assert L.sgap_plan_workspace_bytes(ctypes.byref(k), ctypes.byref(a), 0, 0,
+                                       ctypes.byref(nb)) == _native.ERR_SHAPE
+    a.nnz = 1000
+    assert L.sgap_plan(ctypes.byref(k), ctypes.byref(a), 0, 0, None, 0, ctypes.byref(plan),
+                       None) == _native.ERR_ARG  # no row_ptr / workspace
+    k.n, k.c = 6, 4
+    assert L.sgap_plan_workspace_bytes(ctypes.byref(k), ctypes.byref(a), 0, 0,
+                                       ctypes.byref(nb)) == _native.ERR_CONFIG
+    assert L.sgap_validate_csr(None, None, None, None) == _native.ERR_ARG
     assert L.sgap_block_starts(None, 4, 0, 1, None, None) == _native.ERR_ARG
     assert L.sgap_seg_reduce_group(None, None, None, 5, 4, None, 0, 0, None, None, None) == _native.ERR_ARG
     assert L.sgap_atomic_add_group(None, None, None, 8, 3, None, 0, 0, None, None, None) == _native.ERR_ARG

@@ -132,11 +132,11 @@ def test_pipelined_host_spmm_matches_single_call():
     for point, p, blocks in (("nnz:128,col:4,r:1", 256, 5), ("row:1,col:4,r:1", 256, 3),
                              ("nnz:1,col:4,r:8", 1024, 4)):
         cand = Candidate(point, p)
-        pipe = HostSpmm(a.num_rows, a.num_cols, n, h_rp,
+        pipe = HostSpmm(a.num_rows, a.num_cols, n, h_rp, h_ci,
                         lambda rows, rp: plan_for(cand, n, rows, a.num_cols, rp), blocks=blocks)
         for _ in range(3):  # back-to-back calls exercise both buffer sets
             h_c = torch.full((a.num_rows, n), float("nan")).pin_memory()
-            pipe(h_rp, h_ci, h_v, h_b, h_c)
+            pipe(h_v, h_b, h_c)
             pipe.wait()
             torch.cuda.synchronize()
             assert oracle.max_rel_error(h_c.numpy(), want) <= TOL, point
