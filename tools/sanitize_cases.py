@@ -1,0 +1,94 @@
+"""Small-matrix cases for compute-sanitizer (memcheck / racecheck / synccheck /
+initcheck): every family and every hardware walk of libsgap.so, the planner
+and validation kernels, and the group primitives, each once on a matrix that
+exercises hub rows (the float64 table, the error-free pass), empty rows and
+ragged tails.  Checks results against the oracle so a sanitizer run is also
+a parity run.
+
+    compute-sanitizer --tool memcheck --error-exitcode 9 python tools/sanitize_cases.py
+"""
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import oracle  # noqa: E402
+from paper_2209_02882_b200.device import DeviceCsr, prepare_aux, spmm, validate_csr  # noqa: E402
+from paper_2209_02882_b200.lowering import KernelConfig, lower  # noqa: E402
+from paper_2209_02882_b200.sim import exec_atomic_add_group, exec_seg_reduce_group  # noqa: E402
+from paper_2209_02882_b200.space import parse_point  # noqa: E402
+from paper_2209_02882_b200.templates import algorithm_template  # noqa: E402
+
+
+class _Rp:
+    def __init__(self, m, k, rp):
+        self.num_rows, self.num_cols, self.row_ptr = m, k, rp
+
+
+def matrix(seed=3):
+    rng = np.random.default_rng(seed)
+    m, k = 300, 6000
+    lens = rng.integers(0, 40, m)
+    lens[::11] = 0
+    lens[7] = 5000   # > kExactRow: the error-free pass / float64 products
+    lens[40] = 900   # long row: the float64 table
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    cols = np.concatenate([np.sort(rng.choice(k, int(L), replace=False)) for L in lens if L])
+    vals = rng.uniform(-1, 1, rp[-1])
+    return m, k, rp, cols, vals
+
+
+def main():
+    dev = torch.device("cuda", 0)
+    m, k, rp, cols, vals = matrix()
+    a = DeviceCsr(m, k, torch.from_numpy(rp.astype(np.int32)).to(dev),
+                  torch.from_numpy(cols.astype(np.int32)).to(dev),
+                  torch.from_numpy(vals.astype(np.float32)).to(dev))
+    assert validate_csr(a) is None
+    cases = [
+        ("nnz:64,col:4,r:1", 256, 1), ("nnz:64,col:4,r:1", 256, 2), ("nnz:256,col:4,r:1", 1024, 3),
+        ("nnz:256,col:4,r:1", 1024, 4), ("nnz:6,col:1,r:1", 256, 1), ("nnz:512,col:4,r:1", 256, 1),
+        ("nnz:1,col:4,r:8", 1024, 0), ("nnz:1,col:4,r:1", 256, 0), ("nnz:1,col:1,r:32", 1024, 0),
+        ("row:1,col:4,r:1", 256, 0), ("row:4,col:4,r:1", 256, 2), ("row:4,col:4,r:1", 256, 3),
+        ("row:4,col:4,r:1", 256, 4), ("row:1/8,col:4,r:8", 256, 0), ("row:1/32,col:1,r:32", 256, 0),
+    ]
+    for n in (128, 40):
+        b = torch.rand((k, n), device=dev) * 2 - 1
+        for prec in (torch.float32, torch.float64):
+            aa = DeviceCsr(m, k, a.row_ptr, a.col_idx, a.vals.to(prec))
+            bb = b.to(prec)
+            want = oracle.spmm_f64(rp.astype(np.int32), cols.astype(np.int32),
+                                   aa.vals.cpu().numpy(), bb.cpu().numpy(), n)
+            c = torch.empty((m, n), dtype=prec, device=dev)
+            for text, p, variant in cases:
+                tpl = algorithm_template(parse_point(text), KernelConfig(n=n, p=p))
+                if tpl is None:
+                    continue
+                if variant in (3, 4) and (n // tpl.c) != 32 and text.startswith("row"):
+                    continue
+                if variant in (3, 4) and (n // tpl.c) < 32:
+                    continue
+                kk = lower(tpl, _Rp(m, k, rp), compute_starts=False)
+                aux = prepare_aux(kk, aa, validate=True)
+                for acc in (False, True):
+                    c.zero_() if acc else c.fill_(float("nan"))
+                    spmm(kk, aa, bb, c, aux=aux, accumulate=acc, hw_variant=variant)
+                    err = oracle.max_rel_error(c.cpu().numpy(), want)
+                    tol = 1e-5 if prec == torch.float32 else 1e-12
+                    assert err <= tol, (text, variant, n, prec, acc, err)
+            print("n", n, "ok")
+    # group primitives
+    out = np.zeros(16)
+    assert exec_seg_reduce_group(np.array([5, 5, 7, 7]), np.array([1.0, 2, 3, 4]), out, group_size=4) == 2
+    out = np.zeros(8)
+    assert exec_atomic_add_group(np.array([3, 3, 3, 3]), np.ones(4), out, group_size=4) == 1
+    torch.cuda.synchronize()
+    print("sanitize cases ok")
+
+
+if __name__ == "__main__":
+    main()
