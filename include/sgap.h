@@ -25,6 +25,8 @@
  *                         SimulationFault on an out-of-  sim.py:279-287
  *                         range index
  *   sgap_run              sim.run                        sim.py:431-487
+ *   sgap_run_rbpr_grid    the dgSPARSE RB+PR kernel under one cell of
+ *                         space.enumerate_fine_grained   space.py:294-348
  *   sgap_seg_reduce_group sim.exec_seg_reduce_group      sim.py:139-165
  *   sgap_atomic_add_group sim.exec_atomic_add_group      sim.py:112-136
  *
@@ -264,6 +266,20 @@ int sgap_validate_csr(const sgap_csr_t *a, void *d_scratch, int64_t *fault_pos, 
  *   Launch-only: no allocation, no host synchronisation.                     */
 int sgap_run(const sgap_plan_t *plan, const sgap_csr_t *a, const void *d_b, void *d_c,
              int32_t accumulate, unsigned long long *d_writebacks, void *stream);
+
+/* The dgSPARSE RB+PR+RM kernel under the paper's fine-grained tuning knobs
+ * (one cell of space.enumerate_fine_grained,
+ * space.py:294-348): groupSz = the plan's g (row:1/g,col:c,r:g, coarsenSz =
+ * c), blockSz = block (32..1024), tileSz = tile (a power of two >= g),
+ * workerDimR = worker_scale x num_rows row workers.  Same reduction and
+ * numerics as sgap_run on the plan (one G-lane group sum per row x column
+ * vector, exclusive store); only the thread/block mapping differs.
+ * blockDim.x = max(1, min(N, tile)/c) * g, blockDim.y = max(block,
+ * 2 blockDim.x) / blockDim.x (<= 1024 threads).  The plan must be of the
+ * row-reciprocal family.                                                    */
+int sgap_run_rbpr_grid(const sgap_plan_t *plan, const sgap_csr_t *a, const void *d_b, void *d_c,
+                       int32_t block, int32_t tile, double worker_scale, int32_t accumulate,
+                       unsigned long long *d_writebacks, void *stream);
 
 /* The dense reference product that runner.verify_point checks against
  * (runner.py:193-194 -> matrices.dense_spmm_oracle, matrices.py:241-254),

@@ -48,6 +48,7 @@ EXPORTED = (
     "sgap_plan",
     "sgap_validate_csr",
     "sgap_run",
+    "sgap_run_rbpr_grid",
     "sgap_reference_spmm_f64",
     "sgap_seg_reduce_group",
     "sgap_atomic_add_group",
@@ -192,6 +193,9 @@ def lib():
     L.sgap_validate_csr.restype = ctypes.c_int
     L.sgap_run.argtypes = [ctypes.POINTER(Plan), ctypes.POINTER(Csr), vp, vp, i32, vp, vp]
     L.sgap_run.restype = ctypes.c_int
+    L.sgap_run_rbpr_grid.argtypes = [ctypes.POINTER(Plan), ctypes.POINTER(Csr), vp, vp, i32, i32,
+                                     ctypes.c_double, i32, vp, vp]
+    L.sgap_run_rbpr_grid.restype = ctypes.c_int
     L.sgap_reference_spmm_f64.argtypes = [ctypes.POINTER(Csr), vp, i32, i32, vp, vp]
     L.sgap_reference_spmm_f64.restype = ctypes.c_int
     L.sgap_mm_line_flags.argtypes = [vp, i64, vp, vp, vp]

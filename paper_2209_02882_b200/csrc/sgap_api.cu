@@ -583,6 +583,63 @@ int check_kernel_csr(const sgap_kernel_t *k, const sgap_csr_t *a, int32_t dtype)
 
 constexpr int32_t kPlanMagicAbi = SGAP_ABI_VERSION;
 
+
+// ------------------------------------------------------ dgSPARSE RB+PR grid
+
+template <typename T, int V, int G>
+int launch_rbpr_grid(const sgap_csr_t &a, const T *B, T *C, int n, int block, int tile,
+                     double worker_scale, int acc, unsigned long long *wb, cudaStream_t st) {
+    // blockDim.x = min(N, tile)/coarsen * groupSz (>= one vector), blockDim.y =
+    // max(blockSz, 2 blockDim.x)/blockDim.x rows, capped at 1024 threads
+    const int cols = n < tile ? n : tile;
+    int vecs = cols / V;
+    if (vecs < 1) vecs = 1;
+    const int tile_cols = vecs * V;
+    const int bx = vecs * G;
+    if (bx > 1024) return SGAP_ERR_CONFIG;
+    int threads = block > 2 * bx ? block : 2 * bx;
+    if (threads > 1024) threads = 1024;
+    int by = threads / bx;
+    if (by < 1) by = 1;
+    // workerDimR = worker_scale x M row workers -> blocks along the rows
+    long long workers = (long long)(worker_scale * (double)a.num_rows + 0.5);
+    if (workers < 1) workers = 1;
+    long long gx = ceil_div(workers, by);
+    if (gx > (1LL << 31) - 1) gx = (1LL << 31) - 1;
+    const long long gy = ceil_div(n, tile_cols);
+    if (gy > 65535) return SGAP_ERR_CONFIG;
+    k_rbpr_grid<T, V, G><<<dim3((unsigned)gx, (unsigned)gy), dim3(bx, by), 0, st>>>(
+        a.d_row_ptr, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, (int)a.num_rows, n,
+        tile_cols, acc, wb);
+    return launch_status();
+}
+
+template <typename T, int V>
+int run_rbpr_grid_v(const sgap_csr_t &a, const T *B, T *C, int n, int group, int block, int tile,
+                    double ws, int acc, unsigned long long *wb, cudaStream_t st) {
+    switch (group) {
+        case 2: return launch_rbpr_grid<T, V, 2>(a, B, C, n, block, tile, ws, acc, wb, st);
+        case 4: return launch_rbpr_grid<T, V, 4>(a, B, C, n, block, tile, ws, acc, wb, st);
+        case 8: return launch_rbpr_grid<T, V, 8>(a, B, C, n, block, tile, ws, acc, wb, st);
+        case 16: return launch_rbpr_grid<T, V, 16>(a, B, C, n, block, tile, ws, acc, wb, st);
+        case 32: return launch_rbpr_grid<T, V, 32>(a, B, C, n, block, tile, ws, acc, wb, st);
+        default: return SGAP_ERR_NO_TEMPLATE;
+    }
+}
+
+template <typename T>
+int run_rbpr_grid(const sgap_csr_t &a, const void *b, void *c, int n, int coarsen, int group,
+                  int block, int tile, double ws, int acc, unsigned long long *wb, cudaStream_t st) {
+    const T *B = static_cast<const T *>(b);
+    T *C = static_cast<T *>(c);
+    switch (coarsen) {
+        case 1: return run_rbpr_grid_v<T, 1>(a, B, C, n, group, block, tile, ws, acc, wb, st);
+        case 2: return run_rbpr_grid_v<T, 2>(a, B, C, n, group, block, tile, ws, acc, wb, st);
+        case 4: return run_rbpr_grid_v<T, 4>(a, B, C, n, group, block, tile, ws, acc, wb, st);
+        default: return SGAP_ERR_NO_TEMPLATE;
+    }
+}
+
 }  // namespace
 
 extern "C" {
@@ -885,6 +942,34 @@ int sgap_run(const sgap_plan_t *plan, const sgap_csr_t *a, const void *d_b, void
         return SGAP_ERR_SHAPE;
     return run_impl(&plan->kernel, a, d_b, d_c, plan->dtype, accumulate, &plan->aux,
                     d_writebacks, stream);
+}
+
+int sgap_run_rbpr_grid(const sgap_plan_t *plan, const sgap_csr_t *a, const void *d_b, void *d_c,
+                       int32_t block, int32_t tile, double worker_scale, int32_t accumulate,
+                       unsigned long long *d_writebacks, void *stream) {
+    if (plan == nullptr || a == nullptr) return SGAP_ERR_ARG;
+    if (plan->abi != kPlanMagicAbi) return SGAP_ERR_ARG;
+    const sgap_kernel_t &k = plan->kernel;
+    if (k.family != SGAP_ROW_RECIPROCAL) return SGAP_ERR_ARG;
+    if (a->num_rows != plan->num_rows || a->num_cols != plan->num_cols || a->nnz != plan->nnz ||
+        a->d_row_ptr != plan->d_row_ptr || a->d_col_idx != plan->d_col_idx)
+        return SGAP_ERR_SHAPE;
+    if (block < 32 || block > 1024 || block % 32 || tile < k.g || (tile & (tile - 1)) ||
+        !(worker_scale > 0.0))
+        return SGAP_ERR_CONFIG;
+    const long long out_elems = a->num_rows * (long long)k.n;
+    if (out_elems == 0) return SGAP_OK;
+    const size_t esz = plan->dtype == SGAP_F32 ? 4 : 8;
+    const size_t vec_bytes = esz * (size_t)(k.c == 4 && esz == 8 ? 2 : k.c);
+    if (d_c == nullptr || (a->nnz > 0 && (d_b == nullptr || a->d_vals == nullptr)))
+        return SGAP_ERR_ARG;
+    if ((d_b && !aligned(d_b, vec_bytes)) || !aligned(d_c, vec_bytes)) return SGAP_ERR_ARG;
+    cudaStream_t st = as_stream(stream);
+    if (plan->dtype == SGAP_F32)
+        return run_rbpr_grid<float>(*a, d_b, d_c, k.n, k.c, k.g, block, tile, worker_scale,
+                                    accumulate, d_writebacks, st);
+    return run_rbpr_grid<double>(*a, d_b, d_c, k.n, k.c, k.g, block, tile, worker_scale,
+                                 accumulate, d_writebacks, st);
 }
 
 int sgap_reference_spmm_f64(const sgap_csr_t *a, const void *d_b, int32_t n, int32_t dtype,

@@ -11,7 +11,13 @@ namespace sgap {
 
 constexpr unsigned kFull = 0xffffffffu;
 
-__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+// The hardware lane (%laneid): equal to threadIdx.x & 31 for 1-D blocks,
+// and still right for the 2-D blocks of k_rbpr_grid.
+__device__ __forceinline__ unsigned lane_id() {
+    unsigned l;
+    asm("mov.u32 %0, %%laneid;" : "=r"(l));
+    return l;
+}
 
 // ---------------------------------------------------------------------------
 // c-wide column vectors (c in {1,2,4}); the per-lane unit of a B-row gather and

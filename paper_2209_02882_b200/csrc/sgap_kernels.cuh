@@ -313,6 +313,102 @@ k_row_staged(const int *__restrict__ rp, const int *__restrict__ ci, const T *__
 // Rows longer than 32G: each lane folds its partial into float64 every 32
 // strided terms (shorter rows need no float64: <= 32 terms per lane).
 // ===========================================================================
+// One row x one c-wide column vector, reduced by a group of G lanes: lane j
+// accumulates positions beg+j, beg+j+G, ...; the xor-shuffle tree leaves the
+// group sum in every lane of the group.  Rows of <= 32G nonzeros (<= 32
+// terms per lane) sum in the value type, longer ones fold into float64 after
+// each 32G-position segment, hub rows (> kExactRow) take float64 products.
+// Every lane of the warp must call it (the shuffles use the full mask).
+template <typename T, int V, int G, typename IT>
+__device__ __forceinline__ Vec<T, V> rr_group_dot(const int *__restrict__ ci,
+                                                  const T *__restrict__ av,
+                                                  const T *__restrict__ bk, IT N, int beg,
+                                                  int end, int j) {
+    Vec<T, V> acc[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) acc[u].zero();
+    Vec<double, V> tot;
+    tot.zero();
+    // rows of <= 32G nonzeros (one segment: <= 32 terms per lane) sum in
+    // the value type; longer ones fold into float64 after each segment
+    const bool multi = end - beg > 32 * G;
+    if (sizeof(T) == 4 && end - beg > kExactRow) {
+        // hub rows: float64 products (exact) summed in float64 (float32
+        // product rounding grows like sqrt(row length): config 3 measured
+        // 1.2e-5 without), kBatch gathers in flight
+        int p = beg + j;
+        for (; p + (kBatch - 1) * G < end; p += kBatch * G) {
+            int cc[kBatch];
+            T vv[kBatch];
+            Vec<T, V> bv[kBatch];
+#pragma unroll
+            for (int u = 0; u < kBatch; ++u) {
+                cc[u] = __ldg(ci + p + u * G);
+                vv[u] = __ldg(av + p + u * G);
+            }
+#pragma unroll
+            for (int u = 0; u < kBatch; ++u) ldg_vec<T, V>(bv[u], bk + (IT)cc[u] * (IT)N);
+#pragma unroll
+            for (int u = 0; u < kBatch; ++u)
+#pragma unroll
+                for (int x = 0; x < V; ++x)
+                    tot.v[x] = fma((double)vv[u], (double)bv[u].v[x], tot.v[x]);
+        }
+        for (; p < end; p += G) {
+            Vec<T, V> bv;
+            ldg_vec<T, V>(bv, bk + (IT)__ldg(ci + p) * (IT)N);
+            const double a = (double)__ldg(av + p);
+#pragma unroll
+            for (int x = 0; x < V; ++x) tot.v[x] = fma(a, (double)bv.v[x], tot.v[x]);
+        }
+    } else if (V == 1 && !multi) {
+        // one scalar column, <= 32 terms per lane: the plain strided loop
+        for (int p = beg + j; p < end; p += G)
+            acc[0].v[0] = fma(__ldg(av + p), __ldg(bk + (IT)__ldg(ci + p) * (IT)N), acc[0].v[0]);
+    } else {
+        for (int seg = beg + j; seg < end; seg += 32 * G) {
+            const int seg_end = min(seg + 32 * G, end);
+            int p = seg;
+            for (; p + (kBatch - 1) * G < seg_end; p += kBatch * G) {
+                int cc[kBatch];
+                T vv[kBatch];
+                Vec<T, V> bv[kBatch];
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) {
+                    cc[u] = __ldg(ci + p + u * G);
+                    vv[u] = __ldg(av + p + u * G);
+                }
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) ldg_vec<T, V>(bv[u], bk + (IT)cc[u] * (IT)N);
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) fma_vec<T, V>(acc[u], vv[u], bv[u]);
+            }
+            for (; p < seg_end; p += G) {
+                Vec<T, V> bv;
+                ldg_vec<T, V>(bv, bk + (IT)__ldg(ci + p) * (IT)N);
+                fma_vec<T, V>(acc[0], __ldg(av + p), bv);
+            }
+            if (multi) {
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) fold<T, V>(tot, acc[u]);
+            }
+        }
+    }
+    Vec<T, V> part = acc[0];
+#pragma unroll
+    for (int u = 1; u < kBatch; ++u) add_vec<T, V>(part, acc[u]);
+    if (__any_sync(kFull, multi)) {  // long rows: the group sum in float64 too
+        Vec<double, V> td;
+#pragma unroll
+        for (int x = 0; x < V; ++x) td.v[x] = multi ? tot.v[x] : (double)part.v[x];
+        group_sum_vec<G, double, V>(td);
+        part = narrow<T, V>(td);
+    } else {
+        group_sum_vec<G, T, V>(part);
+    }
+    return part;
+}
+
 // IT: the index type of cells/groups -- unsigned 32-bit whenever M*N fits
 // (the host picks; ncu showed 2.4x the reference kernel's instruction count
 // at one cell per warp with 64-bit index math), else 64-bit.
@@ -340,91 +436,45 @@ k_row_reciprocal(const int *__restrict__ rp, const int *__restrict__ ci,
         const IT k0 = ok ? io0 - i * (IT)N : 0;
         const int beg = ok ? __ldg(rp + i) : 0;
         const int end = ok ? __ldg(rp + i + 1) : 0;
-        const T *bk = B + k0;
-        Vec<T, V> acc[kBatch];
-#pragma unroll
-        for (int u = 0; u < kBatch; ++u) acc[u].zero();
-        Vec<double, V> tot;
-        tot.zero();
-        // rows of <= 32G nonzeros (one segment: <= 32 terms per lane) sum in
-        // the value type; longer ones fold into float64 after each segment
-        const bool multi = end - beg > 32 * G;
-        if (sizeof(T) == 4 && end - beg > kExactRow) {
-            // hub rows: float64 products (exact) summed in float64 (float32
-            // product rounding grows like sqrt(row length): config 3 measured
-            // 1.2e-5 without), kBatch gathers in flight
-            int p = beg + j;
-            for (; p + (kBatch - 1) * G < end; p += kBatch * G) {
-                int cc[kBatch];
-                T vv[kBatch];
-                Vec<T, V> bv[kBatch];
-#pragma unroll
-                for (int u = 0; u < kBatch; ++u) {
-                    cc[u] = __ldg(ci + p + u * G);
-                    vv[u] = __ldg(av + p + u * G);
-                }
-#pragma unroll
-                for (int u = 0; u < kBatch; ++u) ldg_vec<T, V>(bv[u], bk + (IT)cc[u] * (IT)N);
-#pragma unroll
-                for (int u = 0; u < kBatch; ++u)
-#pragma unroll
-                    for (int x = 0; x < V; ++x)
-                        tot.v[x] = fma((double)vv[u], (double)bv[u].v[x], tot.v[x]);
-            }
-            for (; p < end; p += G) {
-                Vec<T, V> bv;
-                ldg_vec<T, V>(bv, bk + (IT)__ldg(ci + p) * (IT)N);
-                const double a = (double)__ldg(av + p);
-#pragma unroll
-                for (int x = 0; x < V; ++x) tot.v[x] = fma(a, (double)bv.v[x], tot.v[x]);
-            }
-        } else if (V == 1 && !multi) {
-            // one scalar column, <= 32 terms per lane: the plain strided loop
-            for (int p = beg + j; p < end; p += G)
-                acc[0].v[0] = fma(__ldg(av + p), __ldg(bk + (IT)__ldg(ci + p) * (IT)N), acc[0].v[0]);
-        } else {
-            for (int seg = beg + j; seg < end; seg += 32 * G) {
-                const int seg_end = min(seg + 32 * G, end);
-                int p = seg;
-                for (; p + (kBatch - 1) * G < seg_end; p += kBatch * G) {
-                    int cc[kBatch];
-                    T vv[kBatch];
-                    Vec<T, V> bv[kBatch];
-#pragma unroll
-                    for (int u = 0; u < kBatch; ++u) {
-                        cc[u] = __ldg(ci + p + u * G);
-                        vv[u] = __ldg(av + p + u * G);
-                    }
-#pragma unroll
-                    for (int u = 0; u < kBatch; ++u) ldg_vec<T, V>(bv[u], bk + (IT)cc[u] * (IT)N);
-#pragma unroll
-                    for (int u = 0; u < kBatch; ++u) fma_vec<T, V>(acc[u], vv[u], bv[u]);
-                }
-                for (; p < seg_end; p += G) {
-                    Vec<T, V> bv;
-                    ldg_vec<T, V>(bv, bk + (IT)__ldg(ci + p) * (IT)N);
-                    fma_vec<T, V>(acc[0], __ldg(av + p), bv);
-                }
-                if (multi) {
-#pragma unroll
-                    for (int u = 0; u < kBatch; ++u) fold<T, V>(tot, acc[u]);
-                }
-            }
-        }
-        Vec<T, V> part = acc[0];
-#pragma unroll
-        for (int u = 1; u < kBatch; ++u) add_vec<T, V>(part, acc[u]);
-        if (__any_sync(kFull, multi)) {  // long rows: the group sum in float64 too
-            Vec<double, V> td;
-#pragma unroll
-            for (int x = 0; x < V; ++x) td.v[x] = multi ? tot.v[x] : (double)part.v[x];
-            group_sum_vec<G, double, V>(td);
-            part = narrow<T, V>(td);
-        } else {
-            group_sum_vec<G, T, V>(part);
-        }
+        const Vec<T, V> part = rr_group_dot<T, V, G, IT>(ci, av, B + k0, (IT)N, beg, end, j);
         if (ok && j == 0) {
             store_vec<T, V>(C + i * (IT)N + k0, part, accumulate != 0);
+            nwb += V;
+        }
+    }
+    flush_count(wb, nwb);
+}
+
+// The dgSPARSE RB+PR+RM kernel with the paper's tuning knobs (PAPER.md:
+// 413-415; the cells of space.enumerate_fine_grained, space.py:294-348):
+// <groupSz = G, blockSz, tileSz, workerDimR> with coarsenSz = V.  A block
+// covers `tile` dense columns as tile/V column vectors of G lanes each
+// (blockDim.x = vectors * G) and blockDim.y rows; gridDim.y column tiles;
+// gridDim.x = the row parallelism (workerDimR / blockDim.y blocks), each
+// block row striding over the rows when that is fewer than M.  The
+// reduction per (row, vector) is the same G-lane group sum as
+// k_row_reciprocal (rr_group_dot), one exclusive store per cell.  Every lane
+// runs the same number of row rounds (shuffles need the whole warp).
+template <typename T, int V, int G>
+__global__ void __launch_bounds__(1024)
+k_rbpr_grid(const int *__restrict__ rp, const int *__restrict__ ci, const T *__restrict__ av,
+            const T *__restrict__ B, T *__restrict__ C, int M, int N, int tile_cols,
+            int accumulate, unsigned long long *wb) {
+    const int j = (int)(threadIdx.x % G);
+    const int vec = (int)(threadIdx.x / G);
+    const long long k0 = (long long)blockIdx.y * tile_cols + (long long)vec * V;
+    const bool kok = k0 < N && (long long)vec * V < tile_cols;
+    const long long stride = (long long)gridDim.x * blockDim.y;
+    unsigned long long nwb = 0;
+    for (long long base = (long long)blockIdx.x * blockDim.y; base < M; base += stride) {
+        const long long i = base + threadIdx.y;
+        const bool ok = kok && i < M;
+        const int beg = ok ? __ldg(rp + i) : 0;
+        const int end = ok ? __ldg(rp + i + 1) : 0;
+        const Vec<T, V> part = rr_group_dot<T, V, G, long long>(ci, av, B + (ok ? k0 : 0),
+                                                                (long long)N, beg, end, j);
+        if (ok && j == 0) {
+            store_vec<T, V>(C + i * (long long)N + k0, part, accumulate != 0);
             nwb += V;
         }
     }

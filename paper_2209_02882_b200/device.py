@@ -21,7 +21,7 @@ from . import _native
 from .lowering import LoweredKernel
 
 __all__ = ["DeviceCsr", "KernelAux", "kernel_struct", "device_block_starts", "prepare_aux", "spmm",
-           "plan_workspace_bytes", "validate_csr",
+           "plan_workspace_bytes", "validate_csr", "spmm_rbpr_grid",
            "launches_per_call", "reference_spmm_f64", "torch_dtype", "native_dtype", "require_cuda"]
 
 _INT32_MAX = 2**31 - 1
@@ -283,6 +283,32 @@ def spmm(k: LoweredKernel, a: DeviceCsr, b: torch.Tensor, c: torch.Tensor, *,
         1 if accumulate else 0, writebacks.data_ptr() if writebacks is not None else None,
         _stream_handle(stream))
     _native.check(st, "sgap_run")
+
+
+def spmm_rbpr_grid(k: LoweredKernel, a: DeviceCsr, b: torch.Tensor, c: torch.Tensor, *,
+                   block: int, tile: int, worker_scale: float, accumulate: bool = False,
+                   aux: KernelAux | None = None, writebacks: torch.Tensor | None = None,
+                   stream=None) -> None:
+    """The dgSPARSE RB+PR+RM kernel under one fine-grained tuning cell
+    <groupSz = k.g, blockSz, tileSz, workerDimR = worker_scale x M>
+    (space.FineGrainedConfig) for a row-reciprocal
+    kernel ``k`` (row:1/g,col:c,r:g).  Same result as ``spmm(k, ...)``."""
+    if k.family != "row-reciprocal":
+        raise ValueError("the fine-grained RB+PR grid runs row-reciprocal kernels")
+    if b.dtype != a.vals.dtype or c.dtype != a.vals.dtype:
+        raise ValueError("A, B and C must share one value dtype")
+    if tuple(b.shape) != (a.num_cols, k.n) or tuple(c.shape) != (a.num_rows, k.n):
+        raise ValueError("shape mismatch")
+    if not (b.is_contiguous() and c.is_contiguous()):
+        raise ValueError("B and C must be contiguous row-major")
+    if aux is None:
+        aux = prepare_aux(k, a, stream=stream)
+    view = a.view()
+    st = _native.lib().sgap_run_rbpr_grid(
+        ctypes.byref(aux.plan), ctypes.byref(view), b.data_ptr(), c.data_ptr(), block, tile,
+        float(worker_scale), 1 if accumulate else 0,
+        writebacks.data_ptr() if writebacks is not None else None, _stream_handle(stream))
+    _native.check(st, "sgap_run_rbpr_grid")
 
 
 def launches_per_call(k: LoweredKernel, aux: KernelAux | None, *, accumulate: bool = False,

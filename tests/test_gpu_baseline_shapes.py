@@ -231,3 +231,46 @@ def test_long_chunk_writebacks_match_simulator(variant, precision):
         assert oracle.max_rel_error(got.vals, want) <= (1e-12 if precision == "double" else TOL)
         checked += 1
     assert checked >= 30
+
+
+# --------------------------------------------------------------- dgSPARSE RB+PR grid
+
+@pytest.mark.parametrize("n", [4, 16, 40, 128])
+def test_rbpr_fine_grained_cells(n):
+    """The dgSPARSE RB+PR+RM kernel under tuning cells of
+    space.enumerate_fine_grained: 2-D blocks narrower than
+    a warp, tiles narrower than N, fewer row workers than rows (workerDimR
+    scale < 1) and idle extra workers (> 1); float32 within 1e-5 and float64
+    within 1e-12 of the oracle, one writeback per output element."""
+    from paper_2209_02882_b200.device import spmm_rbpr_grid
+    from paper_2209_02882_b200.space import enumerate_fine_grained
+    rng = np.random.default_rng(n)
+    m, k = 700, 900
+    lens = rng.integers(0, 30, m)
+    lens[5], lens[9], lens[17] = 850, 0, 880   # rows past 32G: float64 folds
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    cols = np.concatenate([np.sort(rng.choice(k, int(L), replace=False)) for L in lens if L])
+    vals = rng.uniform(-1, 1, rp[-1])
+    cells = enumerate_fine_grained(n)
+    pick = [cells[i] for i in np.random.default_rng(7).choice(len(cells), 24, replace=False)]
+    pick += [c for c in cells if (c.group_size, c.block_size, c.tile_size) == (32, 256, 32)]
+    for dt, tol in ((torch.float32, TOL), (torch.float64, 1e-12)):
+        a = DeviceCsr(m, k, torch.from_numpy(rp.astype(np.int32)).cuda(),
+                      torch.from_numpy(cols.astype(np.int32)).cuda(),
+                      torch.from_numpy(vals).to(dt).cuda())
+        b = (torch.rand((k, n), dtype=torch.float64, device="cuda") * 2 - 1).to(dt)
+        want = oracle.spmm_f64(rp.astype(np.int32), cols.astype(np.int32), a.vals.cpu().numpy(),
+                               b.cpu().numpy(), n)
+        c = torch.empty((m, n), dtype=dt, device="cuda")
+        for cell in pick:
+            text = f"row:1/{cell.group_size},col:{cell.coarsen_size},r:{cell.group_size}"
+            p = _first_p(text, n)
+            kk = lower(algorithm_template(parse_point(text), KernelConfig(n=n, p=p)),
+                       _Rp(m, k, rp), compute_starts=False)
+            wb = torch.zeros(1, dtype=torch.int64, device="cuda")
+            c.fill_(float("nan"))
+            spmm_rbpr_grid(kk, a, b, c, block=cell.block_size, tile=cell.tile_size,
+                           worker_scale=float(cell.worker_scale), writebacks=wb)
+            err = oracle.max_rel_error(c.cpu().numpy(), want)
+            assert err <= tol, (cell, dt, err)
+            assert int(wb.item()) == m * n, cell  # == row-reciprocal's atomic_ops

@@ -82,6 +82,10 @@ def merge(args):
                     and int(e.get("hw_variant", 0)) == args.hw_variant)]
     head = subprocess.run(["git", "rev-parse", "--short", "HEAD"], capture_output=True, text=True,
                           cwd=str(ROOT)).stdout.strip()
+    if not head:  # the GPU box has no .git: identify the build by the library hash
+        import hashlib
+        lib = ROOT / "paper_2209_02882_b200" / "libsgap.so"
+        head = "libsgap.so sha256 " + hashlib.sha256(lib.read_bytes()).hexdigest()[:12]
     ents.append({"workload": key, "point": args.point, "hw_variant": args.hw_variant,
                  "kernel": kernel, "dram_bytes": int(dram),
                  "gpu_time_ms": get("gpu__time_duration.sum") / (1e6 if units[
