@@ -501,6 +501,13 @@ def main():
     roof["b_gather_bytes"] = a.nnz * n * 4  # every nonzero gathers a whole B row through L2
     roof["b_gather_tbs"] = roof["b_gather_bytes"] / (kernel_ms * 1e-3) / 1e12
 
+    # ---- the optional collectives around the shard-parallel SpMM:
+    # B replication (NCCL broadcast over NVLink) and the C gather to rank 0
+    # (ncclSend/ncclRecv of unequal row slabs) -- set-up and epilogue, timed
+    # separately, never inside ``value``
+    collectives = None
+    if world > 1 and os.environ.get("SGAP_BENCH_SHARE_GPU") != "1":
+        collectives = time_collectives(b, c, plan, rank, dev, stream)
     # ---- end to end through host buffers
     e2e = None
     if not args.no_e2e:
@@ -541,7 +548,7 @@ def main():
                          "exact_rows": aux.exact_count, "workspace_bytes": aux.nbytes()},
                 "stats": stats.as_dict(),
             },
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "collectives": collectives,
             "gpu_launches": args.steps * launches_per_call(k, aux, hw_variant=choice.hw_variant),
             "clocks": clk.summary(),
         }
@@ -552,6 +559,37 @@ def main():
                                                     "heuristic": heur.label()}, indent=1))
     if world > 1:
         dist.destroy_process_group()
+
+
+def time_collectives(b, c, plan, rank, dev, stream):
+    """B broadcast from rank 0 and the C row-slab gather to rank 0 over the
+    process group (NCCL on the GPU box), CUDA events, max over ranks."""
+    import torch.distributed as dist
+    from paper_2209_02882_b200.parallel import broadcast_dense, gather_rows
+
+    def timed(fn):
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        out = fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()), out
+
+    timed(lambda: broadcast_dense(b, src=0))  # warm the communicator
+    t_bc, _ = timed(lambda: broadcast_dense(b, src=0))
+    t_ga, full = timed(lambda: gather_rows(c, plan, root=0))
+    del full
+    bb = b.numel() * b.element_size()
+    cb = int(plan.starts[-1]) * c.shape[1] * c.element_size()
+    return {"broadcast_b_ms": t_bc, "broadcast_b_bytes": bb,
+            "broadcast_b_gbs": bb / (t_bc * 1e-3) / 1e9,
+            "gather_c_ms": t_ga, "gather_c_bytes": cb, "gather_c_gbs": cb / (t_ga * 1e-3) / 1e9,
+            "backend": dist.get_backend(),
+            "note": "set-up (B replica) and optional epilogue (C on rank 0); not part of value"}
 
 
 def measure_e2e(args, a, b, c, k, choice, plan_for, n, total_nnz, world, dev, stream):

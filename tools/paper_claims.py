@@ -27,11 +27,21 @@ from paper_2209_02882_b200.space import parse_point  # noqa: E402
 from paper_2209_02882_b200.templates import algorithm_template  # noqa: E402
 
 
-def matrices(dev):
-    yield "config1 uniform 4096^2 1%", G.config_matrix(1, device=dev)
-    yield "rmat scale 18 ef 16", G.rmat(18, 16, seed=1, device=dev)
-    yield "stencil27 64^3", G.stencil27(64, device=dev)
-    yield "chung-lu 100k x ~10M", G.chung_lu(100_000, 1e7, seed=1, device=dev)
+MATRICES = {
+    "cfg1": ("config1 uniform 4096^2 1%", lambda dev: G.config_matrix(1, device=dev)),
+    "rmat18": ("rmat scale 18 ef 16", lambda dev: G.rmat(18, 16, seed=1, device=dev)),
+    "stencil64": ("stencil27 64^3", lambda dev: G.stencil27(64, device=dev)),
+    "chunglu": ("chung-lu 100k x ~10M", lambda dev: G.chung_lu(100_000, 1e7, seed=1, device=dev)),
+    "cfg2": ("config2 R-MAT scale 20", lambda dev: G.config_matrix(2, device=dev)),
+    "cfg3": ("config3 Reddit-shaped", lambda dev: G.config_matrix(3, device=dev)),
+    "cfg4": ("config4 stencil27 160^3", lambda dev: G.config_matrix(4, device=dev)),
+}
+
+
+def matrices(dev, keys):
+    for k in keys:
+        label, make = MATRICES[k]
+        yield label, make(dev)
 
 
 def best_of(a, b, c, n, pts, rp):
@@ -49,11 +59,12 @@ def best_of(a, b, c, n, pts, rp):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", default="4,8")
+    ap.add_argument("--matrices", default="cfg1,rmat18,stencil64,chunglu")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     out = []
-    for label, g in matrices(dev):
+    for label, g in matrices(dev, args.matrices.split(",")):
         a = DeviceCsr(g.num_rows, g.num_cols, g.row_ptr.to(torch.int32), g.col_idx.to(torch.int32),
                       g.vals.to(torch.float32))
         rp = a.row_ptr.cpu().numpy().astype(np.int64)
