@@ -104,7 +104,10 @@ typedef struct {
     int32_t hw_block;       /* CTA size override: 0 = auto (256; 128 for the
                                register EB walk), else a warp multiple in
                                [32, 256]                                    */
-    int32_t hw_variant;     /* nnz-multiple walk: 0 auto, 1 register-staged,
+    int32_t hw_variant;     /* nnz-multiple walk: 0 auto, 1 register-staged
+                               (row_ptr tracking when the plan has chunk
+                               start rows), 5 register-staged on per-position
+                               row ids,
                                2 TMA-staged (cp.async.bulk + mbarrier ring),
                                3/4 lane-staged (warp per chunk, 4/8 B-row
                                gathers in flight; needs N/c >= 32).
@@ -180,6 +183,11 @@ typedef struct {
                                      sgap_exact_row_length()) nonzeros: the
                                      error-free pass walks exactly these    */
     int32_t exact_count;          /* their number (host-known: sizes the grid) */
+    const int32_t *d_chunk_rows;  /* nnz-multiple, g % 4 == 0: [chunks + 1] row
+                                     owning each g-chunk's first position
+                                     (compute_block_starts at chunk g); the
+                                     register walk then tracks rows through
+                                     row_ptr instead of reading d_rowid     */
 } sgap_aux_t;
 
 /* Per-position row ids (what the reference lowering recovers per lane with

@@ -123,6 +123,7 @@ class Aux(ctypes.Structure):
         ("long_chunk", ctypes.c_int64),
         ("d_exact_rows", ctypes.c_void_p),
         ("exact_count", ctypes.c_int32),
+        ("d_chunk_rows", ctypes.c_void_p),
     ]
 
 

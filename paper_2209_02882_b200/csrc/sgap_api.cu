@@ -192,7 +192,7 @@ template <typename T, int V, int W, int U, int STAGES = 3, int MINB = 3>
 int launch_nnz_multiple(bool tma, int tile, int owner, const sgap_kernel_t &k,
                         const sgap_csr_t &a, const T *B, T *C, const int *rowid,
                         const LongRows &lr, unsigned long long *wb, cudaStream_t st, bool pdl,
-                        int exact_inline) {
+                        int exact_inline, const int *chunk_rows) {
     const long long total_pos = k.grid_size * k.chunk;
     if (tma) {
         const size_t smem = tma_smem_bytes<T, STAGES>();
@@ -216,9 +216,15 @@ int launch_nnz_multiple(bool tma, int tile, int owner, const sgap_kernel_t &k,
     const int blk = k.hw_block > 0 ? k.hw_block : kEbWalkBlock;
     const int vec4 = (k.g % 4 == 0) && aligned(rowid, 16) && aligned(a.d_col_idx, 16) &&
                      aligned(a.d_vals, 16);
-    return launch_k(k_nnz_multiple<T, V, W, U>, dim3(grid_for(items, blk)), dim3(blk), 0, st,
+    if (vec4 && chunk_rows != nullptr)  // row_ptr tracking, no per-position row ids
+        return launch_k(k_nnz_multiple<T, V, W, U, true>, dim3(grid_for(items, blk)), dim3(blk), 0,
+                        st, pdl, rowid, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C,
+                        a.d_row_ptr, (int)a.num_rows, k.n, a.nnz, k.g, total_pos, vec4, owner, lr,
+                        wb, exact_inline, chunk_rows);
+    return launch_k(k_nnz_multiple<T, V, W, U, false>, dim3(grid_for(items, blk)), dim3(blk), 0, st,
                     pdl, rowid, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, a.d_row_ptr,
-                    (int)a.num_rows, k.n, a.nnz, k.g, total_pos, vec4, owner, lr, wb, exact_inline);
+                    (int)a.num_rows, k.n, a.nnz, k.g, total_pos, vec4, owner, lr, wb, exact_inline,
+                    (const int *)nullptr);
 }
 
 // hw_variant: 0 auto; 1 register walk; 2 TMA-staged walk; 3/4 lane-staged walk
@@ -240,15 +246,16 @@ int run_nnz_multiple_w(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, 
     // (g <= 128, >= 16 lanes per chunk: config 2, Chung-Lu N=64); the register
     // walk for long chunks (fewer, longer walks amortise the A loads it issues
     // itself) and for narrow N (profiles/r01_selector_regret.json)
-    const int variant = k.hw_variant == 0 ? ((tma_ok && W >= 16 && k.g <= 128) ? 2 : 1) : k.hw_variant;
+    int variant = k.hw_variant == 0 ? ((tma_ok && W >= 16 && k.g <= 128) ? 2 : 1) : k.hw_variant;
     const bool tma = variant == 2;
     // every check that can reject the call runs before the first launch: an
     // error after the exact pass would leave its sums in the float64 table
     // (never folded, so a later call on the same plan would add them to C)
     if (tma && !tma_ok) return SGAP_ERR_ARG;
-    if (variant < 1 || variant > 4) return SGAP_ERR_ARG;
-    if (variant >= 3 && W != 32) return SGAP_ERR_ARG;  // the staged walk takes a whole warp
-    if (variant >= 3 && k.hw_block > 0 && k.hw_block != kHwBlock) return SGAP_ERR_ARG;
+    if (variant < 1 || variant > 5) return SGAP_ERR_ARG;
+    const bool staged = variant == 3 || variant == 4;
+    if (staged && W != 32) return SGAP_ERR_ARG;  // the staged walk takes a whole warp
+    if (staged && k.hw_block > 0 && k.hw_block != kHwBlock) return SGAP_ERR_ARG;
     if (tma) {
         const size_t smem = tma_smem_bytes<T, 3>();
         if (cudaFuncSetAttribute(k_nnz_multiple_tma<T, V, W, 4, 3, 3>,
@@ -266,7 +273,7 @@ int run_nnz_multiple_w(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, 
     bool pdl = false;
     // the register walk (variant 1) takes exact chunks inline (float64
     // products); the other walks leave them to k_nnz_multiple_exact
-    const bool exact_inline = variant == 1 && lr.threshold >= 0 && sizeof(T) == 4;
+    const bool exact_inline = (variant == 1 || variant == 5) && lr.threshold >= 0 && sizeof(T) == 4;
     if (!exact_inline && lr.threshold >= 0 && sizeof(T) == 4 && has_exact && lr.exact_count > 0 &&
         lr.exact_rows != nullptr) {
         const int vec4 = (k.g % 4 == 0) && aligned(rowid, 16) && aligned(a.d_col_idx, 16) &&
@@ -281,7 +288,7 @@ int run_nnz_multiple_w(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, 
         if (s0 != SGAP_OK) return s0;
         pdl = true;
     }
-    if (variant >= 3) {
+    if (variant == 3 || variant == 4) {
         const long long total_pos = k.grid_size * k.chunk;
         const long long chunks = total_pos / k.g;
         const int blk = kHwBlock;
@@ -294,8 +301,11 @@ int run_nnz_multiple_w(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, 
                         a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, a.d_row_ptr,
                         (int)a.num_rows, k.n, a.nnz, k.g, total_pos, owner, lr, wb);
     }
+    // variant 1 tracks rows through row_ptr when the plan has the chunk start
+    // rows; variant 5 is the same walk on per-position row ids
     return launch_nnz_multiple<T, V, W, 4>(tma, tile, owner, k, a, B, C, rowid, lr, wb, st,
-                                                   pdl, exact_inline ? 1 : 0);
+                                           pdl, exact_inline ? 1 : 0,
+                                           variant == 1 ? lr.chunk_rows : nullptr);
 }
 
 template <typename T, int V>
@@ -477,7 +487,7 @@ static int run_impl(const sgap_kernel_t *k, const sgap_csr_t *a, const void *d_b
     const int32_t *rowid = aux ? aux->d_rowid : nullptr;
     if (eb && k->grid_size > 0 && a->nnz > 0 && rowid == nullptr) return SGAP_ERR_ARG;
     if (k->family == SGAP_NNZ_MULTIPLE && (k->g < 1 || k->chunk % k->g)) return SGAP_ERR_CONFIG;
-    LongRows lr{nullptr, nullptr, nullptr, -1, nullptr, 0, nullptr, 0};
+    LongRows lr{nullptr, nullptr, nullptr, -1, nullptr, 0, nullptr, 0, nullptr};
     const bool has_exact = aux != nullptr && aux->has_exact_rows != 0;
     // exact-flagged chunks are skipped by the main walk: their pass needs the list
     if (has_exact && k->family == SGAP_NNZ_MULTIPLE && dtype == SGAP_F32 &&
@@ -487,8 +497,10 @@ static int run_impl(const sgap_kernel_t *k, const sgap_csr_t *a, const void *d_b
         if (aux->d_long_rows == nullptr || aux->d_long_count == nullptr || aux->d_long_acc == nullptr)
             return SGAP_ERR_ARG;
         lr = LongRows{aux->d_long_rows, aux->d_long_count, aux->d_long_acc, aux->long_threshold,
-                      aux->d_long_slot, aux->long_chunk, aux->d_exact_rows, aux->exact_count};
+                      aux->d_long_slot, aux->long_chunk, aux->d_exact_rows, aux->exact_count,
+                      nullptr};
     }
+    if (k->family == SGAP_NNZ_MULTIPLE && aux != nullptr) lr.chunk_rows = aux->d_chunk_rows;
     if (k->family == SGAP_NNZ_ONE && !accumulate) {
         // atomic-writeback families accumulate into C: zero-fill (counts as
         // part of the SpMM); nnz-multiple zero-fills only the
@@ -523,7 +535,7 @@ struct LongerThan {
 // Workspace layout of a plan (every region 256-byte aligned).
 struct PlanLayout {
     size_t starts = 0, rowid = 0, slot = 0, rows = 0, count = 0, acc = 0, exact = 0, stats = 0,
-           tmp = 0, total = 0;
+           tmp = 0, chunk_rows = 0, total = 0;
     long long thr = -1, chunk = 0, cap = 0, exact_cap = 0, exact_cut = 0;
     size_t tmp_bytes = 0;
 };
@@ -544,6 +556,8 @@ int plan_layout(const sgap_kernel_t &k, const sgap_csr_t &a, int32_t dtype, uint
     if (eb) {
         L.starts = take((size_t)(k.grid_size + 1) * sizeof(int));
         L.rowid = take((size_t)(nnz > 4 ? nnz : 4) * sizeof(int));
+        if (k.family == SGAP_NNZ_MULTIPLE && k.g % 4 == 0 && k.g > 0)
+            L.chunk_rows = take((size_t)(k.grid_size * (k.chunk / k.g) + 1) * sizeof(int));
         L.thr = sgap_long_row_threshold(&k, dtype);
         L.chunk = (L.thr >= 0 && (flags & SGAP_PLAN_SPLIT_ROWS)) ? long_row_chunk(&k, dtype) : 0;
         if (L.thr >= 0) {
@@ -887,6 +901,13 @@ int sgap_plan(const sgap_kernel_t *k, const sgap_csr_t *a, int32_t dtype, uint32
                                          reinterpret_cast<int32_t *>(ws + L.starts), stream);
         if (s1 != SGAP_OK) return s1;
         aux.d_block_starts = reinterpret_cast<const int32_t *>(ws + L.starts);
+    }
+    if (L.chunk_rows && k->grid_size > 0) {  // the row owning each g-chunk's first position
+        const long long chunks = k->grid_size * (k->chunk / k->g);
+        const int s4 = sgap_block_starts(a->d_row_ptr, M, k->g, chunks,
+                                         reinterpret_cast<int32_t *>(ws + L.chunk_rows), stream);
+        if (s4 != SGAP_OK) return s4;
+        aux.d_chunk_rows = reinterpret_cast<const int32_t *>(ws + L.chunk_rows);
     }
     if (cudaMemcpyAsync(h, stats, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st) !=
             cudaSuccess ||

@@ -231,6 +231,8 @@ struct LongRows {
     long long chunk;      // > 0: every row straddling a `chunk` boundary is in the table
     const int *exact_rows;  // rows taking the error-free pass (nnz-multiple)
     int exact_count;
+    const int *chunk_rows;  // row owning each g-chunk's first position (register
+                            // walk without row ids); nullptr: use the row ids
 };
 
 // Row ids carry bit 31 when the row belongs to the long-row table and bit 30

@@ -624,12 +624,25 @@ struct GlobalA {
         ldg_vec<T, 4>(v, av + u);
         // (evict-first A loads, __ldcs: 0.833 vs 0.700 ms on config 2)
     }
+    // (col, val) only: the row_ptr-tracking walk needs no per-position row ids
+    template <typename I>
+    __device__ __forceinline__ void load4cv(I q, int4 &c, Vec<T, 4> &v) const {
+        const unsigned u = (unsigned)q;
+        c = __ldg(reinterpret_cast<const int4 *>(ci + u));
+        ldg_vec<T, 4>(v, av + u);
+    }
     // pull the A lines `ahead` positions further into L1 (one per 32 positions)
     template <typename I>
     __device__ __forceinline__ void prefetch(I q) const {
         const unsigned u = (unsigned)q;
         prefetch_l1(ci + u);
         prefetch_l1(rowid + u);
+        prefetch_l1(av + u);
+    }
+    template <typename I>
+    __device__ __forceinline__ void prefetch_cv(I q) const {
+        const unsigned u = (unsigned)q;
+        prefetch_l1(ci + u);
         prefetch_l1(av + u);
     }
 };
@@ -797,6 +810,114 @@ __device__ __forceinline__ void eb_walk4(const ASrc &A, long long q0, long long 
     if (own.on && own.end == own.nnz) zero_rows<T, V>(C, N, kcol, (cur & kRowMask) + 1, own.m);
 }
 
+// The same vectorised walk without per-position row ids (hw variant 1 when
+// the plan carries the g-chunk start rows): the row is tracked from row_ptr
+// as the reference lowering does (lowering.py:490-500) -- the chunk's first
+// row comes from a per-chunk start table (compute_block_starts at chunk g),
+// `ce` is the current row's end and a batch of 4 positions stays in the row
+// iff q + 3 < ce.  A row change walks row_ptr forward (empty rows passed are
+// zeroed in owner mode); the table / error-free flags of a row follow from
+// its length, so the A stream is 8 bytes per position instead of 12.
+__device__ __forceinline__ int row_flags(int cur, unsigned cs, unsigned ce, const LongRows &lr) {
+    if (lr.threshold < 0) return cur;
+    const long long len = (long long)ce - (long long)cs;
+    const bool is_long = len > lr.threshold;
+    const bool split = lr.chunk > 0 && len > 0 &&
+                       (long long)cs / lr.chunk != ((long long)ce - 1) / lr.chunk;
+    return cur | ((is_long || split) ? kLongFlag : 0) | ((is_long && len > kExactRow) ? kExactFlag : 0);
+}
+
+template <typename T, int V>
+__device__ __forceinline__ void zero_gap_before_rp(T *__restrict__ C, int N, long long kcol,
+                                                   const int *__restrict__ rp, int cur,
+                                                   unsigned base) {
+    // empty rows right before `cur` all start (and end) at the chunk base
+    Vec<T, V> z;
+    z.zero();
+    for (int r = cur - 1; r >= 0 && (unsigned)__ldg(rp + r) == base; --r)
+        store_vec<T, V>(C + (long long)r * N + kcol, z, false);
+}
+
+template <typename T, int V>
+__device__ __forceinline__ void eb_walk4_rp(const GlobalA<T> &A, const int *__restrict__ rp,
+                                            int cur, long long q0, long long qend,
+                                            const T *__restrict__ B, int N, long long kcol,
+                                            T *__restrict__ C, const LongRows &lr,
+                                            const Owner &own, unsigned long long &nwb) {
+    unsigned cs = (unsigned)__ldg(rp + cur), ce = (unsigned)__ldg(rp + cur + 1);
+    bool here = own.on && cs == (unsigned)own.base;
+    if (here) zero_gap_before_rp<T, V>(C, N, kcol, rp, cur, (unsigned)own.base);
+    Vec<T, V> acc;
+    acc.zero();
+    Vec<double, V> tot;
+    tot.zero();
+    const T *bk = B + kcol;
+    unsigned q = (unsigned)q0;
+    const unsigned qe = (unsigned)qend;
+    // close the current row and move to the row holding position p
+    auto advance = [&](unsigned p) {
+        fold<T, V>(tot, acc);
+        flush_owned<T, V>(C, N, row_flags(cur, cs, ce, lr), kcol, tot, lr, here);
+        nwb += V;
+        tot.zero();
+        do {
+            ++cur;
+            cs = ce;
+            ce = (unsigned)__ldg(rp + cur + 1);
+            if (own.on && ce <= p) {  // an empty row passed over
+                Vec<T, V> z;
+                z.zero();
+                store_vec<T, V>(C + (long long)cur * N + kcol, z, false);
+            }
+        } while (ce <= p);
+        here = own.on;
+    };
+    auto batch4 = [&](unsigned qq) {
+        int4 c;
+        Vec<T, 4> v;
+        A.load4cv(qq, c, v);
+        Vec<T, V> b0, b1, b2, b3;
+        ldg_vec<T, V>(b0, row_ptr(bk, c.x, N));
+        ldg_vec<T, V>(b1, row_ptr(bk, c.y, N));
+        ldg_vec<T, V>(b2, row_ptr(bk, c.z, N));
+        ldg_vec<T, V>(b3, row_ptr(bk, c.w, N));
+        if (qq + 3 < ce) {
+            fma_vec<T, V>(acc, v.v[0], b0);
+            fma_vec<T, V>(acc, v.v[1], b1);
+            fma_vec<T, V>(acc, v.v[2], b2);
+            fma_vec<T, V>(acc, v.v[3], b3);
+        } else {
+            const Vec<T, V> *bb[4] = {&b0, &b1, &b2, &b3};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (qq + u >= ce) advance(qq + u);
+                fma_vec<T, V>(acc, v.v[u], *bb[u]);
+            }
+        }
+    };
+    for (; q + 8 <= qe; q += 8) {
+        if ((q & 31) == 0 && q + 64 < qe) A.prefetch_cv(q + 64);
+        batch4(q);
+        batch4(q + 4);
+        fold<T, V>(tot, acc);
+    }
+    if (q + 4 <= qe) {
+        batch4(q);
+        q += 4;
+    }
+    for (; q < qe; ++q) {  // < 4 tail positions
+        Vec<T, V> b;
+        ldg_vec<T, V>(b, row_ptr(bk, A.col(q), N));
+        if (q >= ce) advance(q);
+        fma_vec<T, V>(acc, A.val(q), b);
+    }
+    fold<T, V>(tot, acc);
+    const bool complete = here && ce == (unsigned)own.end;
+    flush_owned<T, V>(C, N, row_flags(cur, cs, ce, lr), kcol, tot, lr, complete);
+    nwb += V;
+    if (own.on && own.end == own.nnz) zero_rows<T, V>(C, N, kcol, cur + 1, own.m);
+}
+
 // A chunk lying entirely inside one long row (flagged in its row id): the
 // error-free accumulate (TwoProduct + TwoSum, float64 folds), no row changes.
 // Only rows flagged kExactFlag (> kExactRow nonzeros).  These chunks run in their own kernel (k_nnz_multiple_exact) so the hot walk
@@ -925,9 +1046,9 @@ __device__ __noinline__ void eb_chunk_f64(const GlobalA<T> A, long long base, lo
     unsigned q = (unsigned)base;
     const unsigned qe = (unsigned)end;
     for (; vec4 && q + 4 <= qe; q += 4) {
-        int4 c, r;
+        int4 c;
         Vec<T, 4> v;
-        A.load4(q, c, v, r);
+        A.load4cv(q, c, v);
         Vec<T, V> b0, b1, b2, b3;
         ldg_vec<T, V>(b0, row_ptr(bk, c.x, N));
         ldg_vec<T, V>(b1, row_ptr(bk, c.y, N));
@@ -951,14 +1072,19 @@ __device__ __noinline__ void eb_chunk_f64(const GlobalA<T> A, long long base, lo
     flush_row<T, V>(C, N, r_first, kcol, tot, lr);  // the float64 table
 }
 
-template <typename T, int V, int W, int U>
+template <typename T, int V, int W, int U, bool RPW = false>
 __global__ void __launch_bounds__(256, SGAP_EB_MINB)
 k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
                const T *__restrict__ av, const T *__restrict__ B, T *__restrict__ C,
                const int *__restrict__ rp, int M, int N, long long nnz, int g,
                long long total_pos, int vec4, int owner, LongRows lr, unsigned long long *wb,
-               int exact_inline) {
+               int exact_inline, const int *__restrict__ chunk_rows) {
     const bool VEC4 = vec4 != 0;  // g % 4 == 0 and 16-byte aligned A arrays
+    // row_ptr tracking (no per-position row ids) when the plan has the
+    // g-chunk start rows and the walk is vectorised
+    // (a separate instantiation, so each walk keeps its own register budget)
+    constexpr bool RP = RPW;
+    const long long exact_cut = lr.threshold > kExactRow ? lr.threshold : kExactRow;
     const int NT = N / V;
     constexpr int SG = 32 / W;
     const long long total_chunks = total_pos / g;
@@ -979,6 +1105,24 @@ k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
                 continue;
             }
             const Owner own{rp, rowid, base, end, nnz, M, owner != 0};
+            if constexpr (RP) {
+                const int cur = __ldg(chunk_rows + ch);
+                const long long kcol = (long long)tile * V;
+                const long long cs = __ldg(rp + cur), ce = __ldg(rp + cur + 1);
+                if (lr.threshold >= 0 && ce - cs > exact_cut && ce >= end) {
+                    // a chunk inside an exact-flagged (hub) row
+                    if (own.on && cs == base)
+                        zero_gap_before_rp<T, V>(C, N, kcol, rp, cur, (unsigned)base);
+                    if (own.on && end == nnz) zero_rows<T, V>(C, N, kcol, cur + 1, M);
+                    nwb += V;
+                    if (exact_inline)
+                        eb_chunk_f64<T, V>(A, base, end, B, N, kcol, C, lr,
+                                           cur | kLongFlag | kExactFlag, VEC4);
+                    continue;
+                }
+                eb_walk4_rp<T, V>(A, rp, cur, base, end, B, N, kcol, C, lr, own, nwb);
+                continue;
+            } else {
             const int r_first = A.row(base);
             if ((r_first & kExactFlag) && A.row(end - 1) == r_first) {
                 const long long kcol = (long long)tile * V;
@@ -995,6 +1139,7 @@ k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
                 eb_walk4<T, V>(A, base, end, B, N, (long long)tile * V, C, lr, own, nwb);
             else
                 eb_walk<T, V, U>(A, base, end, B, N, (long long)tile * V, C, lr, own, nwb);
+            }
         }
     }
     flush_count(wb, nwb);

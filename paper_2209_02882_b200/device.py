@@ -326,7 +326,7 @@ def launches_per_call(k: LoweredKernel, aux: KernelAux | None, *, accumulate: bo
             # k_nnz_multiple_exact (sgap_api.cu run_nnz_multiple_w)
             w = min(32, max(1, k.n // k.c))
             variant = hw_variant or (2 if (w >= 16 and k.g <= 128) else 1)
-            n += 0 if variant == 1 else 1
+            n += 0 if variant in (1, 5) else 1
     return n
 
 

@@ -230,7 +230,7 @@ def test_device_group_macros_reference_gate_and_faults():
     assert out[5] == 4.0
 
 
-@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("variant", [1, 2, 5])
 def test_nnz_multiple_walk_variants(zoo, variant):
     """Both nnz-multiple walks (register-staged, TMA-staged) on the zoo and
     config 1, including g that does not divide the TMA tile evenly."""

@@ -74,7 +74,7 @@ def test_config2_long_chunk_walks():
     variant, with and without split-row routing to the float64 table."""
     g = G.rmat(20, 16, seed=1, device="cuda")
     pts = [(t, 256, v, split) for t in ("nnz:512,col:4,r:1", "nnz:2048,col:4,r:1", "nnz:128,col:4,r:1")
-           for v in (1, 3, 4) for split in (False, True)]
+           for v in (1, 3, 4, 5) for split in (False, True)]
     pts += [("nnz:128,col:4,r:1", 256, 2, False), ("nnz:64,col:2,r:1", 1024, 3, True)]
     print(_check(g, 128, pts))
 
@@ -202,7 +202,8 @@ def test_exact_rows_and_empty_row_gaps():
     # (inline float64 chunks), TMA and lane-staged walks (k_nnz_multiple_exact
     # overlapped by programmatic dependent launch), nnz-one (float64 table
     # sums), RB walks (float64 products per row), row-reciprocal groups
-    for text, p, variant in (("nnz:512,col:4,r:1", 256, 1), ("nnz:64,col:4,r:1", 1024, 2),
+    for text, p, variant in (("nnz:512,col:4,r:1", 256, 1), ("nnz:512,col:4,r:1", 256, 5),
+                             ("nnz:64,col:4,r:1", 1024, 2),
                              ("nnz:32,col:4,r:1", 256, 1), ("nnz:256,col:4,r:1", 256, 3),
                              ("nnz:1,col:4,r:8", 1024, 0), ("nnz:1,col:4,r:1", 256, 0),
                              ("row:1,col:4,r:1", 256, 0), ("row:4,col:4,r:1", 256, 2),
