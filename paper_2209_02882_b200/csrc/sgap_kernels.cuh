@@ -845,6 +845,9 @@ __device__ __forceinline__ void eb_walk4_rp(const GlobalA<T> &A, const int *__re
                                             T *__restrict__ C, const LongRows &lr,
                                             const Owner &own, unsigned long long &nwb) {
     unsigned cs = (unsigned)__ldg(rp + cur), ce = (unsigned)__ldg(rp + cur + 1);
+    // the NEXT row's end, loaded one row ahead so a row change does not wait
+    // on a dependent row_ptr load
+    unsigned cn = cur + 1 < own.m ? (unsigned)__ldg(rp + cur + 2) : ce;
     bool here = own.on && cs == (unsigned)own.base;
     if (here) zero_gap_before_rp<T, V>(C, N, kcol, rp, cur, (unsigned)own.base);
     Vec<T, V> acc;
@@ -863,7 +866,8 @@ __device__ __forceinline__ void eb_walk4_rp(const GlobalA<T> &A, const int *__re
         do {
             ++cur;
             cs = ce;
-            ce = (unsigned)__ldg(rp + cur + 1);
+            ce = cn;
+            cn = cur + 1 < own.m ? (unsigned)__ldg(rp + cur + 2) : ce;
             if (own.on && ce <= p) {  // an empty row passed over
                 Vec<T, V> z;
                 z.zero();

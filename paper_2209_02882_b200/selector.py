@@ -90,8 +90,8 @@ GPU_G_VALUES = (2, 4, 8, 16, 32, 64, 128, 256, 512)
 def candidates(n: int, p_values=(256, 1024), g_values=GPU_G_VALUES,
                variants: bool = True) -> list[Candidate]:
     """Every templated point at dense width n for each p (deduplicated by
-    the kernel it lowers to); nnz-multiple points come with both walks
-    (register-staged, TMA-staged, lane-staged) and row-multiple points with
+    the kernel it lowers to); nnz-multiple points come with every walk
+    (register-staged on row_ptr or on row ids, TMA-staged, lane-staged) and row-multiple points with
     the logical, interleaved and warp-per-row mappings when ``variants``."""
     out, seen = [], set()
     for p in p_values:
@@ -105,7 +105,10 @@ def candidates(n: int, p_values=(256, 1024), g_values=GPU_G_VALUES,
                 continue
             seen.add(key)
             if variants and tpl.family == "nnz-multiple":
-                vs = (1, 2, 3) if n // tpl.c >= 32 else (1, 2)
+                # 1: register walk tracking rows through row_ptr (DRAM-bound
+                # matrices: configs 3/5), 5: the same walk on per-position row
+                # ids (latency-bound: config 2), 2: TMA-staged, 3: lane-staged
+                vs = (1, 5, 2, 3) if n // tpl.c >= 32 else (1, 5, 2)
                 out.extend(Candidate(str(pt), p, 0, v) for v in vs)
             elif variants and tpl.family == "row-multiple" and n // tpl.c <= 256:
                 vs = (0, 2, 4) if n // tpl.c == 32 else (0, 2)

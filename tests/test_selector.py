@@ -33,9 +33,9 @@ def test_candidate_grid_covers_families_and_walks():
     fams = {algorithm_template(parse_point(c.point), KernelConfig(128, c.p)).family for c in cands}
     assert fams == {"nnz-one", "nnz-multiple", "row-multiple", "row-reciprocal"}
     assert any(c.point.startswith("nnz:512") for c in cands)
-    # register / TMA walks everywhere, the lane-staged walk where N/c >= 32
-    assert {c.hw_variant for c in cands if c.point.startswith("nnz:64,col:4")} == {1, 2, 3}
-    assert {c.hw_variant for c in candidates(32) if c.point.startswith("nnz:64,col:4")} == {1, 2}
+    # register walks (row_ptr / row ids) and TMA everywhere, lane-staged where N/c >= 32
+    assert {c.hw_variant for c in cands if c.point.startswith("nnz:64,col:4")} == {1, 5, 2, 3}
+    assert {c.hw_variant for c in candidates(32) if c.point.startswith("nnz:64,col:4")} == {1, 5, 2}
     # row-multiple: logical / interleaved, plus a warp per row where N/c == 32
     assert {c.hw_variant for c in cands if c.point.startswith("row:4,col:4")} == {0, 2, 4}
     assert {c.hw_variant for c in cands if c.point.startswith("row:4,col:2")} == {0, 2}
