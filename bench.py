@@ -498,6 +498,10 @@ def main():
         roof["traffic_info"] = tr
         if tr["bytes"]:
             roof["traffic_over_algorithmic"] = tr["bytes"] / roof["algorithmic_bytes"]
+            # the DRAM bytes that actually move, against the same measured peak:
+            # how close the walk runs to the bandwidth floor of its access order
+            roof["traffic_gbs"] = tr["bytes"] / (kernel_ms * 1e-3) / 1e9
+            roof["traffic_frac_of_peak"] = roof["traffic_gbs"] / peaks["hbm_gbs"]
     roof["b_gather_bytes"] = a.nnz * n * 4  # every nonzero gathers a whole B row through L2
     roof["b_gather_tbs"] = roof["b_gather_bytes"] / (kernel_ms * 1e-3) / 1e12
 

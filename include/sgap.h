@@ -188,6 +188,12 @@ typedef struct {
                                      (compute_block_starts at chunk g); the
                                      register walk then tracks rows through
                                      row_ptr instead of reading d_rowid     */
+    const int32_t *d_union_off[2];  /* row-multiple, N/c == 32, rows <= 64:
+                                        per 4-row [0] / 8-row [1] block, the
+                                        offset of its union column stream   */
+    const uint32_t *d_union[2];      /* (col | row mask << (32 - R)) entries:
+                                        the row-blocked walk (hw variants
+                                        6 / 7) gathers each shared B row once */
 } sgap_aux_t;
 
 /* Per-position row ids (what the reference lowering recovers per lane with

@@ -124,6 +124,10 @@ class Aux(ctypes.Structure):
         ("d_exact_rows", ctypes.c_void_p),
         ("exact_count", ctypes.c_int32),
         ("d_chunk_rows", ctypes.c_void_p),
+        ("d_union_off4", ctypes.c_void_p),
+        ("d_union_off8", ctypes.c_void_p),
+        ("d_union4", ctypes.c_void_p),
+        ("d_union8", ctypes.c_void_p),
     ]
 
 

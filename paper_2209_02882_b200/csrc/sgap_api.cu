@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <cstring>
 
+#include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 #include <cuda_runtime.h>
 #include <thrust/iterator/counting_iterator.h>
@@ -82,10 +83,29 @@ int launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStr
 // row and lane-staged A (8/4 gathers in flight; needs N/c == 32).
 template <typename T, int V>
 int run_row_multiple(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
-                     int acc, cudaStream_t st) {
+                     int acc, const LongRows &lr, cudaStream_t st) {
     const int N = k.n, L = N / V;
     const int blk = k.hw_block > 0 ? k.hw_block : kHwBlock;
     const int vec4 = aligned(a.d_col_idx, 16) && aligned(a.d_vals, 16);
+    if (k.hw_variant == 6 || k.hw_variant == 7) {  // row-blocked union walk
+        const int which = k.hw_variant - 6;
+        if (L != 32 || lr.union_e[which] == nullptr) return SGAP_ERR_ARG;
+        const int R = which ? 8 : 4;
+        const long long nblocks = ceil_div(a.num_rows, R);
+        const long long tile_blocks = (long long)(blk / 32) * k.g;
+        const long long tiles = ceil_div(nblocks, tile_blocks);
+        const unsigned ctas = (unsigned)(tiles < (1LL << 30) ? (tiles > 0 ? tiles : 1) : (1LL << 30));
+        const T *Av = static_cast<const T *>(a.d_vals);
+        if (which == 0)
+            k_row_blocked<T, V, 4, 4><<<ctas, blk, 0, st>>>(a.d_row_ptr, lr.union_e[0],
+                                                            lr.union_off[0], Av, B, C,
+                                                            (int)a.num_rows, N, k.g, acc);
+        else
+            k_row_blocked<T, V, 8, 4><<<ctas, blk, 0, st>>>(a.d_row_ptr, lr.union_e[1],
+                                                            lr.union_off[1], Av, B, C,
+                                                            (int)a.num_rows, N, k.g, acc);
+        return launch_status();
+    }
     if (k.hw_variant == 3 || k.hw_variant == 4) {  // lane-staged, a warp per row
         if (L != 32) return SGAP_ERR_ARG;
         const long long tile_rows = (long long)(blk / 32) * k.g;
@@ -336,7 +356,7 @@ int run_family(const sgap_kernel_t &k, const sgap_csr_t &a, const void *b, void 
     const T *B = static_cast<const T *>(b);
     T *C = static_cast<T *>(c);
     switch (k.family) {
-        case SGAP_ROW_MULTIPLE: return run_row_multiple<T, V>(k, a, B, C, acc, st);
+        case SGAP_ROW_MULTIPLE: return run_row_multiple<T, V>(k, a, B, C, acc, lr, st);
         case SGAP_ROW_RECIPROCAL: return run_row_reciprocal<T, V>(k, a, B, C, acc, wb, st);
         case SGAP_NNZ_ONE: return run_nnz_one<T, V>(k, a, B, C, rowid, lr, wb, st);
         case SGAP_NNZ_MULTIPLE:
@@ -487,7 +507,8 @@ static int run_impl(const sgap_kernel_t *k, const sgap_csr_t *a, const void *d_b
     const int32_t *rowid = aux ? aux->d_rowid : nullptr;
     if (eb && k->grid_size > 0 && a->nnz > 0 && rowid == nullptr) return SGAP_ERR_ARG;
     if (k->family == SGAP_NNZ_MULTIPLE && (k->g < 1 || k->chunk % k->g)) return SGAP_ERR_CONFIG;
-    LongRows lr{nullptr, nullptr, nullptr, -1, nullptr, 0, nullptr, 0, nullptr};
+    LongRows lr{nullptr, nullptr, nullptr, -1, nullptr, 0, nullptr, 0, nullptr, {nullptr, nullptr},
+                {nullptr, nullptr}};
     const bool has_exact = aux != nullptr && aux->has_exact_rows != 0;
     // exact-flagged chunks are skipped by the main walk: their pass needs the list
     if (has_exact && k->family == SGAP_NNZ_MULTIPLE && dtype == SGAP_F32 &&
@@ -498,9 +519,15 @@ static int run_impl(const sgap_kernel_t *k, const sgap_csr_t *a, const void *d_b
             return SGAP_ERR_ARG;
         lr = LongRows{aux->d_long_rows, aux->d_long_count, aux->d_long_acc, aux->long_threshold,
                       aux->d_long_slot, aux->long_chunk, aux->d_exact_rows, aux->exact_count,
-                      nullptr};
+                      nullptr, {nullptr, nullptr}, {nullptr, nullptr}};
     }
     if (k->family == SGAP_NNZ_MULTIPLE && aux != nullptr) lr.chunk_rows = aux->d_chunk_rows;
+    if (k->family == SGAP_ROW_MULTIPLE && aux != nullptr) {
+        for (int w = 0; w < 2; ++w) {
+            lr.union_e[w] = reinterpret_cast<const unsigned *>(aux->d_union[w]);
+            lr.union_off[w] = aux->d_union_off[w];
+        }
+    }
     if (k->family == SGAP_NNZ_ONE && !accumulate) {
         // atomic-writeback families accumulate into C: zero-fill (counts as
         // part of the SpMM); nnz-multiple zero-fills only the
@@ -535,7 +562,9 @@ struct LongerThan {
 // Workspace layout of a plan (every region 256-byte aligned).
 struct PlanLayout {
     size_t starts = 0, rowid = 0, slot = 0, rows = 0, count = 0, acc = 0, exact = 0, stats = 0,
-           tmp = 0, chunk_rows = 0, total = 0;
+           tmp = 0, chunk_rows = 0, union_off[2] = {0, 0}, union_e[2] = {0, 0}, union_tmp = 0,
+           total = 0;
+    size_t union_tmp_bytes = 0;
     long long thr = -1, chunk = 0, cap = 0, exact_cap = 0, exact_cut = 0;
     size_t tmp_bytes = 0;
 };
@@ -553,6 +582,20 @@ int plan_layout(const sgap_kernel_t &k, const sgap_csr_t &a, int32_t dtype, uint
         return at;
     };
     L.stats = take(4 * sizeof(unsigned long long));
+    if (k.family == SGAP_ROW_MULTIPLE && k.c > 0 && k.n / k.c == 32 && k.n % k.c == 0 && nnz > 0) {
+        for (int w = 0; w < 2; ++w) {  // 4-row and 8-row union streams (<= nnz entries each)
+            const int R = w ? 8 : 4;
+            if (a.num_cols >= (1LL << (32 - R))) continue;
+            const long long nb = ceil_div(M, R);
+            L.union_off[w] = take((size_t)(nb + 1) * sizeof(int));
+            L.union_e[w] = take((size_t)nnz * sizeof(unsigned));
+            size_t sb = 0;
+            cub::DeviceScan::ExclusiveSum(nullptr, sb, (int *)nullptr, (int *)nullptr,
+                                          (int)(nb + 1));
+            if (sb > L.union_tmp_bytes) L.union_tmp_bytes = sb;
+        }
+        if (L.union_tmp_bytes) L.union_tmp = take(L.union_tmp_bytes);
+    }
     if (eb) {
         L.starts = take((size_t)(k.grid_size + 1) * sizeof(int));
         L.rowid = take((size_t)(nnz > 4 ? nnz : 4) * sizeof(int));
@@ -914,6 +957,38 @@ int sgap_plan(const sgap_kernel_t *k, const sgap_csr_t *a, int32_t dtype, uint32
         cudaStreamSynchronize(st) != cudaSuccess)
         return SGAP_ERR_CUDA;
     plan->longest_row = (int64_t)h[0];
+    if (k->family == SGAP_ROW_MULTIPLE && h[0] <= 64) {
+        // union column streams of 4- and 8-row blocks (row-blocked walk):
+        // count per block, exclusive scan into offsets, fill
+        for (int w = 0; w < 2; ++w) {
+            if (!L.union_e[w]) continue;
+            const long long nb = ceil_div(M, w ? 8 : 4);
+            int *off = reinterpret_cast<int *>(ws + L.union_off[w]);
+            unsigned *ent = reinterpret_cast<unsigned *>(ws + L.union_e[w]);
+            const unsigned grid = grid_for(ceil_div(nb, 32), kHwBlock);
+            if (w == 0)
+                k_union_rows<4><<<grid, kHwBlock, 0, st>>>(a->d_row_ptr, a->d_col_idx, (int)M, nb,
+                                                           nullptr, off, nullptr);
+            else
+                k_union_rows<8><<<grid, kHwBlock, 0, st>>>(a->d_row_ptr, a->d_col_idx, (int)M, nb,
+                                                           nullptr, off, nullptr);
+            if (cudaGetLastError() != cudaSuccess) return SGAP_ERR_CUDA;
+            if (cudaMemsetAsync(off + nb, 0, sizeof(int), st) != cudaSuccess) return SGAP_ERR_CUDA;
+            size_t tb = L.union_tmp_bytes;
+            if (cub::DeviceScan::ExclusiveSum(ws + L.union_tmp, tb, off, off, (int)(nb + 1), st) !=
+                cudaSuccess)
+                return SGAP_ERR_CUDA;
+            if (w == 0)
+                k_union_rows<4><<<grid, kHwBlock, 0, st>>>(a->d_row_ptr, a->d_col_idx, (int)M, nb,
+                                                           off, nullptr, ent);
+            else
+                k_union_rows<8><<<grid, kHwBlock, 0, st>>>(a->d_row_ptr, a->d_col_idx, (int)M, nb,
+                                                           off, nullptr, ent);
+            if (cudaGetLastError() != cudaSuccess) return SGAP_ERR_CUDA;
+            aux.d_union_off[w] = off;
+            aux.d_union[w] = ent;
+        }
+    }
     if (!eb) return SGAP_OK;
     long long thr = L.thr;
     if (thr >= 0 && (long long)h[0] <= thr && L.chunk == 0) thr = -1;  // no table needed

@@ -4,6 +4,7 @@
 // (sim.py:112-165; declared-only in the reference's emitted CUDA, cuda.py:52-56).
 #pragma once
 
+#include <climits>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -233,6 +234,8 @@ struct LongRows {
     int exact_count;
     const int *chunk_rows;  // row owning each g-chunk's first position (register
                             // walk without row ids); nullptr: use the row ids
+    const unsigned *union_e[2];  // row-blocked RB walk: union column streams of
+    const int *union_off[2];     // 4-row [0] and 8-row [1] blocks (k_union_rows)
 };
 
 // Row ids carry bit 31 when the row belongs to the long-row table and bit 30

@@ -305,6 +305,118 @@ k_row_staged(const int *__restrict__ rp, const int *__restrict__ ci, const T *__
 }
 
 // ===========================================================================
+// Row-blocked RB walk (row-multiple hw variants 6 / 7, N/c == 32): a warp
+// owns R consecutive rows and walks the UNION of their column lists once --
+// a plan-time stream of (col | row-mask << (32 - R)) entries per R-row block,
+// built by k_union_rows -- so a B row shared by several rows of the block is
+// gathered once and feeds every row whose mask bit is set (stencils and
+// meshes: adjacent rows share 2/3 of their columns).  Each row still sums its
+// own nonzeros in ascending position order (the union is sorted, a row's
+// entries appear in its CSR order and its values are read from its own
+// position cursor), one serial sum per (row, tile) as the reference's
+// row-multiple thread does (lowering.py:573-585); rows are at most 64 long
+// (float32 sums, as rb_short_staged), which the plan checks.
+// ===========================================================================
+template <int R>
+struct UnionFmt {
+    static constexpr int kShift = 32 - R;
+    static constexpr unsigned kColMask = (1u << kShift) - 1u;
+};
+
+// Per block of R rows: the number of distinct columns (pass 0) or the
+// entries themselves (pass 1) -- an R-way merge of the sorted row lists by
+// one thread per block.
+template <int R>
+__global__ void __launch_bounds__(256)
+k_union_rows(const int *__restrict__ rp, const int *__restrict__ ci, int M, long long nblocks,
+             const int *__restrict__ off, int *__restrict__ out_count,
+             unsigned *__restrict__ out_entries) {
+    for (long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x; b < nblocks;
+         b += (long long)gridDim.x * blockDim.x) {
+        const long long i0 = b * R;
+        int p[R], e[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const bool ok = i0 + r < M;
+            p[r] = ok ? __ldg(rp + i0 + r) : 0;
+            e[r] = ok ? __ldg(rp + i0 + r + 1) : 0;
+        }
+        long long w = off ? off[b] : 0;
+        int count = 0;
+        for (;;) {
+            int best = INT_MAX;
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if (p[r] < e[r]) best = min(best, __ldg(ci + p[r]));
+            if (best == INT_MAX) break;
+            unsigned mask = 0;
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if (p[r] < e[r] && __ldg(ci + p[r]) == best) {
+                    mask |= 1u << r;
+                    ++p[r];
+                }
+            if (out_entries) out_entries[w++] = (unsigned)best | (mask << UnionFmt<R>::kShift);
+            ++count;
+        }
+        if (out_count) out_count[b] = count;
+    }
+}
+
+template <typename T, int V, int R, int U>
+__global__ void __launch_bounds__(256, 4)
+k_row_blocked(const int *__restrict__ rp, const unsigned *__restrict__ ue,
+              const int *__restrict__ uoff, const T *__restrict__ av, const T *__restrict__ B,
+              T *__restrict__ C, int M, int N, int g, int accumulate) {
+    const int warps = (int)(blockDim.x >> 5);
+    const int w = (int)(threadIdx.x >> 5);
+    const unsigned lane = lane_id();
+    const long long kcol = (long long)lane * V;
+    const T *bk = B + kcol;
+    const long long nblocks = ((long long)M + R - 1) / R;
+    const long long tile_blocks = (long long)warps * g;
+    const long long tiles = (nblocks + tile_blocks - 1) / tile_blocks;
+    for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        for (int st = 0; st < g; ++st) {
+            const long long b = tile * tile_blocks + (long long)st * warps + w;
+            if (b >= nblocks) break;
+            const long long i0 = b * R;
+            int pos[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) pos[r] = i0 + r < M ? __ldg(rp + i0 + r) : 0;
+            Vec<T, V> acc[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) acc[r].zero();
+            const int e0 = __ldg(uoff + b), e1 = __ldg(uoff + b + 1);
+            for (int s = e0; s < e1; s += 32) {
+                const unsigned x_l = __ldg(ue + (s + (int)lane < e1 ? s + (int)lane : s));
+                const int nv = min(32, e1 - s);
+                for (int j = 0; j < nv; j += U) {
+                    unsigned xx[U];
+                    Vec<T, V> bb[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        xx[u] = __shfl_sync(kFull, x_l, (j + u) & 31);
+                        gather_vec<T, V>(bb[u], row_ptr(bk, (int)(xx[u] & UnionFmt<R>::kColMask), N));
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        if (j + u >= nv) break;
+                        const unsigned mask = xx[u] >> UnionFmt<R>::kShift;
+#pragma unroll
+                        for (int r = 0; r < R; ++r)
+                            if (mask & (1u << r)) fma_vec<T, V>(acc[r], __ldg(av + pos[r]++), bb[u]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if (i0 + r < M) store_vec<T, V>(C + (i0 + r) * (long long)N + kcol, acc[r], accumulate != 0);
+        }
+    }
+}
+
+// ===========================================================================
 // RB + parallel group reduction: row:1/g,col:c,r:g (row-reciprocal).
 // A group of G lanes owns c consecutive fused cells io = i*N + k (one row, c
 // columns); lane j accumulates positions begin+j, begin+j+G, ...

@@ -111,7 +111,9 @@ def candidates(n: int, p_values=(256, 1024), g_values=GPU_G_VALUES,
                 vs = (1, 5, 2, 3) if n // tpl.c >= 32 else (1, 5, 2)
                 out.extend(Candidate(str(pt), p, 0, v) for v in vs)
             elif variants and tpl.family == "row-multiple" and n // tpl.c <= 256:
-                vs = (0, 2, 4) if n // tpl.c == 32 else (0, 2)
+                # 6/7: a warp per 4/8-row block walking the union of the
+                # block's columns (rows <= 64; stencils / meshes)
+                vs = (0, 2, 4, 6, 7) if n // tpl.c == 32 else (0, 2)
                 out.extend(Candidate(str(pt), p, 0, v) for v in vs)
             else:
                 out.append(Candidate(str(pt), p))

@@ -219,3 +219,52 @@ def test_exact_rows_and_empty_row_gaps():
         got = c.cpu().numpy()
         assert not np.isnan(got).any(), text
         assert oracle.max_rel_error(got, want) <= TOL, text
+
+
+@pytest.mark.parametrize("variant", [6, 7])
+def test_row_blocked_union_walk(variant):
+    """Row-multiple hw variants 6/7: a warp per 4/8-row block walking the
+    union of the block's columns (plan-time k_union_rows).  Stencils, a
+    banded matrix with empty rows and M not a multiple of the block, both
+    precisions, overwrite and accumulate; matrices with rows > 64 are
+    rejected (SGAP_ERR_ARG) rather than run."""
+    from paper_2209_02882_b200 import _native
+    rng = np.random.default_rng(variant)
+    m, k = 10_003, 9_000
+    lens = rng.integers(0, 40, m)
+    lens[::17] = 0
+    rows, cols = [], []
+    for i, L in enumerate(lens):
+        lo = max(0, min(k - 80, i * k // m - 40))
+        cs = np.sort(rng.choice(np.arange(lo, lo + 80), int(L), replace=False))
+        rows.append(np.full(L, i))
+        cols.append(cs)
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    import types
+    band = types.SimpleNamespace(num_rows=m, num_cols=k, row_ptr=torch.from_numpy(rp).cuda(),
+                                 col_idx=torch.from_numpy(np.concatenate(cols)).cuda(),
+                                 vals=torch.from_numpy(rng.uniform(-1, 1, rp[-1])).cuda())
+    for g in (G.stencil27(40, device="cuda"), band):
+        print(_check(g, 128, [("row:4,col:4,r:1", 256, variant), ("row:1,col:4,r:1", 256, variant)]))
+        print(_check(g, 64, [("row:2,col:2,r:1", 256, variant)]))
+        print(_check(g, 32, [("row:4,col:1,r:1", 256, variant)]))
+    # float64 and accumulate mode
+    a = _device(band)
+    a64 = DeviceCsr(a.num_rows, a.num_cols, a.row_ptr, a.col_idx, band.vals.to(torch.float64))
+    b = torch.rand((k, 128), dtype=torch.float64, device="cuda") * 2 - 1
+    c = torch.ones((m, 128), dtype=torch.float64, device="cuda")
+    tpl = algorithm_template(parse_point("row:4,col:4,r:1"), KernelConfig(n=128, p=256))
+    kk = lower(tpl, _Rp(m, k, rp), compute_starts=False)
+    spmm(kk, a64, b, c, aux=prepare_aux(kk, a64), accumulate=True, hw_variant=variant)
+    want = oracle.spmm_f64(rp.astype(np.int32), a.col_idx.cpu().numpy(), a64.vals.cpu().numpy(),
+                           b.cpu().numpy(), 128) + 1.0
+    assert oracle.max_rel_error(c.cpu().numpy(), want) <= 1e-12
+    # rows longer than 64: no union plan, the variant refuses
+    rm = G.rmat(14, 16, seed=2, device="cuda")
+    ar = _device(rm)
+    kr = lower(tpl, _Rp(ar.num_rows, ar.num_cols, ar.row_ptr.cpu().numpy().astype(np.int64)),
+               compute_starts=False)
+    cr = torch.empty((ar.num_rows, 128), device="cuda")
+    br = torch.rand((ar.num_cols, 128), device="cuda")
+    with pytest.raises(_native.SgapError):
+        spmm(kr, ar, br, cr, aux=prepare_aux(kr, ar), hw_variant=variant)

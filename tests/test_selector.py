@@ -37,6 +37,6 @@ def test_candidate_grid_covers_families_and_walks():
     assert {c.hw_variant for c in cands if c.point.startswith("nnz:64,col:4")} == {1, 5, 2, 3}
     assert {c.hw_variant for c in candidates(32) if c.point.startswith("nnz:64,col:4")} == {1, 5, 2}
     # row-multiple: logical / interleaved, plus a warp per row where N/c == 32
-    assert {c.hw_variant for c in cands if c.point.startswith("row:4,col:4")} == {0, 2, 4}
+    assert {c.hw_variant for c in cands if c.point.startswith("row:4,col:4")} == {0, 2, 4, 6, 7}
     assert {c.hw_variant for c in cands if c.point.startswith("row:4,col:2")} == {0, 2}
     assert heuristic(STENCIL160, 128).hw_variant == 4
