@@ -517,6 +517,11 @@ def main():
     if not args.no_e2e:
         e2e = measure_e2e(args, a, b, c, k, choice, plan_for, n, total_nnz, world, dev, stream)
 
+    # ---- one call through the reference-facing drop-in (sim.run on host
+    # CsrMatrix / DenseMatrix in the reference's float64 layout)
+    if e2e is not None and rank == 0 and world == 1:
+        e2e["dropin"] = measure_dropin(a, b, k, n)
+
     # ---- CPU baselines (rank 0, single GPU only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -594,6 +599,41 @@ def time_collectives(b, c, plan, rank, dev, stream):
             "gather_c_ms": t_ga, "gather_c_bytes": cb, "gather_c_gbs": cb / (t_ga * 1e-3) / 1e9,
             "backend": dist.get_backend(),
             "note": "set-up (B replica) and optional epilogue (C on rank 0); not part of value"}
+
+
+def measure_dropin(a, b, k, n):
+    """One SpMM through ``paper_2209_02882_b200.sim.run(kernel, CsrMatrix,
+    DenseMatrix, precision="single")`` -- the call a reference caller makes
+    (spmmlab/sim.py:431-487): float64 host operands in, float64 host C out,
+    conversions, uploads, validation, planning and the download all inside
+    the wall-clock region.  Skipped when the host lacks the memory for the
+    reference layout (~2x the float32 footprint)."""
+    from paper_2209_02882_b200.matrices import CsrMatrix, DenseMatrix
+    from paper_2209_02882_b200.sim import run as sim_run
+    need = (a.nnz * 16 + a.num_cols * n * 8 + a.num_rows * n * 8) * 3
+    try:
+        import psutil
+        if psutil.virtual_memory().available < need:
+            return {"skipped": f"needs ~{need / 1e9:.0f} GB host memory"}
+    except Exception:
+        pass
+    A = CsrMatrix(a.num_rows, a.num_cols, a.row_ptr.cpu().numpy().astype(np.int64),
+                  a.col_idx.cpu().numpy().astype(np.int64),
+                  a.vals.cpu().numpy().astype(np.float64))
+    B = DenseMatrix(a.num_cols, n, b.cpu().numpy().astype(np.float64).reshape(-1))
+    torch.cuda.empty_cache()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    C, m = sim_run(k, A, B, precision="single")
+    wall = time.perf_counter() - t0
+    out = {"wall_ms": wall * 1e3, "gflops": 2.0 * a.nnz * n / wall / 1e9,
+           "kernel_ms": m.device_ms, "h2d_bytes": A.nnz * 8 + (A.num_rows + 1) * 4 + B.vals.size * 4,
+           "d2h_bytes": C.vals.size * 4,
+           "path": "sim.run(kernel, CsrMatrix f64, DenseMatrix f64, precision='single'): host "
+                   "f64->f32 / int64->int32 conversion, upload, CSR validation, sgap_plan, SpMM, "
+                   "download, f32->f64; one call, wall clock"}
+    del A, B, C
+    return out
 
 
 def measure_e2e(args, a, b, c, k, choice, plan_for, n, total_nnz, world, dev, stream):
