@@ -236,6 +236,11 @@ int launch_nnz_multiple(bool tma, int tile, int owner, const sgap_kernel_t &k,
     const int blk = k.hw_block > 0 ? k.hw_block : kEbWalkBlock;
     const int vec4 = (k.g % 4 == 0) && aligned(rowid, 16) && aligned(a.d_col_idx, 16) &&
                      aligned(a.d_vals, 16);
+    if (vec4 && chunk_rows != nullptr && k.hw_variant == 9)  // + cold-column cache hints
+        return launch_k(k_nnz_multiple<T, V, W, U, true, true>, dim3(grid_for(items, blk)),
+                        dim3(blk), 0, st, pdl, rowid, a.d_col_idx, static_cast<const T *>(a.d_vals),
+                        B, C, a.d_row_ptr, (int)a.num_rows, k.n, a.nnz, k.g, total_pos, vec4, owner,
+                        lr, wb, exact_inline, chunk_rows);
     if (vec4 && chunk_rows != nullptr)  // row_ptr tracking, no per-position row ids
         return launch_k(k_nnz_multiple<T, V, W, U, true>, dim3(grid_for(items, blk)), dim3(blk), 0,
                         st, pdl, rowid, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C,
@@ -272,6 +277,7 @@ int run_nnz_multiple_w(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, 
     // error after the exact pass would leave its sums in the float64 table
     // (never folded, so a later call on the same plan would add them to C)
     if (tma && !tma_ok) return SGAP_ERR_ARG;
+    if (variant == 9) variant = 1;  // (experiment: variant 1 with cold-column cache hints)
     if (variant < 1 || variant > 5) return SGAP_ERR_ARG;
     const bool staged = variant == 3 || variant == 4;
     if (staged && W != 32) return SGAP_ERR_ARG;  // the staged walk takes a whole warp
@@ -326,6 +332,7 @@ int run_nnz_multiple_w(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, 
     return launch_nnz_multiple<T, V, W, 4>(tma, tile, owner, k, a, B, C, rowid, lr, wb, st,
                                            pdl, exact_inline ? 1 : 0,
                                            variant == 1 ? lr.chunk_rows : nullptr);
+    // (k.hw_variant == 9 selects the cold-hint instantiation inside)
 }
 
 template <typename T, int V>

@@ -930,6 +930,27 @@ __device__ __forceinline__ void eb_walk4(const ASrc &A, long long q0, long long 
 // iff q + 3 < ce.  A row change walks row_ptr forward (empty rows passed are
 // zeroed in owner mode); the table / error-free flags of a row follow from
 // its length, so the A stream is 8 bytes per position instead of 12.
+// B-row gather of the row_ptr walk.  HINT: the column carries bit 31 for
+// "cold" columns (outside the plan's hot set) whose rows are loaded with the
+// streaming cache operator (ld.global.cs: evict-first in L1 and L2) so they
+// do not push the hot rows out of L2.
+template <typename T, int V, bool HINT>
+__device__ __forceinline__ void gather_b(Vec<T, V> &o, const T *__restrict__ bk, int c, int N) {
+    if constexpr (HINT && sizeof(T) == 4 && V == 4) {
+        const float *p = row_ptr(bk, c & 0x7fffffff, N);
+        if (c < 0) {
+            const float4 t = __ldcs(reinterpret_cast<const float4 *>(p));
+            o.v[0] = t.x; o.v[1] = t.y; o.v[2] = t.z; o.v[3] = t.w;
+        } else {
+            ldg_vec<T, V>(o, p);
+        }
+    } else if constexpr (HINT) {
+        ldg_vec<T, V>(o, row_ptr(bk, c & 0x7fffffff, N));
+    } else {
+        ldg_vec<T, V>(o, row_ptr(bk, c, N));
+    }
+}
+
 __device__ __forceinline__ int row_flags(int cur, unsigned cs, unsigned ce, const LongRows &lr) {
     if (lr.threshold < 0) return cur;
     const long long len = (long long)ce - (long long)cs;
@@ -950,7 +971,7 @@ __device__ __forceinline__ void zero_gap_before_rp(T *__restrict__ C, int N, lon
         store_vec<T, V>(C + (long long)r * N + kcol, z, false);
 }
 
-template <typename T, int V>
+template <typename T, int V, bool HINT = false>
 __device__ __forceinline__ void eb_walk4_rp(const GlobalA<T> &A, const int *__restrict__ rp,
                                             int cur, long long q0, long long qend,
                                             const T *__restrict__ B, int N, long long kcol,
@@ -993,10 +1014,10 @@ __device__ __forceinline__ void eb_walk4_rp(const GlobalA<T> &A, const int *__re
         Vec<T, 4> v;
         A.load4cv(qq, c, v);
         Vec<T, V> b0, b1, b2, b3;
-        ldg_vec<T, V>(b0, row_ptr(bk, c.x, N));
-        ldg_vec<T, V>(b1, row_ptr(bk, c.y, N));
-        ldg_vec<T, V>(b2, row_ptr(bk, c.z, N));
-        ldg_vec<T, V>(b3, row_ptr(bk, c.w, N));
+        gather_b<T, V, HINT>(b0, bk, c.x, N);
+        gather_b<T, V, HINT>(b1, bk, c.y, N);
+        gather_b<T, V, HINT>(b2, bk, c.z, N);
+        gather_b<T, V, HINT>(b3, bk, c.w, N);
         if (qq + 3 < ce) {
             fma_vec<T, V>(acc, v.v[0], b0);
             fma_vec<T, V>(acc, v.v[1], b1);
@@ -1023,7 +1044,7 @@ __device__ __forceinline__ void eb_walk4_rp(const GlobalA<T> &A, const int *__re
     }
     for (; q < qe; ++q) {  // < 4 tail positions
         Vec<T, V> b;
-        ldg_vec<T, V>(b, row_ptr(bk, A.col(q), N));
+        gather_b<T, V, HINT>(b, bk, A.col(q), N);
         if (q >= ce) advance(q);
         fma_vec<T, V>(acc, A.val(q), b);
     }
@@ -1165,11 +1186,11 @@ __device__ __noinline__ void eb_chunk_f64(const GlobalA<T> A, long long base, lo
         int4 c;
         Vec<T, 4> v;
         A.load4cv(q, c, v);
-        Vec<T, V> b0, b1, b2, b3;
-        ldg_vec<T, V>(b0, row_ptr(bk, c.x, N));
-        ldg_vec<T, V>(b1, row_ptr(bk, c.y, N));
-        ldg_vec<T, V>(b2, row_ptr(bk, c.z, N));
-        ldg_vec<T, V>(b3, row_ptr(bk, c.w, N));
+        Vec<T, V> b0, b1, b2, b3;  // (bit 31: the cold-column hint, not part of the index)
+        ldg_vec<T, V>(b0, row_ptr(bk, c.x & 0x7fffffff, N));
+        ldg_vec<T, V>(b1, row_ptr(bk, c.y & 0x7fffffff, N));
+        ldg_vec<T, V>(b2, row_ptr(bk, c.z & 0x7fffffff, N));
+        ldg_vec<T, V>(b3, row_ptr(bk, c.w & 0x7fffffff, N));
 #pragma unroll
         for (int x = 0; x < V; ++x) {
             tot.v[x] = fma((double)v.v[0], (double)b0.v[x], tot.v[x]);
@@ -1180,7 +1201,7 @@ __device__ __noinline__ void eb_chunk_f64(const GlobalA<T> A, long long base, lo
     }
     for (; q < qe; ++q) {
         Vec<T, V> b;
-        ldg_vec<T, V>(b, row_ptr(bk, A.col(q), N));
+        ldg_vec<T, V>(b, row_ptr(bk, A.col(q) & 0x7fffffff, N));
         const double a = (double)A.val(q);
 #pragma unroll
         for (int x = 0; x < V; ++x) tot.v[x] = fma(a, (double)b.v[x], tot.v[x]);
@@ -1188,7 +1209,7 @@ __device__ __noinline__ void eb_chunk_f64(const GlobalA<T> A, long long base, lo
     flush_row<T, V>(C, N, r_first, kcol, tot, lr);  // the float64 table
 }
 
-template <typename T, int V, int W, int U, bool RPW = false>
+template <typename T, int V, int W, int U, bool RPW = false, bool HINT = false>
 __global__ void __launch_bounds__(256, SGAP_EB_MINB)
 k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
                const T *__restrict__ av, const T *__restrict__ B, T *__restrict__ C,
@@ -1236,7 +1257,7 @@ k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
                                            cur | kLongFlag | kExactFlag, VEC4);
                     continue;
                 }
-                eb_walk4_rp<T, V>(A, rp, cur, base, end, B, N, kcol, C, lr, own, nwb);
+                eb_walk4_rp<T, V, HINT>(A, rp, cur, base, end, B, N, kcol, C, lr, own, nwb);
                 continue;
             } else {
             const int r_first = A.row(base);
