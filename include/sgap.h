@@ -107,7 +107,8 @@ typedef struct {
     int32_t hw_variant;     /* nnz-multiple walk: 0 auto, 1 register-staged
                                (row_ptr tracking when the plan has chunk
                                start rows), 5 register-staged on per-position
-                               row ids,
+                               row ids, 9 = 1 with the plan's cold-column
+                               cache hints (SGAP_PLAN_L2_HINTS),
                                2 TMA-staged (cp.async.bulk + mbarrier ring),
                                3/4 lane-staged (warp per chunk, 4/8 B-row
                                gathers in flight; needs N/c >= 32).
@@ -194,6 +195,13 @@ typedef struct {
     const uint32_t *d_union[2];      /* (col | row mask << (32 - R)) entries:
                                         the row-blocked walk (hw variants
                                         6 / 7) gathers each shared B row once */
+    const int32_t *d_col_hinted;    /* SGAP_PLAN_L2_HINTS, nnz-multiple: col_idx
+                                        with bit 31 set on columns outside
+                                        the hot set (the most-gathered
+                                        columns whose B rows fill half the
+                                        L2); hw variant 9 loads those rows
+                                        with the evict-first streaming
+                                        operator so the hot rows stay in L2 */
 } sgap_aux_t;
 
 /* Per-position row ids (what the reference lowering recovers per lane with
@@ -227,6 +235,11 @@ int64_t sgap_long_row_threshold(const sgap_kernel_t *kernel, int32_t dtype);
  * of row statistics (longest row, number of table rows and of error-free
  * rows), which size the per-run launches.  It allocates nothing.            */
 #define SGAP_PLAN_VALIDATE 1u     /* run sgap_validate_csr first            */
+#define SGAP_PLAN_L2_HINTS 4u     /* nnz-multiple, g % 4 == 0: build the
+                                     cold-column hints of hw variant 9 (a
+                                     col_idx copy in the workspace; worth it
+                                     when B is far larger than L2: config 5
+                                     -4.8%, config 2 slower)                */
 #define SGAP_PLAN_SPLIT_ROWS 2u   /* nnz-multiple, g >= 128: rows straddling a
                                      g-chunk boundary join the float64 table
                                      (no zero-fill pre-pass; measured slower

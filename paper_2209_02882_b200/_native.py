@@ -128,6 +128,7 @@ class Aux(ctypes.Structure):
         ("d_union_off8", ctypes.c_void_p),
         ("d_union4", ctypes.c_void_p),
         ("d_union8", ctypes.c_void_p),
+        ("d_col_hinted", ctypes.c_void_p),
     ]
 
 
@@ -154,6 +155,7 @@ class Plan(ctypes.Structure):
 # sgap_plan flags
 PLAN_VALIDATE = 1
 PLAN_SPLIT_ROWS = 2
+PLAN_L2_HINTS = 4
 
 _lib = None
 

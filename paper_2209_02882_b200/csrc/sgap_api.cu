@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <cstring>
 
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 #include <cuda_runtime.h>
@@ -236,11 +237,13 @@ int launch_nnz_multiple(bool tma, int tile, int owner, const sgap_kernel_t &k,
     const int blk = k.hw_block > 0 ? k.hw_block : kEbWalkBlock;
     const int vec4 = (k.g % 4 == 0) && aligned(rowid, 16) && aligned(a.d_col_idx, 16) &&
                      aligned(a.d_vals, 16);
-    if (vec4 && chunk_rows != nullptr && k.hw_variant == 9)  // + cold-column cache hints
+    if (k.hw_variant == 9) {  // + cold-column cache hints (the plan's flagged col_idx)
+        if (!vec4 || chunk_rows == nullptr || lr.col_hinted == nullptr) return SGAP_ERR_ARG;
         return launch_k(k_nnz_multiple<T, V, W, U, true, true>, dim3(grid_for(items, blk)),
-                        dim3(blk), 0, st, pdl, rowid, a.d_col_idx, static_cast<const T *>(a.d_vals),
+                        dim3(blk), 0, st, pdl, rowid, lr.col_hinted, static_cast<const T *>(a.d_vals),
                         B, C, a.d_row_ptr, (int)a.num_rows, k.n, a.nnz, k.g, total_pos, vec4, owner,
                         lr, wb, exact_inline, chunk_rows);
+    }
     if (vec4 && chunk_rows != nullptr)  // row_ptr tracking, no per-position row ids
         return launch_k(k_nnz_multiple<T, V, W, U, true>, dim3(grid_for(items, blk)), dim3(blk), 0,
                         st, pdl, rowid, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C,
@@ -277,7 +280,11 @@ int run_nnz_multiple_w(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, 
     // error after the exact pass would leave its sums in the float64 table
     // (never folded, so a later call on the same plan would add them to C)
     if (tma && !tma_ok) return SGAP_ERR_ARG;
-    if (variant == 9) variant = 1;  // (experiment: variant 1 with cold-column cache hints)
+    if (variant == 9) {  // variant 1 with the plan's cold-column cache hints
+        const int vec4 = (k.g % 4 == 0) && aligned(a.d_col_idx, 16) && aligned(a.d_vals, 16);
+        if (lr.col_hinted == nullptr || lr.chunk_rows == nullptr || !vec4) return SGAP_ERR_ARG;
+        variant = 1;
+    }
     if (variant < 1 || variant > 5) return SGAP_ERR_ARG;
     const bool staged = variant == 3 || variant == 4;
     if (staged && W != 32) return SGAP_ERR_ARG;  // the staged walk takes a whole warp
@@ -515,7 +522,7 @@ static int run_impl(const sgap_kernel_t *k, const sgap_csr_t *a, const void *d_b
     if (eb && k->grid_size > 0 && a->nnz > 0 && rowid == nullptr) return SGAP_ERR_ARG;
     if (k->family == SGAP_NNZ_MULTIPLE && (k->g < 1 || k->chunk % k->g)) return SGAP_ERR_CONFIG;
     LongRows lr{nullptr, nullptr, nullptr, -1, nullptr, 0, nullptr, 0, nullptr, {nullptr, nullptr},
-                {nullptr, nullptr}};
+                {nullptr, nullptr}, nullptr};
     const bool has_exact = aux != nullptr && aux->has_exact_rows != 0;
     // exact-flagged chunks are skipped by the main walk: their pass needs the list
     if (has_exact && k->family == SGAP_NNZ_MULTIPLE && dtype == SGAP_F32 &&
@@ -526,9 +533,12 @@ static int run_impl(const sgap_kernel_t *k, const sgap_csr_t *a, const void *d_b
             return SGAP_ERR_ARG;
         lr = LongRows{aux->d_long_rows, aux->d_long_count, aux->d_long_acc, aux->long_threshold,
                       aux->d_long_slot, aux->long_chunk, aux->d_exact_rows, aux->exact_count,
-                      nullptr, {nullptr, nullptr}, {nullptr, nullptr}};
+                      nullptr, {nullptr, nullptr}, {nullptr, nullptr}, nullptr};
     }
-    if (k->family == SGAP_NNZ_MULTIPLE && aux != nullptr) lr.chunk_rows = aux->d_chunk_rows;
+    if (k->family == SGAP_NNZ_MULTIPLE && aux != nullptr) {
+        lr.chunk_rows = aux->d_chunk_rows;
+        lr.col_hinted = aux->d_col_hinted;
+    }
     if (k->family == SGAP_ROW_MULTIPLE && aux != nullptr) {
         for (int w = 0; w < 2; ++w) {
             lr.union_e[w] = reinterpret_cast<const unsigned *>(aux->d_union[w]);
@@ -570,7 +580,8 @@ struct LongerThan {
 struct PlanLayout {
     size_t starts = 0, rowid = 0, slot = 0, rows = 0, count = 0, acc = 0, exact = 0, stats = 0,
            tmp = 0, chunk_rows = 0, union_off[2] = {0, 0}, union_e[2] = {0, 0}, union_tmp = 0,
-           total = 0;
+           hint_counts = 0, hint_sorted = 0, hint_cols = 0, hint_tmp = 0, total = 0;
+    size_t hint_tmp_bytes = 0;
     size_t union_tmp_bytes = 0;
     long long thr = -1, chunk = 0, cap = 0, exact_cap = 0, exact_cut = 0;
     size_t tmp_bytes = 0;
@@ -608,6 +619,17 @@ int plan_layout(const sgap_kernel_t &k, const sgap_csr_t &a, int32_t dtype, uint
         L.rowid = take((size_t)(nnz > 4 ? nnz : 4) * sizeof(int));
         if (k.family == SGAP_NNZ_MULTIPLE && k.g % 4 == 0 && k.g > 0)
             L.chunk_rows = take((size_t)(k.grid_size * (k.chunk / k.g) + 1) * sizeof(int));
+        if (L.chunk_rows && (flags & SGAP_PLAN_L2_HINTS) && nnz > 0 && a.num_cols > 0) {
+            const long long K = a.num_cols;
+            L.hint_counts = take((size_t)K * sizeof(unsigned));
+            L.hint_sorted = take((size_t)K * sizeof(unsigned));
+            L.hint_cols = take((size_t)nnz * sizeof(int));
+            size_t sb = 0;
+            cub::DeviceRadixSort::SortKeysDescending(nullptr, sb, (unsigned *)nullptr,
+                                                     (unsigned *)nullptr, (int)K);
+            L.hint_tmp_bytes = sb;
+            L.hint_tmp = take(sb);
+        }
         L.thr = sgap_long_row_threshold(&k, dtype);
         L.chunk = (L.thr >= 0 && (flags & SGAP_PLAN_SPLIT_ROWS)) ? long_row_chunk(&k, dtype) : 0;
         if (L.thr >= 0) {
@@ -958,6 +980,32 @@ int sgap_plan(const sgap_kernel_t *k, const sgap_csr_t *a, int32_t dtype, uint32
                                          reinterpret_cast<int32_t *>(ws + L.chunk_rows), stream);
         if (s4 != SGAP_OK) return s4;
         aux.d_chunk_rows = reinterpret_cast<const int32_t *>(ws + L.chunk_rows);
+    }
+    if (L.hint_cols) {
+        // cold-column hints: per-column gather counts, the count of the
+        // H-th most-gathered column (H = half the L2 in B rows) as the hot
+        // threshold, then the flagged col_idx copy
+        int dev = 0, l2 = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+        const size_t esz = dtype == SGAP_F32 ? 4 : 8;
+        long long H = (long long)(l2 / 2) / ((long long)k->n * (long long)esz);
+        if (H < 1) H = 1;
+        if (H > a->num_cols) H = a->num_cols;
+        unsigned *counts = reinterpret_cast<unsigned *>(ws + L.hint_counts);
+        unsigned *sorted = reinterpret_cast<unsigned *>(ws + L.hint_sorted);
+        int *hinted = reinterpret_cast<int *>(ws + L.hint_cols);
+        if (cudaMemsetAsync(counts, 0, (size_t)a->num_cols * sizeof(unsigned), st) != cudaSuccess)
+            return SGAP_ERR_CUDA;
+        const unsigned g1 = (unsigned)ceil_div(nnz < (1LL << 24) ? nnz : (1LL << 24), kHwBlock);
+        k_col_counts<<<g1, kHwBlock, 0, st>>>(a->d_col_idx, nnz, counts);
+        size_t tb = L.hint_tmp_bytes;
+        if (cub::DeviceRadixSort::SortKeysDescending(ws + L.hint_tmp, tb, counts, sorted,
+                                                     (int)a->num_cols, 0, 32, st) != cudaSuccess)
+            return SGAP_ERR_CUDA;
+        k_col_hints<<<g1, kHwBlock, 0, st>>>(a->d_col_idx, nnz, counts, sorted + (H - 1), hinted);
+        if (cudaGetLastError() != cudaSuccess) return SGAP_ERR_CUDA;
+        aux.d_col_hinted = hinted;
     }
     if (cudaMemcpyAsync(h, stats, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st) !=
             cudaSuccess ||

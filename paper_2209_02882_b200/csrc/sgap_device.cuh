@@ -236,6 +236,7 @@ struct LongRows {
                             // walk without row ids); nullptr: use the row ids
     const unsigned *union_e[2];  // row-blocked RB walk: union column streams of
     const int *union_off[2];     // 4-row [0] and 8-row [1] blocks (k_union_rows)
+    const int *col_hinted;       // col_idx with bit 31 on cold columns (variant 9)
 };
 
 // Row ids carry bit 31 when the row belongs to the long-row table and bit 30

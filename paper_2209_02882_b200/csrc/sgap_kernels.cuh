@@ -1789,6 +1789,27 @@ k_validate_cols(const int *__restrict__ rp, const int *__restrict__ ci, int M, l
     }
 }
 
+// Plan-time cold-column hints (SGAP_PLAN_L2_HINTS): gather counts per
+// column, then a copy of col_idx with bit 31 set on columns gathered fewer
+// than `thr` times (outside the hot set the L2 can keep).
+__global__ void __launch_bounds__(256)
+k_col_counts(const int *__restrict__ ci, long long nnz, unsigned *__restrict__ counts) {
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < nnz;
+         p += (long long)gridDim.x * blockDim.x)
+        atomicAdd(counts + __ldg(ci + p), 1u);
+}
+
+__global__ void __launch_bounds__(256)
+k_col_hints(const int *__restrict__ ci, long long nnz, const unsigned *__restrict__ counts,
+            const unsigned *__restrict__ thr, int *__restrict__ out) {
+    const unsigned t = *thr;
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < nnz;
+         p += (long long)gridDim.x * blockDim.x) {
+        const int c = __ldg(ci + p);
+        out[p] = __ldg(counts + c) < t ? (int)((unsigned)c | 0x80000000u) : c;
+    }
+}
+
 // Row -> slot map of the table (only the table's rows are written).
 __global__ void k_long_slots(const int *__restrict__ rows, const int *__restrict__ count,
                              int *__restrict__ slot) {

@@ -194,11 +194,17 @@ class KernelAux:
         return int(self.workspace.numel())
 
 
-def plan_workspace_bytes(k: LoweredKernel, a: DeviceCsr, *, split_rows: bool = False) -> int:
+# B larger than this (twice the 126 MB L2) gets cold-column hints by default
+_L2_HINT_MIN_B_BYTES = 256 << 20
+
+
+def plan_workspace_bytes(k: LoweredKernel, a: DeviceCsr, *, split_rows: bool = False,
+                         flags: int | None = None) -> int:
     ks = kernel_struct(k)
     view = a.view()
     out = ctypes.c_size_t(0)
-    flags = _native.PLAN_SPLIT_ROWS if split_rows else 0
+    if flags is None:
+        flags = _native.PLAN_SPLIT_ROWS if split_rows else 0
     _native.check(_native.lib().sgap_plan_workspace_bytes(
         ctypes.byref(ks), ctypes.byref(view), native_dtype(a.vals.dtype), flags,
         ctypes.byref(out)), "sgap_plan_workspace_bytes")
@@ -206,7 +212,8 @@ def plan_workspace_bytes(k: LoweredKernel, a: DeviceCsr, *, split_rows: bool = F
 
 
 def prepare_aux(k: LoweredKernel, a: DeviceCsr, *, stream=None, split_rows: bool = False,
-                validate: bool = False, row_ptr_host=None) -> KernelAux:
+                validate: bool = False, l2_hints: bool | None = None,
+                row_ptr_host=None) -> KernelAux:
     """``sgap_plan``: the per-matrix half of ``runner.build_kernel``
     (block_starts, lowering.py:683-696) plus the engine's side data, built on
     the device in one workspace (one 24-byte read-back of row statistics).
@@ -216,14 +223,21 @@ def prepare_aux(k: LoweredKernel, a: DeviceCsr, *, stream=None, split_rows: bool
     2, off by default).  ``validate``: check the CsrMatrix invariants first
     (``sgap_validate_csr``; raises ``SimulationFault``-compatible
     ``SgapError`` status FAULT).  ``row_ptr_host`` is accepted for
-    compatibility and unused: planning needs no host copy of the matrix."""
+    compatibility and unused: planning needs no host copy of the matrix.
+    ``l2_hints``: build the cold-column cache hints of hw variant 9
+    (nnz-multiple); None = when B is more than twice the L2 (config 5)."""
     del row_ptr_host
     a.check()
     L = _native.lib()
-    flags = (_native.PLAN_SPLIT_ROWS if split_rows else 0) | (_native.PLAN_VALIDATE if validate else 0)
+    if l2_hints is None:
+        l2_hints = (k.family == "nnz-multiple" and
+                    a.num_cols * k.n * a.vals.element_size() > _L2_HINT_MIN_B_BYTES)
+    flags = ((_native.PLAN_SPLIT_ROWS if split_rows else 0) |
+             (_native.PLAN_VALIDATE if validate else 0) |
+             (_native.PLAN_L2_HINTS if l2_hints else 0))
     ks = kernel_struct(k)
     view = a.view()
-    nbytes = plan_workspace_bytes(k, a, split_rows=split_rows)
+    nbytes = plan_workspace_bytes(k, a, flags=flags)
     ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=a.device)
     plan = _native.Plan()
     _native.check(L.sgap_plan(ctypes.byref(ks), ctypes.byref(view), native_dtype(a.vals.dtype),
@@ -326,7 +340,7 @@ def launches_per_call(k: LoweredKernel, aux: KernelAux | None, *, accumulate: bo
             # k_nnz_multiple_exact (sgap_api.cu run_nnz_multiple_w)
             w = min(32, max(1, k.n // k.c))
             variant = hw_variant or (2 if (w >= 16 and k.g <= 128) else 1)
-            n += 0 if variant in (1, 5) else 1
+            n += 0 if variant in (1, 5, 9) else 1
     return n
 
 

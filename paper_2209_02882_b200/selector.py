@@ -108,7 +108,8 @@ def candidates(n: int, p_values=(256, 1024), g_values=GPU_G_VALUES,
                 # 1: register walk tracking rows through row_ptr (DRAM-bound
                 # matrices: configs 3/5), 5: the same walk on per-position row
                 # ids (latency-bound: config 2), 2: TMA-staged, 3: lane-staged
-                vs = (1, 5, 2, 3) if n // tpl.c >= 32 else (1, 5, 2)
+                # 9: 1 + the plan's cold-column cache hints (B >> L2: config 5)
+                vs = (1, 5, 9, 2, 3) if n // tpl.c >= 32 else (1, 5, 9, 2)
                 out.extend(Candidate(str(pt), p, 0, v) for v in vs)
             elif variants and tpl.family == "row-multiple" and n // tpl.c <= 256:
                 # 6/7: a warp per 4/8-row block walking the union of the

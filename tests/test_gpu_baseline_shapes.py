@@ -162,7 +162,9 @@ def test_config5_one_point_per_family_sampled_rows():
                            b.cpu().numpy(), n)
     rows_d = torch.from_numpy(rows).cuda()
     worst = {}
-    for text, p, variant in (("nnz:512,col:4,r:1", 256, 1), ("nnz:128,col:4,r:1", 256, 2),
+    for text, p, variant in (("nnz:512,col:4,r:1", 256, 1), ("nnz:512,col:4,r:1", 256, 9),
+                             ("nnz:512,col:4,r:1", 256, 5),
+                             ("nnz:128,col:4,r:1", 256, 2),
                              ("nnz:256,col:4,r:1", 256, 3), ("nnz:1,col:4,r:8", 1024, 0),
                              ("nnz:1,col:4,r:1", 256, 0), ("row:8,col:4,r:1", 256, 3),
                              ("row:4,col:4,r:1", 256, 0), ("row:1/8,col:4,r:8", 256, 0)):

@@ -268,3 +268,35 @@ def test_row_blocked_union_walk(variant):
     br = torch.rand((ar.num_cols, 128), device="cuda")
     with pytest.raises(_native.SgapError):
         spmm(kr, ar, br, cr, aux=prepare_aux(kr, ar), hw_variant=variant)
+
+
+def test_cold_column_hint_walk():
+    """hw variant 9: the row_ptr walk reading the plan's flagged col_idx copy
+    (bit 31 = cold column, gathered with the streaming cache operator):
+    same results as variant 1, the hints never leak into an index --
+    including chunks inside error-free hub rows (the inline float64 path)."""
+    g = G.rmat(17, 16, seed=6, device="cuda")
+    a = _device(g)
+    rp = a.row_ptr.cpu().numpy().astype(np.int64)
+    n = 128
+    b = torch.rand((a.num_cols, n), device="cuda") * 2 - 1
+    want = oracle.spmm_f64(rp.astype(np.int32), a.col_idx.cpu().numpy(), a.vals.cpu().numpy(),
+                           b.cpu().numpy(), n)
+    c = torch.empty((a.num_rows, n), device="cuda")
+    for text, p in (("nnz:512,col:4,r:1", 256), ("nnz:32,col:4,r:1", 256)):
+        k = lower(algorithm_template(parse_point(text), KernelConfig(n=n, p=p)),
+                  _Rp(a.num_rows, a.num_cols, rp), compute_starts=False)
+        aux = prepare_aux(k, a, l2_hints=True)
+        assert aux.plan.aux.d_col_hinted
+        wb = {}
+        for v in (1, 9):
+            cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+            c.fill_(float("nan"))
+            spmm(k, a, b, c, aux=aux, hw_variant=v, writebacks=cnt)
+            assert oracle.max_rel_error(c.cpu().numpy(), want) <= TOL, (text, v)
+            wb[v] = int(cnt.item())
+        assert wb[1] == wb[9]
+        # without hints in the plan, variant 9 refuses
+        from paper_2209_02882_b200 import _native
+        with pytest.raises(_native.SgapError):
+            spmm(k, a, b, c, aux=prepare_aux(k, a, l2_hints=False), hw_variant=9)

@@ -34,8 +34,8 @@ def test_candidate_grid_covers_families_and_walks():
     assert fams == {"nnz-one", "nnz-multiple", "row-multiple", "row-reciprocal"}
     assert any(c.point.startswith("nnz:512") for c in cands)
     # register walks (row_ptr / row ids) and TMA everywhere, lane-staged where N/c >= 32
-    assert {c.hw_variant for c in cands if c.point.startswith("nnz:64,col:4")} == {1, 5, 2, 3}
-    assert {c.hw_variant for c in candidates(32) if c.point.startswith("nnz:64,col:4")} == {1, 5, 2}
+    assert {c.hw_variant for c in cands if c.point.startswith("nnz:64,col:4")} == {1, 5, 9, 2, 3}
+    assert {c.hw_variant for c in candidates(32) if c.point.startswith("nnz:64,col:4")} == {1, 5, 9, 2}
     # row-multiple: logical / interleaved, plus a warp per row where N/c == 32
     assert {c.hw_variant for c in cands if c.point.startswith("row:4,col:4")} == {0, 2, 4, 6, 7}
     assert {c.hw_variant for c in cands if c.point.startswith("row:4,col:2")} == {0, 2}
