@@ -410,7 +410,7 @@ def main():
     from paper_2209_02882_b200.device import DeviceCsr, launches_per_call, prepare_aux, spmm
     from paper_2209_02882_b200.partition import plan_shards, shard_csr
     from paper_2209_02882_b200.selector import (Candidate, autotune, candidates, heuristic,
-                                                matrix_stats, plan_for)
+                                                matrix_stats, plan_for, refine)
     import torch.distributed as dist
 
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -443,7 +443,9 @@ def main():
                               stream=stream, max_ms=50.0)
             sweep_rows = [{"point": cd.point, "p": cd.p, "hw_variant": cd.hw_variant, "ms": ms,
                            "gflops": 2.0 * a.nnz * n / (ms * 1e6)} for cd, ms in ranked]
-            choice = ranked[0][0]
+            # the leaders again, interleaved (drift-proof pick among near-ties)
+            final = refine(a, b, c, n, ranked, row_ptr_host=rp_host, stream=stream)
+            choice = final[0][0]
         if world > 1:
             obj = [choice]
             dist.broadcast_object_list(obj, src=0)

@@ -230,3 +230,35 @@ def autotune(a: DeviceCsr, b: torch.Tensor, c: torch.Tensor, n: int, cands, *, r
         results.append((cand, best))
     results.sort(key=lambda t: t[1])
     return results
+
+
+def refine(a: DeviceCsr, b: torch.Tensor, c: torch.Tensor, n: int, ranked, *, top: int = 6,
+           rounds: int = 4, reps: int = 3, row_ptr_host=None, stream=None):
+    """Re-time the ``top`` candidates of an ``autotune`` ranking in
+    interleaved rounds (median of ``reps`` launches per round, median over
+    rounds), so clock and power drift during the sweep cannot pick a
+    candidate that is only a few percent ahead by luck (config 5's walks
+    differ by 3-5%).  Returns [(candidate, ms)] fastest first."""
+    import statistics
+    rp = row_ptr_host if row_ptr_host is not None else a.row_ptr.cpu().numpy()
+    stream = stream or torch.cuda.current_stream()
+    arms = []
+    for cand, _ in ranked[:top]:
+        k = plan_for(cand, n, a.num_rows, a.num_cols, rp)
+        arms.append((cand, k, prepare_aux(k, a, stream=stream)))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    times = {id(cd): [] for cd, _, _ in arms}
+    for _ in range(rounds):
+        for cand, k, aux in arms:
+            ts = []
+            for _ in range(reps):
+                e0.record(stream)
+                spmm(k, a, b, c, aux=aux, hw_block=cand.hw_block, hw_variant=cand.hw_variant,
+                     stream=stream)
+                e1.record(stream)
+                e1.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            times[id(cand)].append(statistics.median(ts))
+    out = [(cand, statistics.median(times[id(cand)])) for cand, _, _ in arms]
+    out.sort(key=lambda t: t[1])
+    return out
