@@ -85,6 +85,7 @@ def plan_for(cand: Candidate, n: int, num_rows: int, num_cols: int, row_ptr_host
 # (space.py:220) with longer serial chunks, which the EB walk amortises
 # best on power-law matrices; the point grammar already admits any g >= 2.
 GPU_G_VALUES = (2, 4, 8, 16, 32, 64, 128, 256, 512)
+L2_BYTES = 126 << 20  # B200 (cudaDevAttrL2CacheSize: 132,644,864)
 
 
 def candidates(n: int, p_values=(256, 1024), g_values=GPU_G_VALUES,
@@ -187,11 +188,18 @@ def heuristic(stats: MatrixStats, n: int) -> Candidate:
         return Candidate(pt, _first_p(pt, n) or 256)
     c = widest if n >= 16 else min(widest, max(1, n // 4))
     g = max(32, min(512, _pow2_floor(stats.nnz / 40_000)))
+    # the register walk's flavour by the size of B against the L2 (round-2
+    # interleaved A/B, profiles/r02_ab_*): B within L2 -> row_ptr tracking
+    # (config 3), B a few L2s -> row ids (config 2: latency-bound, row
+    # changes every ~16 positions), B >> L2 -> row_ptr tracking + cold-column
+    # cache hints (config 5: DRAM-bound)
+    b_bytes = stats.num_cols * n * 4
+    variant = 1 if b_bytes <= L2_BYTES else (5 if b_bytes <= 16 * L2_BYTES else 9)
     for gg in (g, 256, 128, 64, 32):
         pt = f"nnz:{gg},col:{col(c)},r:1"
         p = _first_p(pt, n)
         if p is not None:
-            return Candidate(pt, p)
+            return Candidate(pt, p, 0, variant if gg % 4 == 0 else 5)
     pt = f"row:1,col:{col(widest)},r:1"
     return Candidate(pt, _first_p(pt, n) or 256)
 
