@@ -186,9 +186,45 @@ int run_nnz_one_r(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
     return launch_status();
 }
 
+template <typename T, int V, int W>
+int run_nnz_multiple_w(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
+                       const int *rowid, const LongRows &lr, int owner, bool has_exact,
+                       bool zero, unsigned long long *wb, cudaStream_t st);
+
+// nnz-one hw variant 1: each aligned segment group of r positions walked
+// serially by N/c lanes along the columns (the register walk with g = r, one
+// red per segment -- the same writebacks as the shuffle scan, which gathers
+// B rows in (32/r)-tile pieces); the group straddling nnz adds the padded run
+// (owner mode 2 in k_nnz_multiple).
+template <typename T, int V>
+int run_nnz_one_walk(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
+                     const int *rowid, const LongRows &lr, unsigned long long *wb,
+                     cudaStream_t st) {
+    sgap_kernel_t km = k;
+    km.family = SGAP_NNZ_MULTIPLE;
+    km.g = k.r;
+    km.hw_variant = 5;  // the row-id walk (the nnz-one plan has row ids, no chunk rows)
+    km.hw_block = 0;
+    LongRows lw = lr;
+    lw.chunk_rows = nullptr;
+    // owner mode 2: segment groups (r > 1, padded lanes are a run of row
+    // M-1); 3: r = 1 atomics (lanes past nnz do not write)
+    const int mode = k.r > 1 ? 2 : 3;
+    switch (pow2_floor(k.n / V)) {
+        case 1: return run_nnz_multiple_w<T, V, 1>(km, a, B, C, rowid, lw, mode, false, false, wb, st);
+        case 2: return run_nnz_multiple_w<T, V, 2>(km, a, B, C, rowid, lw, mode, false, false, wb, st);
+        case 4: return run_nnz_multiple_w<T, V, 4>(km, a, B, C, rowid, lw, mode, false, false, wb, st);
+        case 8: return run_nnz_multiple_w<T, V, 8>(km, a, B, C, rowid, lw, mode, false, false, wb, st);
+        case 16: return run_nnz_multiple_w<T, V, 16>(km, a, B, C, rowid, lw, mode, false, false, wb, st);
+        default: return run_nnz_multiple_w<T, V, 32>(km, a, B, C, rowid, lw, mode, false, false, wb, st);
+    }
+}
+
 template <typename T, int V>
 int run_nnz_one(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
                 const int *rowid, const LongRows &lr, unsigned long long *wb, cudaStream_t st) {
+    if (k.hw_variant == 1) return run_nnz_one_walk<T, V>(k, a, B, C, rowid, lr, wb, st);
+    if (k.hw_variant != 0) return SGAP_ERR_ARG;
     switch (k.r) {
         case 1: return run_nnz_one_r<T, V, 1>(k, a, B, C, rowid, lr, wb, st);
         case 2: return run_nnz_one_r<T, V, 2>(k, a, B, C, rowid, lr, wb, st);

@@ -1238,10 +1238,19 @@ k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
         const long long end = min(base + (long long)g, nnz);
         for (int tile = sl; tile < NT; tile += W) {
             if (base >= end) {  // chunk past nnz: the reference flushes 0 into row M-1
-                nwb += V;
+                // (not nnz-one at r = 1, owner 3: its lanes past nnz break
+                // before the atomic, cuda_nnz_one_serial.cu)
+                if (owner != 3) nwb += V;
                 continue;
             }
-            const Owner own{rp, rowid, base, end, nnz, M, owner != 0};
+            // owner == 2: nnz-one's segment groups walked as g = r chunks (hw
+            // variant 1 of nnz-one): the group straddling nnz also holds
+            // zero-extended lanes of row M-1, a run of their own unless the
+            // last real row is M-1 (cuda_nnz_one_segment.cu padding)
+            if (owner == 2 && end == nnz && base + g > nnz &&
+                (__ldg(rowid + nnz - 1) & kRowMask) != M - 1)
+                nwb += V;
+            const Owner own{rp, rowid, base, end, nnz, M, owner == 1};  // 2/3: red only
             if constexpr (RP) {
                 const int cur = __ldg(chunk_rows + ch);
                 const long long kcol = (long long)tile * V;
@@ -1465,7 +1474,7 @@ k_nnz_multiple_staged(const int *__restrict__ rowid, const int *__restrict__ ci,
                 if (on) nwb += V;
                 continue;
             }
-            const Owner own{rp, rowid, base, end, nnz, M, owner != 0};
+            const Owner own{rp, rowid, base, end, nnz, M, owner == 1};
             const int r_first = __ldg(rowid + base);
             if ((r_first & kExactFlag) && __ldg(rowid + end - 1) == r_first) {  // the exact kernel's
                 if (on) {
@@ -1584,7 +1593,7 @@ k_nnz_multiple_tma(const int *__restrict__ rowid, const int *__restrict__ ci,
                         nwb += V;
                         continue;
                     }
-                    const Owner own{rp, rowid, p0 + q0, p0 + qend, nnz, M, owner != 0};
+                    const Owner own{rp, rowid, p0 + q0, p0 + qend, nnz, M, owner == 1};
                     const int r_first = SA.row(q0);
                     if ((r_first & kExactFlag) && SA.row(qend - 1) == r_first) {  // exact kernel's
                         if (own.on && __ldg(rp + (r_first & kRowMask)) == own.base)

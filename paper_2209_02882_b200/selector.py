@@ -112,6 +112,10 @@ def candidates(n: int, p_values=(256, 1024), g_values=GPU_G_VALUES,
                 # 9: 1 + the plan's cold-column cache hints (B >> L2: config 5)
                 vs = (1, 5, 9, 2, 3) if n // tpl.c >= 32 else (1, 5, 9, 2)
                 out.extend(Candidate(str(pt), p, 0, v) for v in vs)
+            elif variants and tpl.family == "nnz-one":
+                # 0: the shuffle segment scan; 1: each segment group walked
+                # serially by lanes along the columns (full-row gathers)
+                out.extend(Candidate(str(pt), p, 0, v) for v in (0, 1))
             elif variants and tpl.family == "row-multiple" and n // tpl.c <= 256:
                 # 6/7: a warp per 4/8-row block walking the union of the
                 # block's columns (rows <= 64; stencils / meshes)

@@ -335,3 +335,42 @@ def test_device_shard_cuts_bit_exact(k):
     for rp in cases:
         got = shard_starts_device(torch.as_tensor(rp.astype(np.int32), device="cuda"), k)
         assert np.array_equal(got.cpu().numpy(), shard_starts(rp, k)), (k, rp[:8])
+
+
+def test_nnz_one_segment_walk_variant(zoo):
+    """nnz-one hw variant 1: every aligned segment group walked serially by
+    lanes along the columns (the register walk with g = r) instead of the
+    shuffle scan -- identical writeback counts to the reference simulator
+    on the zoo (including the padded tail group), both precisions, and on
+    config 1 against the oracle's writeback restatement."""
+    sim = {(r["matrix"], r["n"], r["point"]): r for r in
+           json.loads((GOLDEN / "sim_metrics.json").read_text())}
+    golden = np.load(GOLDEN / "zoo_oracle.npz")
+    runs = 0
+    for n in (4, 8):
+        cfg = KernelConfig(n=n, p=256)
+        pts = [pt for pt in templated(n, 256) if str(pt).startswith("nnz:1,")]
+        assert pts
+        for label, mat, b_seed in zoo:
+            b = random_dense(mat.num_cols, n, seed=b_seed)
+            want32 = oracle_f32(mat, b, n)
+            for pt in pts:
+                k = build_kernel(pt, cfg, mat)
+                got, m = run(k, mat, b, precision="single", hw_variant=1)
+                assert oracle.max_rel_error(got.vals, want32) <= F32_TOL, (label, str(pt))
+                assert m.atomic_ops == sim[(label, n, str(pt))]["atomic_ops"], (label, n, str(pt))
+                got64, m64 = run(k, mat, b, precision="double", hw_variant=1)
+                assert oracle.max_rel_error(got64.vals, golden[f"{label}|{n}"]) <= F64_TOL
+                assert m64.atomic_ops == m.atomic_ops
+                runs += 1
+    a = random_csr(4096, 4096, 0.01, seed=1)
+    b = random_dense(4096, 32, seed=2)
+    want = oracle_f32(a, b, 32)
+    for text, p in (("nnz:1,col:4,r:8", 256), ("nnz:1,col:1,r:32", 1024), ("nnz:1,col:2,r:1", 256)):
+        k = build_kernel(parse_point(text), KernelConfig(32, p), a)
+        got, m = run(k, a, b, precision="single", hw_variant=1)
+        assert oracle.max_rel_error(got.vals, want) <= F32_TOL, text
+        st = oracle.block_starts(a.row_ptr, k.chunk, k.grid_size)
+        assert m.atomic_ops == oracle.writebacks(k.family, a.row_ptr, 32, k.grid_size, starts=st,
+                                                 npb=k.chunk, r=k.r), text
+    print("nnz-one segment walk:", runs, "zoo runs")

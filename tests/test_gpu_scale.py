@@ -75,6 +75,9 @@ def test_config2_long_chunk_walks():
     g = G.rmat(20, 16, seed=1, device="cuda")
     pts = [(t, 256, v, split) for t in ("nnz:512,col:4,r:1", "nnz:2048,col:4,r:1", "nnz:128,col:4,r:1")
            for v in (1, 3, 4, 5) for split in (False, True)]
+    # nnz-one's segment groups as a serial walk (variant 1), hub rows in the table
+    pts += [("nnz:1,col:4,r:8", 1024, 1, False), ("nnz:1,col:4,r:32", 1024, 1, False),
+            ("nnz:1,col:4,r:1", 256, 1, False)]
     pts += [("nnz:128,col:4,r:1", 256, 2, False), ("nnz:64,col:2,r:1", 1024, 3, True)]
     print(_check(g, 128, pts))
 

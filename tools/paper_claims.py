@@ -50,6 +50,8 @@ def best_of(a, b, c, n, pts, rp):
         for p in (256, 1024):
             if algorithm_template(parse_point(text), KernelConfig(n=n, p=p)) is not None:
                 cands.append(Candidate(text, p))
+                if text.startswith("nnz:1,"):  # the segment-group family's serial-walk mapping
+                    cands.append(Candidate(text, p, 0, 1))
     if not cands:
         return None, None
     res = autotune(a, b, c, n, cands, reps=5, row_ptr_host=rp)
