@@ -41,7 +41,8 @@ for n, s in grid["summary"].items():
     p = paper.get(str(n), ("-", "-"))
     out.append(f"| {n} | {s['tuned_vs_default_geomean']:.2f} ({s['tuned_vs_default_max']:.2f}) | "
                f"`{s['best_static']}` | {s['dynamic_vs_static_geomean']:.2f} | tuned {p[0]}; dynamic {p[1]} |")
-out += ["", "Reading: on B200 the tuned grid beats dgSPARSE's default cell by more than on the paper's "
+out += ["", "Segment groups are timed with both hardware mappings of the nnz-one family (the shuffle scan and the serial segment walk, hw variants 0/1) and the faster one is reported.  ", "",
+        "Reading: on B200 the tuned grid beats dgSPARSE's default cell by more than on the paper's "
         "GPUs at large N (the default gives every 4-column vector of a row its own 32-lane warp, so wide "
         "B rows are gathered 16 bytes per lane), and by about the paper's margin at N = 4-16; a per-"
         "matrix choice beats the best single static cell by 1.25-1.75x, i.e. at or above the paper's "
