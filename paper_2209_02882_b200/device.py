@@ -20,11 +20,35 @@ import torch
 from . import _native
 from .lowering import LoweredKernel
 
-__all__ = ["DeviceCsr", "KernelAux", "kernel_struct", "device_block_starts", "prepare_aux", "spmm",
+__all__ = ["host_cast", "host_widen", "DeviceCsr", "KernelAux", "kernel_struct", "device_block_starts", "prepare_aux", "spmm",
            "plan_workspace_bytes", "validate_csr", "spmm_rbpr_grid",
            "launches_per_call", "reference_spmm_f64", "torch_dtype", "native_dtype", "require_cuda"]
 
 _INT32_MAX = 2**31 - 1
+
+
+_TORCH_DT = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64,
+             np.dtype(np.int32): torch.int32, np.dtype(np.int64): torch.int64}
+
+
+def host_cast(x, dt) -> torch.Tensor:
+    """A contiguous host tensor of numpy dtype ``dt`` from array-like ``x``;
+    the element conversion runs on torch's CPU thread pool (the reference's
+    float64 / int64 host layout to the device layout: config 5's 8.6 GB B
+    takes ~2.8 s through numpy's single-threaded astype)."""
+    a = np.asarray(x)
+    if not a.flags.c_contiguous:
+        a = np.ascontiguousarray(a)
+    t = torch.from_numpy(a)
+    want = _TORCH_DT[np.dtype(dt)]
+    return t if t.dtype == want else t.to(want)
+
+
+def host_widen(t: torch.Tensor) -> np.ndarray:
+    """Device result -> float64 numpy on the host: download in the value
+    dtype (half the bytes for float32), widen on the CPU thread pool."""
+    h = t.cpu()
+    return (h if h.dtype == torch.float64 else h.to(torch.float64)).numpy()
 
 
 def require_cuda(device=None) -> torch.device:
@@ -85,7 +109,7 @@ class DeviceCsr:
         np_dt = np.float32 if dtype == torch.float32 else np.float64
 
         def up(x, dt):
-            t = torch.from_numpy(np.ascontiguousarray(x, dtype=dt))
+            t = host_cast(x, dt)
             if non_blocking:
                 t = t.pin_memory()
             return t.to(dev, non_blocking=non_blocking)

@@ -30,8 +30,8 @@ import numpy as np
 import torch
 
 from . import _native
-from .device import (DeviceCsr, native_dtype, prepare_aux, require_cuda, spmm, torch_dtype,
-                     validate_csr)
+from .device import (DeviceCsr, host_cast, host_widen, native_dtype, prepare_aux, require_cuda,
+                     spmm, torch_dtype, validate_csr)
 from .lowering import LoweredKernel
 from .matrices import DenseMatrix
 from .space import parse_point
@@ -113,11 +113,11 @@ def run(kernel, a, b, c0=None, *, precision: str = "double", device=None,
     dev = require_cuda(device)
     np_dt = np.float32 if dt == torch.float32 else np.float64
     da = DeviceCsr.from_host(a, dtype=dt, device=dev)
-    db = torch.from_numpy(np.ascontiguousarray(np.asarray(b.vals, dtype=np_dt).reshape(a.num_cols, n))).to(dev)
+    db = host_cast(b.vals, np_dt).reshape(a.num_cols, n).to(dev)
     if c0 is None:
         dc = torch.empty((a.num_rows, n), dtype=dt, device=dev)
     else:
-        dc = torch.from_numpy(np.asarray(c0.vals, dtype=np_dt).reshape(a.num_rows, n).copy()).to(dev)
+        dc = host_cast(c0.vals, np_dt).reshape(a.num_rows, n).to(dev)  # a copy: c0 is not aliased
     wb = torch.zeros(1, dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream(dev)
     # the simulator faults on an out-of-range index (sim.py:279-287) instead of
@@ -135,7 +135,7 @@ def run(kernel, a, b, c0=None, *, precision: str = "double", device=None,
          hw_block=hw_block, hw_variant=hw_variant, stream=stream)
     t1.record(stream)
     t1.synchronize()
-    out = DenseMatrix(a.num_rows, n, dc.double().cpu().numpy().reshape(-1))
+    out = DenseMatrix(a.num_rows, n, host_widen(dc).reshape(-1))
     metrics = GpuMetrics(atomic_ops=int(wb.item()), device_ms=float(t0.elapsed_time(t1)),
                          grid_size=k.grid_size, block_size=k.block_size, family=k.family)
     return out, metrics
