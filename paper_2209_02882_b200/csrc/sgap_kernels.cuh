@@ -736,6 +736,16 @@ struct GlobalA {
         ldg_vec<T, 4>(v, av + u);
         // (evict-first A loads, __ldcs: 0.833 vs 0.700 ms on config 2)
     }
+    // split loads for the column-pipelined row_ptr walk: the columns of the
+    // next batch go out before this batch's gathers are consumed
+    template <typename I>
+    __device__ __forceinline__ int4 load4c(I q) const {
+        return __ldg(reinterpret_cast<const int4 *>(ci + (unsigned)q));
+    }
+    template <typename I>
+    __device__ __forceinline__ void load4v(I q, Vec<T, 4> &v) const {
+        ldg_vec<T, 4>(v, av + (unsigned)q);
+    }
     // (col, val) only: the row_ptr-tracking walk needs no per-position row ids
     template <typename I>
     __device__ __forceinline__ void load4cv(I q, int4 &c, Vec<T, 4> &v) const {
@@ -1009,38 +1019,41 @@ __device__ __forceinline__ void eb_walk4_rp(const GlobalA<T> &A, const int *__re
         } while (ce <= p);
         here = own.on;
     };
-    auto batch4 = [&](unsigned qq) {
-        int4 c;
-        Vec<T, 4> v;
-        A.load4cv(qq, c, v);
-        Vec<T, V> b0, b1, b2, b3;
-        gather_b<T, V, HINT>(b0, bk, c.x, N);
-        gather_b<T, V, HINT>(b1, bk, c.y, N);
-        gather_b<T, V, HINT>(b2, bk, c.z, N);
-        gather_b<T, V, HINT>(b3, bk, c.w, N);
-        if (qq + 3 < ce) {
-            fma_vec<T, V>(acc, v.v[0], b0);
-            fma_vec<T, V>(acc, v.v[1], b1);
-            fma_vec<T, V>(acc, v.v[2], b2);
-            fma_vec<T, V>(acc, v.v[3], b3);
-        } else {
-            const Vec<T, V> *bb[4] = {&b0, &b1, &b2, &b3};
+    {  // column-pipelined: the next batch's 16-byte column load goes out
+       // before this batch's gathers, so the gather addresses do not wait on
+       // an L2 round trip for their columns (ncu, config 2: 10.5% of the
+       // stall samples sat on that address computation; interleaved A/B:
+       // config 3 -3.5%, config 5 (with hints) -2%)
+        int4 cn = make_int4(0, 0, 0, 0);
+        if (q + 4 <= qe) cn = A.load4c(q);
+        bool odd = false;
+        for (; q + 4 <= qe; q += 4) {
+            const int4 c = cn;
+            if (q + 8 <= qe) cn = A.load4c(q + 4);
+            if ((q & 31) == 0 && q + 64 < qe) A.prefetch_cv(q + 64);
+            Vec<T, V> b0, b1, b2, b3;
+            gather_b<T, V, HINT>(b0, bk, c.x, N);
+            gather_b<T, V, HINT>(b1, bk, c.y, N);
+            gather_b<T, V, HINT>(b2, bk, c.z, N);
+            gather_b<T, V, HINT>(b3, bk, c.w, N);
+            Vec<T, 4> v;
+            A.load4v(q, v);
+            if (q + 3 < ce) {
+                fma_vec<T, V>(acc, v.v[0], b0);
+                fma_vec<T, V>(acc, v.v[1], b1);
+                fma_vec<T, V>(acc, v.v[2], b2);
+                fma_vec<T, V>(acc, v.v[3], b3);
+            } else {
+                const Vec<T, V> *bb[4] = {&b0, &b1, &b2, &b3};
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                if (qq + u >= ce) advance(qq + u);
-                fma_vec<T, V>(acc, v.v[u], *bb[u]);
+                for (int u = 0; u < 4; ++u) {
+                    if (q + u >= ce) advance(q + u);
+                    fma_vec<T, V>(acc, v.v[u], *bb[u]);
+                }
             }
+            if (odd) fold<T, V>(tot, acc);
+            odd = !odd;
         }
-    };
-    for (; q + 8 <= qe; q += 8) {
-        if ((q & 31) == 0 && q + 64 < qe) A.prefetch_cv(q + 64);
-        batch4(q);
-        batch4(q + 4);
-        fold<T, V>(tot, acc);
-    }
-    if (q + 4 <= qe) {
-        batch4(q);
-        q += 4;
     }
     for (; q < qe; ++q) {  // < 4 tail positions
         Vec<T, V> b;
