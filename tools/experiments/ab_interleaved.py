@@ -23,9 +23,11 @@ ap.add_argument("--variants", default="1,9,5")
 ap.add_argument("--rounds", type=int, default=6)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--probe-h", type=int, default=0)
+ap.add_argument("--n", type=int, default=0)
+ap.add_argument("--hints", action="store_true", help="force the planner's cold-column hints")
 args = ap.parse_args()
 dev = torch.device("cuda", 0)
-n = bench.default_n(args.config)
+n = args.n or bench.default_n(args.config)
 g, desc, _ = bench.build_workload(args.config, 1, 1, dev)
 a = DeviceCsr(g.num_rows, g.num_cols, g.row_ptr.to(torch.int32), g.col_idx.to(torch.int32),
               g.vals.to(torch.float32))
@@ -34,8 +36,9 @@ torch.cuda.empty_cache()
 b = bench.dense_b(a.num_cols, n, 1, dev)
 c = torch.empty((a.num_rows, n), dtype=torch.float32, device=dev)
 rp = a.row_ptr.cpu().numpy().astype(np.int64)
-k = plan_for(Candidate(args.point, 256), n, a.num_rows, a.num_cols, rp)
-aux = prepare_aux(k, a)
+from paper_2209_02882_b200.selector import _first_p  # noqa: E402
+k = plan_for(Candidate(args.point, _first_p(args.point, n)), n, a.num_rows, a.num_cols, rp)
+aux = prepare_aux(k, a, l2_hints=True if args.hints else None)
 arms = [(f"v{v}", a, aux, int(v)) for v in args.variants.split(",")]
 if args.probe_h:
     counts = torch.bincount(a.col_idx.long(), minlength=a.num_cols)

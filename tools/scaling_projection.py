@@ -35,7 +35,7 @@ n = 128
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 res = []
 for world in [int(w) for w in args.worlds.split(",")]:
-    g, desc, _ = bench.build_workload(5 if args.strong else 2, 1 if args.strong else world, 1, dev)
+    g, desc, _ = bench.build_workload(5 if args.strong else 2, world, 1, dev, weak=not args.strong)
     plan = plan_shards(g.row_ptr.cpu().numpy(), world)
     b = bench.dense_b(g.num_cols, n, 1, dev)
     times = []
