@@ -192,13 +192,19 @@ def heuristic(stats: MatrixStats, n: int) -> Candidate:
         return Candidate(pt, _first_p(pt, n) or 256)
     c = widest if n >= 16 else min(widest, max(1, n // 4))
     g = max(32, min(512, _pow2_floor(stats.nnz / 40_000)))
-    # the register walk's flavour by the size of B against the L2 (round-2
-    # interleaved A/B, profiles/r02_ab_*): B within L2 -> row_ptr tracking
-    # (config 3), B a few L2s -> row ids (config 2: latency-bound, row
-    # changes every ~16 positions), B >> L2 -> row_ptr tracking + cold-column
-    # cache hints (config 5: DRAM-bound)
+    # the register walk's flavour (round-2 interleaved A/B, profiles/r02_ab_*):
+    # B far beyond the L2 -> row_ptr tracking + cold-column cache hints
+    # (config 5: DRAM-bound, -4.5%); short rows with many empty rows -> the
+    # per-position row ids (config 2: every row change of the row_ptr walk
+    # waits on row_ptr loads, 56% / 48% empty rows); otherwise row_ptr
+    # tracking with the column-pipelined batches (config 3 at N = 64 / 256)
     b_bytes = stats.num_cols * n * 4
-    variant = 1 if b_bytes <= L2_BYTES else (5 if b_bytes <= 16 * L2_BYTES else 9)
+    if b_bytes > 16 * L2_BYTES:
+        variant = 9
+    elif stats.mean_row < 32 and stats.empty_frac > 0.2:
+        variant = 5
+    else:
+        variant = 1
     for gg in (g, 256, 128, 64, 32):
         pt = f"nnz:{gg},col:{col(c)},r:1"
         p = _first_p(pt, n)

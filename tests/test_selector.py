@@ -26,11 +26,13 @@ CHUNGLU = MatrixStats(232965, 232965, 114492479, 491.5, 3.0, 76000, 0.0)
 
 def test_heuristic_matrix_classes():
     assert heuristic(RMAT20, 128).point.startswith("nnz:")      # power law -> EB walk
-    # register-walk flavour by B against L2: row ids (config 2), row_ptr +
-    # cold-column hints (config 5), row_ptr (config 3)
+    # register-walk flavour: row ids (config 2: short rows, many empty),
+    # row_ptr + cold-column hints (config 5: B >> L2), row_ptr (config 3)
     assert heuristic(RMAT20, 128).hw_variant == 5
+    assert heuristic(RMAT20, 8).hw_variant == 5
     assert heuristic(RMAT24, 128).hw_variant == 9
     assert heuristic(CHUNGLU, 64).hw_variant == 1
+    assert heuristic(CHUNGLU, 256).hw_variant == 1
     assert heuristic(STENCIL160, 128).point.startswith("row:4")  # regular -> RB
     assert heuristic(STENCIL160, 4).point == "row:1,col:4,r:1"
     assert heuristic(UNIFORM1, 4).point == "row:1/8,col:1,r:8"    # flexible group beats r=32
