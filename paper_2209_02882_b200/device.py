@@ -20,7 +20,7 @@ import torch
 from . import _native
 from .lowering import LoweredKernel
 
-__all__ = ["host_cast", "host_widen", "DeviceCsr", "KernelAux", "kernel_struct", "device_block_starts", "prepare_aux", "spmm",
+__all__ = ["host_cast", "host_widen", "DeviceCsr", "KernelAux", "SpmmGraph", "kernel_struct", "device_block_starts", "prepare_aux", "spmm",
            "plan_workspace_bytes", "validate_csr", "spmm_rbpr_grid",
            "launches_per_call", "reference_spmm_f64", "torch_dtype", "native_dtype", "require_cuda"]
 
@@ -347,6 +347,36 @@ def spmm_rbpr_grid(k: LoweredKernel, a: DeviceCsr, b: torch.Tensor, c: torch.Ten
         float(worker_scale), 1 if accumulate else 0,
         writebacks.data_ptr() if writebacks is not None else None, _stream_handle(stream))
     _native.check(st, "sgap_run_rbpr_grid")
+
+
+class SpmmGraph:
+    """One planned SpMM call captured as a CUDA graph and replayed: for
+    repeated products on the same structure (iterative solvers, GNN layers)
+    the whole call -- zero-fill, walk, long-row fold -- becomes one graph
+    launch with no per-kernel host work.  ``sgap_run`` neither allocates nor
+    synchronises, so it is capturable once the plan exists.  The captured
+    call reads ``a.vals`` / ``b`` and writes ``c`` at their current
+    addresses: update those tensors in place between replays."""
+
+    def __init__(self, k: LoweredKernel, a: DeviceCsr, b: torch.Tensor, c: torch.Tensor, *,
+                 aux: KernelAux | None = None, accumulate: bool = False, hw_block: int = 0,
+                 hw_variant: int = 0):
+        self.k, self.a, self.b, self.c = k, a, b, c
+        self.aux = aux if aux is not None else prepare_aux(k, a)
+        side = torch.cuda.Stream(a.device)
+        side.wait_stream(torch.cuda.current_stream(a.device))
+        with torch.cuda.stream(side):  # warm-up outside the capture (lazy loading)
+            spmm(k, a, b, c, accumulate=accumulate, aux=self.aux, hw_block=hw_block,
+                 hw_variant=hw_variant, stream=side)
+        torch.cuda.current_stream(a.device).wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            spmm(k, a, b, c, accumulate=accumulate, aux=self.aux, hw_block=hw_block,
+                 hw_variant=hw_variant, stream=torch.cuda.current_stream(a.device))
+
+    def replay(self) -> torch.Tensor:
+        self.graph.replay()
+        return self.c
 
 
 def launches_per_call(k: LoweredKernel, aux: KernelAux | None, *, accumulate: bool = False,

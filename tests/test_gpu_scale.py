@@ -303,3 +303,29 @@ def test_cold_column_hint_walk():
         from paper_2209_02882_b200 import _native
         with pytest.raises(_native.SgapError):
             spmm(k, a, b, c, aux=prepare_aux(k, a, l2_hints=False), hw_variant=9)
+
+
+def test_cuda_graph_replay_matches_direct_calls():
+    """SpmmGraph: a planned call captured once and replayed (new values and
+    B written in place between replays) gives the direct call's results for
+    the EB walk (zero-fill + walk + long-row fold) and an RB walk."""
+    from paper_2209_02882_b200.device import SpmmGraph
+    g = G.rmat(16, 16, seed=8, device="cuda")
+    a = _device(g)
+    rp = a.row_ptr.cpu().numpy().astype(np.int64)
+    n = 64
+    b = torch.rand((a.num_cols, n), device="cuda") * 2 - 1
+    c = torch.empty((a.num_rows, n), device="cuda")
+    for text, p, v in (("nnz:256,col:4,r:1", 256, 1), ("row:2,col:2,r:1", 256, 4)):
+        k = lower(algorithm_template(parse_point(text), KernelConfig(n=n, p=p)),
+                  _Rp(a.num_rows, a.num_cols, rp), compute_starts=False)
+        gr = SpmmGraph(k, a, b, c, hw_variant=v)
+        for step in range(3):
+            a.vals.mul_(-1.0 if step % 2 else 0.5)   # new values, same structure
+            b.add_(0.25)
+            c.fill_(float("nan"))
+            gr.replay()
+            torch.cuda.synchronize()
+            want = oracle.spmm_f64(rp.astype(np.int32), a.col_idx.cpu().numpy(),
+                                   a.vals.cpu().numpy(), b.cpu().numpy(), n)
+            assert oracle.max_rel_error(c.cpu().numpy(), want) <= TOL, (text, step)
