@@ -47,8 +47,10 @@ def main():
             best = res[0]
             rec = {"matrix": label, "n": n, "nnz": a.nnz, "stats": st.as_dict(),
                    "best": best[0].label(), "best_ms": best[1], "heuristic": h.label(),
-                   "heuristic_ms": ht, "regret": ht / best[1], "candidates": len(res)}
-            print(json.dumps(rec), flush=True)
+                   "heuristic_ms": ht, "regret": ht / best[1], "candidates": len(res),
+                   # every candidate's time, so a revised heuristic can be scored offline
+                   "times": {cd.label(): ms for cd, ms in res}}
+            print(json.dumps({k: v for k, v in rec.items() if k != "times"}), flush=True)
             rows.append(rec)
             del b, c
         del a
