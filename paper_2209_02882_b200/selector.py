@@ -183,15 +183,29 @@ def heuristic(stats: MatrixStats, n: int) -> Candidate:
             if p is not None:
                 return Candidate(pt, p)
         if n >= 16:
-            pt = f"row:4,col:{col(widest)},r:1"
+            # 8 rows per logical thread from N = 64 (stencil 64^3 N=64, config 4
+            # N=128: the round-2 sweeps), 4 below (config 4 N=16)
+            pt = f"row:{8 if n >= 64 else 4},col:{col(widest)},r:1"
             p = _first_p(pt, n)
             if p is not None:
-                # a warp per row when N/c == 32 (config 4 N=128: 3.35 vs 3.82 ms)
-                return Candidate(pt, p, 0, 4 if n // widest == 32 else 2)
+                # a warp per row when N/c == 32 (config 4 N=128: 3.35 vs 3.82 ms),
+                # the logical mapping at N/c == 16 (config 4 / stencil 64^3 at
+                # N=64), adjacent rows per CTA step below (config 4 N=16)
+                lanes = n // widest
+                return Candidate(pt, p, 0, 4 if lanes == 32 else (0 if lanes >= 16 else 2))
         pt = f"row:1,col:{col(widest)},r:1"
         return Candidate(pt, _first_p(pt, n) or 256)
     c = widest if n >= 16 else min(widest, max(1, n // 4))
-    g = max(32, min(512, _pow2_floor(stats.nnz / 40_000)))
+    if n <= 4:
+        # narrow B on power-law rows: segment groups of 16, walked serially
+        # (nnz-one variant 1; R-MAT s18 N=4 best of the whole sweep)
+        pt = f"nnz:1,col:{col(c)},r:16"
+        p = _first_p(pt, n)
+        if p is not None:
+            return Candidate(pt, p, 0, 1)
+    # long chunks amortise the walk on wide B; narrow B wants more, shorter
+    # chunks (config 2 / Chung-Lu at N = 8: g = 64)
+    g = 64 if n <= 16 else max(32, min(512, _pow2_floor(stats.nnz / 40_000)))
     # the register walk's flavour (round-2 interleaved A/B, profiles/r02_ab_*):
     # B far beyond the L2 -> row_ptr tracking + cold-column cache hints
     # (config 5: DRAM-bound, -4.5%); short rows with many empty rows -> the

@@ -33,8 +33,13 @@ def test_heuristic_matrix_classes():
     assert heuristic(RMAT24, 128).hw_variant == 9
     assert heuristic(CHUNGLU, 64).hw_variant == 1
     assert heuristic(CHUNGLU, 256).hw_variant == 1
-    assert heuristic(STENCIL160, 128).point.startswith("row:4")  # regular -> RB
+    assert heuristic(STENCIL160, 128).point.startswith("row:8")  # regular -> RB
+    assert heuristic(STENCIL160, 128).hw_variant == 4             # warp per row
+    assert heuristic(STENCIL160, 16).point.startswith("row:4")
     assert heuristic(STENCIL160, 4).point == "row:1,col:4,r:1"
+    # narrow B on power-law rows: serial segment groups; N=8: short chunks
+    assert (heuristic(RMAT20, 4).point, heuristic(RMAT20, 4).hw_variant) == ("nnz:1,col:1,r:16", 1)
+    assert heuristic(RMAT20, 8).point.startswith("nnz:64,")
     assert heuristic(UNIFORM1, 4).point == "row:1/8,col:1,r:8"    # flexible group beats r=32
     assert heuristic(UNIFORM1, 32).point == "row:1/2,col:2,r:2"
 
@@ -50,4 +55,3 @@ def test_candidate_grid_covers_families_and_walks():
     # row-multiple: logical / interleaved, plus a warp per row where N/c == 32
     assert {c.hw_variant for c in cands if c.point.startswith("row:4,col:4")} == {0, 2, 4, 6, 7}
     assert {c.hw_variant for c in cands if c.point.startswith("row:4,col:2")} == {0, 2}
-    assert heuristic(STENCIL160, 128).hw_variant == 4
