@@ -44,4 +44,4 @@ def score(path=ROOT / "profiles" / "r02_selector_regret_full.json", verbose=True
 
 
 if __name__ == "__main__":
-    score()
+    score(sys.argv[1] if len(sys.argv) > 1 else ROOT / "profiles" / "r02_selector_regret_full.json")

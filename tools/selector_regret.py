@@ -25,13 +25,24 @@ CASES = [
 ]
 
 
+# matrices the heuristic was NOT fitted on (other sizes, seeds, widths)
+HOLDOUT = [
+    ("uniform 8192 x 40/row", lambda d: G.uniform_random(8192, 8192, 40.0, seed=7, device=d), (8, 64)),
+    ("rmat s19 seed 5", lambda d: G.rmat(19, 16, seed=5, device=d), (4, 16, 128)),
+    ("rmat s21 unpermuted", lambda d: G.rmat(21, 8, seed=2, permute=False, device=d), (32, 128)),
+    ("stencil 96^3", lambda d: G.stencil27(96, device=d), (8, 32, 256)),
+    ("chung-lu 300k", lambda d: G.chung_lu(300_000, 3e7, seed=3, device=d), (16, 128)),
+]
+
+
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--holdout", action="store_true", help="score on matrices not used for fitting")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     rows = []
-    for label, make, ns in CASES:
+    for label, make, ns in (HOLDOUT if args.holdout else CASES):
         g = make(dev)
         a = DeviceCsr(g.num_rows, g.num_cols, g.row_ptr.to(torch.int32), g.col_idx.to(torch.int32),
                       g.vals.to(torch.float32))
