@@ -50,7 +50,10 @@ def main():
                   torch.from_numpy(vals.astype(np.float32)).to(dev))
     assert validate_csr(a) is None
     cases = [
-        ("nnz:64,col:4,r:1", 256, 1), ("nnz:64,col:4,r:1", 256, 2), ("nnz:256,col:4,r:1", 1024, 3),
+        ("nnz:64,col:4,r:1", 256, 1), ("nnz:64,col:4,r:1", 256, 5), ("nnz:64,col:4,r:1", 256, 9),
+        ("nnz:1,col:4,r:8", 1024, 1), ("nnz:1,col:4,r:1", 256, 1),
+        ("row:4,col:4,r:1", 256, 6), ("row:4,col:4,r:1", 256, 7),
+        ("nnz:64,col:4,r:1", 256, 2), ("nnz:256,col:4,r:1", 1024, 3),
         ("nnz:256,col:4,r:1", 1024, 4), ("nnz:6,col:1,r:1", 256, 1), ("nnz:512,col:4,r:1", 256, 1),
         ("nnz:1,col:4,r:8", 1024, 0), ("nnz:1,col:4,r:1", 256, 0), ("nnz:1,col:1,r:32", 1024, 0),
         ("row:1,col:4,r:1", 256, 0), ("row:4,col:4,r:1", 256, 2), ("row:4,col:4,r:1", 256, 3),
@@ -73,7 +76,9 @@ def main():
                 if variant in (3, 4) and (n // tpl.c) < 32:
                     continue
                 kk = lower(tpl, _Rp(m, k, rp), compute_starts=False)
-                aux = prepare_aux(kk, aa, validate=True)
+                aux = prepare_aux(kk, aa, validate=True, l2_hints=True)
+                if variant in (6, 7) and not aux.plan.aux.d_union_off4:
+                    continue  # rows > 64: no union plan (the hub rows of this matrix)
                 for acc in (False, True):
                     c.zero_() if acc else c.fill_(float("nan"))
                     spmm(kk, aa, bb, c, aux=aux, accumulate=acc, hw_variant=variant)
