@@ -86,6 +86,30 @@ def main():
                     tol = 1e-5 if prec == torch.float32 else 1e-12
                     assert err <= tol, (text, variant, n, prec, acc, err)
             print("n", n, "ok")
+    # the row-blocked union walk (row-multiple variants 6/7) needs rows <= 64:
+    # a banded matrix with empty rows and M not a multiple of 8
+    rng = np.random.default_rng(5)
+    m2, k2 = 203, 400
+    lens2 = rng.integers(0, 30, m2)
+    lens2[::13] = 0
+    rp2 = np.concatenate([[0], np.cumsum(lens2)]).astype(np.int64)
+    cols2 = np.concatenate([np.sort(rng.choice(np.arange(max(0, i * 2 - 40), max(0, i * 2 - 40) + 80),
+                                               int(L), replace=False)) for i, L in enumerate(lens2) if L])
+    a2 = DeviceCsr(m2, k2, torch.from_numpy(rp2.astype(np.int32)).to(dev),
+                   torch.from_numpy(cols2.astype(np.int32)).to(dev),
+                   torch.from_numpy(rng.uniform(-1, 1, rp2[-1]).astype(np.float32)).to(dev))
+    b2 = torch.rand((k2, 128), device=dev) * 2 - 1
+    want2 = oracle.spmm_f64(rp2.astype(np.int32), cols2.astype(np.int32), a2.vals.cpu().numpy(),
+                            b2.cpu().numpy(), 128)
+    c2 = torch.empty((m2, 128), device=dev)
+    for variant in (6, 7):
+        kk = lower(algorithm_template(parse_point("row:4,col:4,r:1"), KernelConfig(n=128, p=256)),
+                   _Rp(m2, k2, rp2), compute_starts=False)
+        aux = prepare_aux(kk, a2, validate=True)
+        c2.fill_(float("nan"))
+        spmm(kk, a2, b2, c2, aux=aux, hw_variant=variant)
+        assert oracle.max_rel_error(c2.cpu().numpy(), want2) <= 1e-5, variant
+    print("union walk ok")
     # group primitives
     out = np.zeros(16)
     assert exec_seg_reduce_group(np.array([5, 5, 7, 7]), np.array([1.0, 2, 3, 4]), out, group_size=4) == 2
