@@ -27,6 +27,9 @@ ap.add_argument("--point", default="nnz:512,col:4,r:1")
 ap.add_argument("--variant", type=int, default=1)
 ap.add_argument("--worlds", default="1,2,4,8")
 ap.add_argument("--strong", action="store_true", help="config 5 strong scaling instead")
+ap.add_argument("--unpermuted", action="store_true",
+                help="strong scaling on the UNPERMUTED R-MAT scale 24 (SURVEY 8(e) stress case)")
+ap.add_argument("--balance", default="nnz", choices=["nnz", "bytes"])
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--out", default="")
 args = ap.parse_args()
@@ -35,8 +38,14 @@ n = 128
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 res = []
 for world in [int(w) for w in args.worlds.split(",")]:
-    g, desc, _ = bench.build_workload(5 if args.strong else 2, world, 1, dev, weak=not args.strong)
-    plan = plan_shards(g.row_ptr.cpu().numpy(), world)
+    if args.unpermuted:
+        from paper_2209_02882_b200 import generators as G
+        g = G.rmat(24, 16, seed=1, permute=False, device=dev)
+        desc = f"R-MAT scale 24 unpermuted ({args.balance}-balanced shards)"
+    else:
+        g, desc, _ = bench.build_workload(5 if args.strong else 2, world, 1, dev,
+                                          weak=not args.strong)
+    plan = plan_shards(g.row_ptr.cpu().numpy(), world, balance=args.balance, n=n)
     b = bench.dense_b(g.num_cols, n, 1, dev)
     times = []
     for rank in range(world):
@@ -62,6 +71,7 @@ for world in [int(w) for w in args.worlds.split(",")]:
     t = max(x["ms"] for x in times)
     value = 2.0 * g.nnz * n / (t * 1e6)
     res.append({"world": world, "workload": desc, "nnz": g.nnz, "max_rank_ms": t,
+                "shard_rows": [x["rows"] for x in times],
                 "gflops": value, "ranks": times})
     print(f"W={world}: {desc}: max-rank {t:.3f} ms -> {value:.0f} GFLOP/s "
           f"(rank ms {min(x['ms'] for x in times):.3f}-{t:.3f})", flush=True)
