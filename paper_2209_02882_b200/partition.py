@@ -75,6 +75,30 @@ def bytes_balanced_starts(row_ptr, k: int, n: int) -> np.ndarray:
     return np.maximum.accumulate(np.minimum(starts, m))
 
 
+def cost_balanced_starts(row_ptr, k: int, slice_starts, slice_costs) -> np.ndarray:
+    """Cut points balancing a MEASURED cost: ``slice_starts`` (int[S+1] row
+    cuts of S calibration slices, e.g. shard_starts(row_ptr, 64)) and
+    ``slice_costs`` (S device times of each slice's SpMM on its own); cuts
+    fall on slice boundaries where the cumulative cost crosses c*total/k.
+    For matrices whose per-nonzero cost is far from uniform -- the
+    unpermuted R-MAT, where low-id rows gather the L2-resident hot columns
+    and high-id rows the cold ones, so nnz- and bytes-balanced shards differ
+    2.6x in time (profiles/r02_scaling_projection_unpermuted_*.json)."""
+    rp = np.asarray(row_ptr, dtype=np.int64)
+    m = rp.shape[0] - 1
+    ss = np.asarray(slice_starts, dtype=np.int64)
+    cost = np.asarray(slice_costs, dtype=np.float64)
+    if ss.shape[0] != cost.shape[0] + 1 or k < 1:
+        raise ValueError("slice_starts must have one more entry than slice_costs")
+    cum = np.concatenate([[0.0], np.cumsum(cost)])
+    out = np.empty(k + 1, dtype=np.int64)
+    out[0], out[k] = 0, m
+    for c in range(1, k):
+        j = int(np.argmin(np.abs(cum - cum[-1] * c / k)))
+        out[c] = ss[j]
+    return np.maximum.accumulate(np.minimum(out, m))
+
+
 @dataclass(frozen=True)
 class ShardPlan:
     starts: np.ndarray          # int64[k+1] row cut points
@@ -92,12 +116,20 @@ class ShardPlan:
         return int(self.nnz_end[g] - self.nnz_begin[g])
 
 
-def plan_shards(row_ptr, k: int, *, balance: str = "nnz", n: int = 0) -> ShardPlan:
+def plan_shards(row_ptr, k: int, *, balance: str = "nnz", n: int = 0,
+                calibration=None) -> ShardPlan:
+    """``balance``: "nnz" (the reference's compute_block_starts cuts),
+    "bytes" (A stream + C write), or "cost" with ``calibration`` =
+    (slice_starts, slice_costs) measured on the device."""
     rp = np.asarray(row_ptr, dtype=np.int64)
     if balance == "nnz":
         s = shard_starts(rp, k)
     elif balance == "bytes":
         s = bytes_balanced_starts(rp, k, n)
+    elif balance == "cost":
+        if calibration is None:
+            raise ValueError("balance='cost' needs calibration=(slice_starts, slice_costs)")
+        s = cost_balanced_starts(rp, k, *calibration)
     else:
         raise ValueError(f"unknown balance {balance!r}")
     return ShardPlan(s, rp[s[:-1]], rp[s[1:]])

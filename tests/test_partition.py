@@ -124,3 +124,18 @@ def test_gloo_world2_broadcast_and_gather():
         assert p.exitcode == 0
     assert all(ok for ok, _ in results)
     assert all(t == 2.0 for _, t in results)
+
+
+def test_cost_balanced_cuts_follow_measured_time():
+    from paper_2209_02882_b200.partition import cost_balanced_starts, plan_shards
+    rp = np.arange(0, 1001, dtype=np.int64) * 10      # 1000 rows, 10 nnz each
+    slices = np.arange(0, 1001, 100, dtype=np.int64)  # 10 calibration slices
+    costs = np.array([8, 1, 1, 1, 1, 1, 1, 1, 1, 4], dtype=np.float64)  # total 20
+    s = cost_balanced_starts(rp, 2, slices, costs)
+    assert list(s) == [0, 300, 1000]   # 8 + 1 + 1 = 10 of 20: the cut after the third slice
+    s4 = cost_balanced_starts(rp, 4, slices, costs)
+    assert s4[0] == 0 and s4[-1] == 1000 and np.all(np.diff(s4) >= 0)
+    plan = plan_shards(rp, 2, balance="cost", calibration=(slices, costs))
+    assert plan.rows(0) == (0, 300) and plan.nnz(0) == 3000
+    with pytest.raises(ValueError):
+        plan_shards(rp, 2, balance="cost")

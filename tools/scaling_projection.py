@@ -29,7 +29,8 @@ ap.add_argument("--worlds", default="1,2,4,8")
 ap.add_argument("--strong", action="store_true", help="config 5 strong scaling instead")
 ap.add_argument("--unpermuted", action="store_true",
                 help="strong scaling on the UNPERMUTED R-MAT scale 24 (SURVEY 8(e) stress case)")
-ap.add_argument("--balance", default="nnz", choices=["nnz", "bytes"])
+ap.add_argument("--balance", default="nnz", choices=["nnz", "bytes", "cost"])
+ap.add_argument("--slices", type=int, default=64, help="calibration slices for --balance cost")
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--out", default="")
 args = ap.parse_args()
@@ -45,7 +46,32 @@ for world in [int(w) for w in args.worlds.split(",")]:
     else:
         g, desc, _ = bench.build_workload(5 if args.strong else 2, world, 1, dev,
                                           weak=not args.strong)
-    plan = plan_shards(g.row_ptr.cpu().numpy(), world, balance=args.balance, n=n)
+    calib = None
+    if args.balance == "cost":  # time S nnz-balanced slices alone, cut on their cumulative time
+        rph_all = g.row_ptr.cpu().numpy()
+        cal_plan = plan_shards(rph_all, args.slices)
+        cb = bench.dense_b(g.num_cols, n, 1, dev)
+        costs = []
+        for sl in range(args.slices):
+            rp, ci, vals = shard_csr(g.row_ptr, g.col_idx, g.vals, cal_plan, sl)
+            lo, hi = cal_plan.rows(sl)
+            a = DeviceCsr(hi - lo, g.num_cols, rp.to(torch.int32).contiguous(),
+                          ci.to(torch.int32).contiguous(), vals.to(torch.float32).contiguous())
+            rph = a.row_ptr.cpu().numpy().astype(np.int64)
+            c = torch.empty((a.num_rows, n), dtype=torch.float32, device=dev)
+            k = plan_for(Candidate(args.point, 256), n, a.num_rows, a.num_cols, rph)
+            aux = prepare_aux(k, a)
+            spmm(k, a, cb, c, aux=aux, hw_variant=args.variant)
+            e0.record()
+            spmm(k, a, cb, c, aux=aux, hw_variant=args.variant)
+            e1.record()
+            e1.synchronize()
+            costs.append(e0.elapsed_time(e1))
+            del a, c, aux, rp, ci, vals
+        calib = (cal_plan.starts, np.asarray(costs))
+        del cb
+    plan = plan_shards(g.row_ptr.cpu().numpy(), world, balance=args.balance, n=n,
+                       calibration=calib)
     b = bench.dense_b(g.num_cols, n, 1, dev)
     times = []
     for rank in range(world):
