@@ -1034,12 +1034,13 @@ int sgap_plan(const sgap_kernel_t *k, const sgap_csr_t *a, int32_t dtype, uint32
         if (cudaMemsetAsync(counts, 0, (size_t)a->num_cols * sizeof(unsigned), st) != cudaSuccess)
             return SGAP_ERR_CUDA;
         const unsigned g1 = (unsigned)ceil_div(nnz < (1LL << 24) ? nnz : (1LL << 24), kHwBlock);
-        k_col_counts<<<g1, kHwBlock, 0, st>>>(a->d_col_idx, nnz, counts);
+        k_col_counts<<<g1, kHwBlock, 0, st>>>(a->d_col_idx, nnz, a->num_cols, counts);
         size_t tb = L.hint_tmp_bytes;
         if (cub::DeviceRadixSort::SortKeysDescending(ws + L.hint_tmp, tb, counts, sorted,
                                                      (int)a->num_cols, 0, 32, st) != cudaSuccess)
             return SGAP_ERR_CUDA;
-        k_col_hints<<<g1, kHwBlock, 0, st>>>(a->d_col_idx, nnz, counts, sorted + (H - 1), hinted);
+        k_col_hints<<<g1, kHwBlock, 0, st>>>(a->d_col_idx, nnz, a->num_cols, counts,
+                                             sorted + (H - 1), hinted);
         if (cudaGetLastError() != cudaSuccess) return SGAP_ERR_CUDA;
         aux.d_col_hinted = hinted;
     }

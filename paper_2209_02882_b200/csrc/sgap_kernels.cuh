@@ -1815,20 +1815,26 @@ k_validate_cols(const int *__restrict__ rp, const int *__restrict__ ci, int M, l
 // column, then a copy of col_idx with bit 31 set on columns gathered fewer
 // than `thr` times (outside the hot set the L2 can keep).
 __global__ void __launch_bounds__(256)
-k_col_counts(const int *__restrict__ ci, long long nnz, unsigned *__restrict__ counts) {
+k_col_counts(const int *__restrict__ ci, long long nnz, long long K,
+             unsigned *__restrict__ counts) {
     for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < nnz;
-         p += (long long)gridDim.x * blockDim.x)
-        atomicAdd(counts + __ldg(ci + p), 1u);
+         p += (long long)gridDim.x * blockDim.x) {
+        const int c = __ldg(ci + p);
+        // an unvalidated CSR may hold out-of-range columns: never write outside
+        if (c >= 0 && (long long)c < K) atomicAdd(counts + c, 1u);
+    }
 }
 
 __global__ void __launch_bounds__(256)
-k_col_hints(const int *__restrict__ ci, long long nnz, const unsigned *__restrict__ counts,
-            const unsigned *__restrict__ thr, int *__restrict__ out) {
+k_col_hints(const int *__restrict__ ci, long long nnz, long long K,
+            const unsigned *__restrict__ counts, const unsigned *__restrict__ thr,
+            int *__restrict__ out) {
     const unsigned t = *thr;
     for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < nnz;
          p += (long long)gridDim.x * blockDim.x) {
         const int c = __ldg(ci + p);
-        out[p] = __ldg(counts + c) < t ? (int)((unsigned)c | 0x80000000u) : c;
+        const bool in = c >= 0 && (long long)c < K;
+        out[p] = in && __ldg(counts + c) < t ? (int)((unsigned)c | 0x80000000u) : c;
     }
 }
 
