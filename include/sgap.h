@@ -114,7 +114,13 @@ typedef struct {
                                gathers in flight; needs N/c >= 32).
                                row-multiple: 0/1 logical mapping, 2
                                interleaved rows, 3/4 interleaved + warp per
-                               row, lane-staged A (needs N/c == 32)          */
+                               row, lane-staged A (needs N/c == 32), 6/7 a
+                               warp per 4/8-row block walking the union of
+                               its columns (N/c == 32, rows <= 64).
+                               nnz-one: 0 the shuffle segment scan, 1 each
+                               segment group walked serially by lanes along
+                               the columns (same writebacks).
+                               Other families: 0.                          */
 } sgap_kernel_t;
 
 /* CSR operand on the device (matrices.py:38-86 with int32 indices). */
