@@ -126,6 +126,10 @@ __device__ __forceinline__ const T *row_ptr(const T *base, int r, int n) {
 }
 
 // Software prefetch of a streamed A line into L1 (non-blocking, no register).
+__device__ __forceinline__ void prefetch_l2(const void *p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 __device__ __forceinline__ void prefetch_l1(const void *p) {
     asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }

@@ -981,7 +981,7 @@ __device__ __forceinline__ void zero_gap_before_rp(T *__restrict__ C, int N, lon
         store_vec<T, V>(C + (long long)r * N + kcol, z, false);
 }
 
-template <typename T, int V, bool HINT = false>
+template <typename T, int V, bool HINT = false, bool PF = false>
 __device__ __forceinline__ void eb_walk4_rp(const GlobalA<T> &A, const int *__restrict__ rp,
                                             int cur, long long q0, long long qend,
                                             const T *__restrict__ B, int N, long long kcol,
@@ -1038,6 +1038,17 @@ __device__ __forceinline__ void eb_walk4_rp(const GlobalA<T> &A, const int *__re
             gather_b<T, V, HINT>(b3, bk, c.w, N);
             Vec<T, 4> v;
             A.load4v(q, v);
+            if constexpr (PF) {
+                // the next batch's B rows toward L2 now (its columns are in
+                // cn, an L1 hit after the A-line prefetch): memory-level
+                // parallelism without holding registers for the data
+                if (q + 8 <= qe) {
+                    prefetch_l2(row_ptr(bk, cn.x & 0x7fffffff, N));
+                    prefetch_l2(row_ptr(bk, cn.y & 0x7fffffff, N));
+                    prefetch_l2(row_ptr(bk, cn.z & 0x7fffffff, N));
+                    prefetch_l2(row_ptr(bk, cn.w & 0x7fffffff, N));
+                }
+            }
             if (q + 3 < ce) {
                 fma_vec<T, V>(acc, v.v[0], b0);
                 fma_vec<T, V>(acc, v.v[1], b1);
@@ -1222,7 +1233,7 @@ __device__ __noinline__ void eb_chunk_f64(const GlobalA<T> A, long long base, lo
     flush_row<T, V>(C, N, r_first, kcol, tot, lr);  // the float64 table
 }
 
-template <typename T, int V, int W, int U, bool RPW = false, bool HINT = false>
+template <typename T, int V, int W, int U, bool RPW = false, bool HINT = false, bool PF = false>
 __global__ void __launch_bounds__(256, SGAP_EB_MINB)
 k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
                const T *__restrict__ av, const T *__restrict__ B, T *__restrict__ C,
@@ -1279,7 +1290,7 @@ k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
                                            cur | kLongFlag | kExactFlag, VEC4);
                     continue;
                 }
-                eb_walk4_rp<T, V, HINT>(A, rp, cur, base, end, B, N, kcol, C, lr, own, nwb);
+                eb_walk4_rp<T, V, HINT, PF>(A, rp, cur, base, end, B, N, kcol, C, lr, own, nwb);
                 continue;
             } else {
             const int r_first = A.row(base);
