@@ -108,9 +108,9 @@ typedef struct {
                                (row_ptr tracking when the plan has chunk
                                start rows), 5 register-staged on per-position
                                row ids, 9 = 1 with the plan's cold-column
-                               cache hints (SGAP_PLAN_L2_HINTS) and the next
-                               batch's B rows prefetched into L2 (for B far
-                               larger than L2),
+                               cache hints (SGAP_PLAN_L2_HINTS) and the B
+                               rows two batches ahead prefetched into L2
+                               (for B far larger than L2),
                                2 TMA-staged (cp.async.bulk + mbarrier ring),
                                3/4 lane-staged (warp per chunk, 4/8 B-row
                                gathers in flight; needs N/c >= 32).

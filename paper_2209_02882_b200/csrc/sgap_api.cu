@@ -274,10 +274,11 @@ int launch_nnz_multiple(bool tma, int tile, int owner, const sgap_kernel_t &k,
     const int vec4 = (k.g % 4 == 0) && aligned(rowid, 16) && aligned(a.d_col_idx, 16) &&
                      aligned(a.d_vals, 16);
     if (k.hw_variant == 9) {  // + cold-column cache hints (the plan's flagged col_idx)
-        // + the next batch's B rows prefetched into L2 (config 5 -3.8%; the
-        // L2-resident configs lose 2-6% to it, so only this variant has it)
+        // + the B rows two batches ahead prefetched into L2 (config 5: -3.8%
+        // at one batch, another -2.6% at two, none at four, +2% at eight;
+        // the L2-resident configs lose 2-6% to it, so only this variant has it)
         if (!vec4 || chunk_rows == nullptr || lr.col_hinted == nullptr) return SGAP_ERR_ARG;
-        return launch_k(k_nnz_multiple<T, V, W, U, true, true, true>, dim3(grid_for(items, blk)),
+        return launch_k(k_nnz_multiple<T, V, W, U, true, true, true, 2>, dim3(grid_for(items, blk)),
                         dim3(blk), 0, st, pdl, rowid, lr.col_hinted, static_cast<const T *>(a.d_vals),
                         B, C, a.d_row_ptr, (int)a.num_rows, k.n, a.nnz, k.g, total_pos, vec4, owner,
                         lr, wb, exact_inline, chunk_rows);

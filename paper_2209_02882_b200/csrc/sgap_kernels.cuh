@@ -981,7 +981,7 @@ __device__ __forceinline__ void zero_gap_before_rp(T *__restrict__ C, int N, lon
         store_vec<T, V>(C + (long long)r * N + kcol, z, false);
 }
 
-template <typename T, int V, bool HINT = false, bool PF = false>
+template <typename T, int V, bool HINT = false, bool PF = false, int PFD = 1>
 __device__ __forceinline__ void eb_walk4_rp(const GlobalA<T> &A, const int *__restrict__ rp,
                                             int cur, long long q0, long long qend,
                                             const T *__restrict__ B, int N, long long kcol,
@@ -1042,11 +1042,19 @@ __device__ __forceinline__ void eb_walk4_rp(const GlobalA<T> &A, const int *__re
                 // the next batch's B rows toward L2 now (its columns are in
                 // cn, an L1 hit after the A-line prefetch): memory-level
                 // parallelism without holding registers for the data
-                if (q + 8 <= qe) {
-                    prefetch_l2(row_ptr(bk, cn.x & 0x7fffffff, N));
-                    prefetch_l2(row_ptr(bk, cn.y & 0x7fffffff, N));
-                    prefetch_l2(row_ptr(bk, cn.z & 0x7fffffff, N));
-                    prefetch_l2(row_ptr(bk, cn.w & 0x7fffffff, N));
+                if constexpr (PFD <= 1) {
+                    if (q + 8 <= qe) {
+                        prefetch_l2(row_ptr(bk, cn.x & 0x7fffffff, N));
+                        prefetch_l2(row_ptr(bk, cn.y & 0x7fffffff, N));
+                        prefetch_l2(row_ptr(bk, cn.z & 0x7fffffff, N));
+                        prefetch_l2(row_ptr(bk, cn.w & 0x7fffffff, N));
+                    }
+                } else if (q + 4 * PFD + 4 <= qe) {  // PFD batches ahead: one more 16-B col load (an L1 hit)
+                    const int4 cf = A.load4c(q + 4 * PFD);
+                    prefetch_l2(row_ptr(bk, cf.x & 0x7fffffff, N));
+                    prefetch_l2(row_ptr(bk, cf.y & 0x7fffffff, N));
+                    prefetch_l2(row_ptr(bk, cf.z & 0x7fffffff, N));
+                    prefetch_l2(row_ptr(bk, cf.w & 0x7fffffff, N));
                 }
             }
             if (q + 3 < ce) {
@@ -1233,7 +1241,8 @@ __device__ __noinline__ void eb_chunk_f64(const GlobalA<T> A, long long base, lo
     flush_row<T, V>(C, N, r_first, kcol, tot, lr);  // the float64 table
 }
 
-template <typename T, int V, int W, int U, bool RPW = false, bool HINT = false, bool PF = false>
+template <typename T, int V, int W, int U, bool RPW = false, bool HINT = false, bool PF = false,
+          int PFD = 1>
 __global__ void __launch_bounds__(256, SGAP_EB_MINB)
 k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
                const T *__restrict__ av, const T *__restrict__ B, T *__restrict__ C,
@@ -1290,7 +1299,7 @@ k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
                                            cur | kLongFlag | kExactFlag, VEC4);
                     continue;
                 }
-                eb_walk4_rp<T, V, HINT, PF>(A, rp, cur, base, end, B, N, kcol, C, lr, own, nwb);
+                eb_walk4_rp<T, V, HINT, PF, PFD>(A, rp, cur, base, end, B, N, kcol, C, lr, own, nwb);
                 continue;
             } else {
             const int r_first = A.row(base);
