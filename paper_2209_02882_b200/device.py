@@ -218,8 +218,9 @@ class KernelAux:
         return int(self.workspace.numel())
 
 
-# B larger than this (twice the 126 MB L2) gets cold-column hints by default
-_L2_HINT_MIN_B_BYTES = 256 << 20
+# B larger than this (1.5x the 126 MB L2) gets cold-column hints by default
+# (config 3 at N=256, B = 238 MB: variant 9 -3.2%, profiles/r02_ab_hints_cfg3_n256.log)
+_L2_HINT_MIN_B_BYTES = 192 << 20
 
 
 def plan_workspace_bytes(k: LoweredKernel, a: DeviceCsr, *, split_rows: bool = False,
@@ -249,7 +250,7 @@ def prepare_aux(k: LoweredKernel, a: DeviceCsr, *, stream=None, split_rows: bool
     ``SgapError`` status FAULT).  ``row_ptr_host`` is accepted for
     compatibility and unused: planning needs no host copy of the matrix.
     ``l2_hints``: build the cold-column cache hints of hw variant 9
-    (nnz-multiple); None = when B is more than twice the L2 (config 5)."""
+    (nnz-multiple); None = when B is more than 1.5x the L2 (configs 3 at N=256, 5)."""
     del row_ptr_host
     a.check()
     L = _native.lib()
