@@ -32,7 +32,7 @@ def test_heuristic_matrix_classes():
     assert heuristic(RMAT20, 8).hw_variant == 5
     assert heuristic(RMAT24, 128).hw_variant == 9
     assert heuristic(CHUNGLU, 64).hw_variant == 1
-    assert heuristic(CHUNGLU, 256).hw_variant == 1
+    assert heuristic(CHUNGLU, 256).hw_variant == 9   # B = 238 MB > 1.5 L2: cold-column hints
     assert heuristic(STENCIL160, 128).point.startswith("row:8")  # regular -> RB
     assert heuristic(STENCIL160, 128).hw_variant == 4             # warp per row
     assert heuristic(STENCIL160, 16).point.startswith("row:4")
