@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define SGAP_ABI_VERSION 4
+#define SGAP_ABI_VERSION 5
 
 typedef enum {
     SGAP_OK = 0,
@@ -110,7 +110,10 @@ typedef struct {
                                row ids, 9 = 1 with the plan's cold-column
                                cache hints (SGAP_PLAN_L2_HINTS) and the B
                                rows two batches ahead prefetched into L2
-                               (for B far larger than L2),
+                               (for B far larger than L2), 10 = 1 in
+                               column-panel order over the plan's
+                               panel-major copy of B (SGAP_PLAN_PANELS: B
+                               larger than L2, a panel fits half of it),
                                2 TMA-staged (cp.async.bulk + mbarrier ring),
                                3/4 lane-staged (warp per chunk, 4/8 B-row
                                gathers in flight; needs N/c >= 32).
@@ -210,6 +213,11 @@ typedef struct {
                                         L2); hw variant 9 loads those rows
                                         with the evict-first streaming
                                         operator so the hot rows stay in L2 */
+    void *d_panel_b;                /* SGAP_PLAN_PANELS (ABI v5): room for the
+                                        panel-major copy of B that hw variant
+                                        10 walks one column panel at a time */
+    int32_t panel_lanes;            /* its panel width in c-wide column
+                                        tiles (0: no panels for this plan)  */
 } sgap_aux_t;
 
 /* Per-position row ids (what the reference lowering recovers per lane with
@@ -248,6 +256,14 @@ int64_t sgap_long_row_threshold(const sgap_kernel_t *kernel, int32_t dtype);
                                      col_idx copy in the workspace; worth it
                                      when B is far larger than L2: config 5
                                      -4.8%, config 2 slower)                */
+#define SGAP_PLAN_PANELS 8u       /* nnz-multiple, g % 4 == 0, B (num_cols x
+                                     n) larger than the L2: reserve a copy of
+                                     B in column panels of 8-32 c-wide tiles,
+                                     the widest whose num_cols rows fit half
+                                     the L2 (hw variant 10; config 3 at
+                                     N = 256: 64-column panels).  Costs
+                                     num_cols x n elements of workspace;
+                                     nothing when no panel fits.           */
 #define SGAP_PLAN_SPLIT_ROWS 2u   /* nnz-multiple, g >= 128: rows straddling a
                                      g-chunk boundary join the float64 table
                                      (no zero-fill pre-pass; measured slower

@@ -129,6 +129,8 @@ class Aux(ctypes.Structure):
         ("d_union4", ctypes.c_void_p),
         ("d_union8", ctypes.c_void_p),
         ("d_col_hinted", ctypes.c_void_p),
+        ("d_panel_b", ctypes.c_void_p),
+        ("panel_lanes", ctypes.c_int32),
     ]
 
 
@@ -156,6 +158,7 @@ class Plan(ctypes.Structure):
 PLAN_VALIDATE = 1
 PLAN_SPLIT_ROWS = 2
 PLAN_L2_HINTS = 4
+PLAN_PANELS = 8
 
 _lib = None
 

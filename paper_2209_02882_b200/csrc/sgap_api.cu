@@ -249,7 +249,7 @@ template <typename T, int V, int W, int U, int STAGES = 3, int MINB = 3>
 int launch_nnz_multiple(bool tma, int tile, int owner, const sgap_kernel_t &k,
                         const sgap_csr_t &a, const T *B, T *C, const int *rowid,
                         const LongRows &lr, unsigned long long *wb, cudaStream_t st, bool pdl,
-                        int exact_inline, const int *chunk_rows) {
+                        int exact_inline, const int *chunk_rows, int panel = 0) {
     const long long total_pos = k.grid_size * k.chunk;
     if (tma) {
         const size_t smem = tma_smem_bytes<T, STAGES>();
@@ -281,17 +281,46 @@ int launch_nnz_multiple(bool tma, int tile, int owner, const sgap_kernel_t &k,
         return launch_k(k_nnz_multiple<T, V, W, U, true, true, true, 2>, dim3(grid_for(items, blk)),
                         dim3(blk), 0, st, pdl, rowid, lr.col_hinted, static_cast<const T *>(a.d_vals),
                         B, C, a.d_row_ptr, (int)a.num_rows, k.n, a.nnz, k.g, total_pos, vec4, owner,
-                        lr, wb, exact_inline, chunk_rows);
+                        lr, wb, exact_inline, chunk_rows, 0);
     }
+    if constexpr (W >= 8) {
+        if (panel) {  // variant 10: variant 1, one launch per column panel
+            if (!vec4 || chunk_rows == nullptr) return SGAP_ERR_ARG;
+            // (kernel boundaries keep every warp on one panel: a single
+            // launch looping over the panels let warps drift across two
+            // panels and was 1.19x slower than variant 1 on config 3 N=256)
+            constexpr int PW = W * V;
+            const int passes = (int)ceil_div(k.n, PW);
+            const long long K = a.num_cols;
+            T *P = static_cast<T *>(lr.panel_b);
+            const long long vecs = K * passes * (PW * (int)sizeof(T) / 16);
+            k_panelize<T><<<grid_for(ceil_div(vecs, 32), kHwBlock), kHwBlock, 0, st>>>(B, P, K, k.n,
+                                                                                     PW);
+            const int sp = launch_status();
+            if (sp != SGAP_OK) return sp;
+            auto kern = k_nnz_multiple<T, V, W, U, true, false, false, 1, true>;
+            for (int ps = 0; ps < passes; ++ps) {
+                const int s0 = launch_k(kern,
+                                        dim3(grid_for(items, blk)), dim3(blk), 0, st, pdl && ps == 0,
+                                        rowid, a.d_col_idx, static_cast<const T *>(a.d_vals),
+                                        static_cast<const T *>(P + (long long)ps * K * PW), C,
+                                        a.d_row_ptr, (int)a.num_rows, k.n, a.nnz, k.g, total_pos,
+                                        vec4, owner, lr, wb, exact_inline, chunk_rows, ps);
+                if (s0 != SGAP_OK) return s0;
+            }
+            return SGAP_OK;
+        }
+    }
+    if (panel) return SGAP_ERR_ARG;
     if (vec4 && chunk_rows != nullptr)  // row_ptr tracking, no per-position row ids
         return launch_k(k_nnz_multiple<T, V, W, U, true>, dim3(grid_for(items, blk)), dim3(blk), 0,
                         st, pdl, rowid, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C,
                         a.d_row_ptr, (int)a.num_rows, k.n, a.nnz, k.g, total_pos, vec4, owner, lr,
-                        wb, exact_inline, chunk_rows);
+                        wb, exact_inline, chunk_rows, 0);
     return launch_k(k_nnz_multiple<T, V, W, U, false>, dim3(grid_for(items, blk)), dim3(blk), 0, st,
                     pdl, rowid, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, a.d_row_ptr,
                     (int)a.num_rows, k.n, a.nnz, k.g, total_pos, vec4, owner, lr, wb, exact_inline,
-                    (const int *)nullptr);
+                    (const int *)nullptr, 0);
 }
 
 // hw_variant: 0 auto; 1 register walk; 2 TMA-staged walk; 3/4 lane-staged walk
@@ -322,6 +351,16 @@ int run_nnz_multiple_w(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, 
     if (variant == 9) {  // variant 1 with the plan's cold-column cache hints
         const int vec4 = (k.g % 4 == 0) && aligned(a.d_col_idx, 16) && aligned(a.d_vals, 16);
         if (lr.col_hinted == nullptr || lr.chunk_rows == nullptr || !vec4) return SGAP_ERR_ARG;
+        variant = 1;
+    }
+    const int panel = variant == 10 ? 1 : 0;
+    if (panel) {  // variant 1 in column-panel order (W lanes = one panel)
+        const int vec4 = (k.g % 4 == 0) && aligned(rowid, 16) && aligned(a.d_col_idx, 16) &&
+                         aligned(a.d_vals, 16);
+        constexpr int E = 16 / (int)sizeof(T);  // k_panelize moves 16-byte vectors
+        if (lr.chunk_rows == nullptr || !vec4 || W < 8 || W >= k.n / V || lr.panel_b == nullptr ||
+            W != lr.panel_lanes || k.n % E || (W * V) % E || !aligned(B, 16))
+            return SGAP_ERR_ARG;
         variant = 1;
     }
     if (variant < 1 || variant > 5) return SGAP_ERR_ARG;
@@ -377,8 +416,25 @@ int run_nnz_multiple_w(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, 
     // rows; variant 5 is the same walk on per-position row ids
     return launch_nnz_multiple<T, V, W, 4>(tma, tile, owner, k, a, B, C, rowid, lr, wb, st,
                                            pdl, exact_inline ? 1 : 0,
-                                           variant == 1 ? lr.chunk_rows : nullptr);
+                                           variant == 1 ? lr.chunk_rows : nullptr, panel);
     // (k.hw_variant == 9 selects the cold-hint instantiation inside)
+}
+
+// Column-panel width for hw variant 10, in lanes of V columns: the widest
+// power-of-two panel (8..32 lanes, at least two panels) whose B rows
+// (num_cols x panel columns) fit in half the L2.  0 when none does or when
+// the whole of B already fits (config 3 at N = 256: 16 lanes = 64 columns,
+// 60 MB of B per panel against 238 MB for all of B; column-panel probe
+// profiles/r02_panel_probe_cfg3_n256.log).
+int panel_lanes(const sgap_kernel_t &k, const sgap_csr_t &a, int V, size_t esz) {
+    int dev = 0, l2 = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev) != cudaSuccess || l2 <= 0) return 0;
+    const long long nt = k.n / V;
+    if ((long long)a.num_cols * k.n * (long long)esz <= (long long)l2) return 0;
+    for (int w = 32; w >= 8; w >>= 1)
+        if (w < nt && (long long)a.num_cols * w * V * (long long)esz <= l2 / 2) return w;
+    return 0;
 }
 
 template <typename T, int V>
@@ -392,6 +448,15 @@ int run_nnz_multiple(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T 
     const int owner = acc ? 0 : 1;
     const bool routed = lr.threshold >= 0 && lr.chunk == k.g;
     const bool zero = owner && !routed;  // launched by the walk after its checks
+    if (k.hw_variant == 10) {  // column panels: W = the panel's lanes
+        switch (lr.panel_lanes) {  // chosen by the planner (panel_lanes)
+            case 8: return run_nnz_multiple_w<T, V, 8>(k, a, B, C, rowid, lr, owner, has_exact, zero, wb, st);
+            case 16: return run_nnz_multiple_w<T, V, 16>(k, a, B, C, rowid, lr, owner, has_exact, zero, wb, st);
+            case 32: return run_nnz_multiple_w<T, V, 32>(k, a, B, C, rowid, lr, owner, has_exact, zero, wb, st);
+            default: return SGAP_ERR_ARG;  // no panels in the plan (none fits half the L2,
+                                           // B already does, or no SGAP_PLAN_PANELS)
+        }
+    }
     switch (pow2_floor(k.n / V)) {
         case 1: return run_nnz_multiple_w<T, V, 1>(k, a, B, C, rowid, lr, owner, has_exact, zero, wb, st);
         case 2: return run_nnz_multiple_w<T, V, 2>(k, a, B, C, rowid, lr, owner, has_exact, zero, wb, st);
@@ -577,6 +642,8 @@ static int run_impl(const sgap_kernel_t *k, const sgap_csr_t *a, const void *d_b
     if (k->family == SGAP_NNZ_MULTIPLE && aux != nullptr) {
         lr.chunk_rows = aux->d_chunk_rows;
         lr.col_hinted = aux->d_col_hinted;
+        lr.panel_b = aux->d_panel_b;
+        lr.panel_lanes = aux->d_panel_b ? aux->panel_lanes : 0;
     }
     if (k->family == SGAP_ROW_MULTIPLE && aux != nullptr) {
         for (int w = 0; w < 2; ++w) {
@@ -619,7 +686,8 @@ struct LongerThan {
 struct PlanLayout {
     size_t starts = 0, rowid = 0, slot = 0, rows = 0, count = 0, acc = 0, exact = 0, stats = 0,
            tmp = 0, chunk_rows = 0, union_off[2] = {0, 0}, union_e[2] = {0, 0}, union_tmp = 0,
-           hint_counts = 0, hint_sorted = 0, hint_cols = 0, hint_tmp = 0, total = 0;
+           hint_counts = 0, hint_sorted = 0, hint_cols = 0, hint_tmp = 0, panel_b = 0, total = 0;
+    int panel_lanes = 0;
     size_t hint_tmp_bytes = 0;
     size_t union_tmp_bytes = 0;
     long long thr = -1, chunk = 0, cap = 0, exact_cap = 0, exact_cut = 0;
@@ -668,6 +736,15 @@ int plan_layout(const sgap_kernel_t &k, const sgap_csr_t &a, int32_t dtype, uint
                                                      (unsigned *)nullptr, (int)K);
             L.hint_tmp_bytes = sb;
             L.hint_tmp = take(sb);
+        }
+        if (L.chunk_rows && (flags & SGAP_PLAN_PANELS) && nnz > 0) {
+            const size_t esz = dtype == SGAP_F32 ? 4 : 8;
+            L.panel_lanes = panel_lanes(k, a, k.c, esz);
+            if (L.panel_lanes > 0) {
+                const long long pw = (long long)L.panel_lanes * k.c;
+                const long long passes = ceil_div(k.n, pw);
+                L.panel_b = take((size_t)(passes * a.num_cols * pw) * esz);
+            }
         }
         L.thr = sgap_long_row_threshold(&k, dtype);
         L.chunk = (L.thr >= 0 && (flags & SGAP_PLAN_SPLIT_ROWS)) ? long_row_chunk(&k, dtype) : 0;
@@ -1046,6 +1123,10 @@ int sgap_plan(const sgap_kernel_t *k, const sgap_csr_t *a, int32_t dtype, uint32
                                              sorted + (H - 1), hinted);
         if (cudaGetLastError() != cudaSuccess) return SGAP_ERR_CUDA;
         aux.d_col_hinted = hinted;
+    }
+    if (L.panel_b) {
+        aux.d_panel_b = ws + L.panel_b;
+        aux.panel_lanes = L.panel_lanes;
     }
     if (cudaMemcpyAsync(h, stats, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st) !=
             cudaSuccess ||

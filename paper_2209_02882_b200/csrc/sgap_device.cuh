@@ -241,6 +241,8 @@ struct LongRows {
     const unsigned *union_e[2];  // row-blocked RB walk: union column streams of
     const int *union_off[2];     // 4-row [0] and 8-row [1] blocks (k_union_rows)
     const int *col_hinted;       // col_idx with bit 31 on cold columns (variant 9)
+    void *panel_b;               // panel-major copy of B (variant 10; host side only)
+    int panel_lanes;             // its panel width in c-wide tiles (0: none)
 };
 
 // Row ids carry bit 31 when the row belongs to the long-row table and bit 30

@@ -986,7 +986,10 @@ __device__ __forceinline__ void eb_walk4_rp(const GlobalA<T> &A, const int *__re
                                             int cur, long long q0, long long qend,
                                             const T *__restrict__ B, int N, long long kcol,
                                             T *__restrict__ C, const LongRows &lr,
-                                            const Owner &own, unsigned long long &nwb) {
+                                            const Owner &own, unsigned long long &nwb,
+                                            int ldb, long long bcol) {
+    // B rows: stride ldb, this tile at column bcol (N / kcol, except for the
+    // panel-major copy of B that hw variant 10 walks); C: stride N, column kcol
     unsigned cs = (unsigned)__ldg(rp + cur), ce = (unsigned)__ldg(rp + cur + 1);
     // the NEXT row's end, loaded one row ahead so a row change does not wait
     // on a dependent row_ptr load
@@ -997,7 +1000,7 @@ __device__ __forceinline__ void eb_walk4_rp(const GlobalA<T> &A, const int *__re
     acc.zero();
     Vec<double, V> tot;
     tot.zero();
-    const T *bk = B + kcol;
+    const T *bk = B + bcol;
     unsigned q = (unsigned)q0;
     const unsigned qe = (unsigned)qend;
     // close the current row and move to the row holding position p
@@ -1032,10 +1035,10 @@ __device__ __forceinline__ void eb_walk4_rp(const GlobalA<T> &A, const int *__re
             if (q + 8 <= qe) cn = A.load4c(q + 4);
             if ((q & 31) == 0 && q + 64 < qe) A.prefetch_cv(q + 64);
             Vec<T, V> b0, b1, b2, b3;
-            gather_b<T, V, HINT>(b0, bk, c.x, N);
-            gather_b<T, V, HINT>(b1, bk, c.y, N);
-            gather_b<T, V, HINT>(b2, bk, c.z, N);
-            gather_b<T, V, HINT>(b3, bk, c.w, N);
+            gather_b<T, V, HINT>(b0, bk, c.x, ldb);
+            gather_b<T, V, HINT>(b1, bk, c.y, ldb);
+            gather_b<T, V, HINT>(b2, bk, c.z, ldb);
+            gather_b<T, V, HINT>(b3, bk, c.w, ldb);
             Vec<T, 4> v;
             A.load4v(q, v);
             if constexpr (PF) {
@@ -1044,17 +1047,17 @@ __device__ __forceinline__ void eb_walk4_rp(const GlobalA<T> &A, const int *__re
                 // parallelism without holding registers for the data
                 if constexpr (PFD <= 1) {
                     if (q + 8 <= qe) {
-                        prefetch_l2(row_ptr(bk, cn.x & 0x7fffffff, N));
-                        prefetch_l2(row_ptr(bk, cn.y & 0x7fffffff, N));
-                        prefetch_l2(row_ptr(bk, cn.z & 0x7fffffff, N));
-                        prefetch_l2(row_ptr(bk, cn.w & 0x7fffffff, N));
+                        prefetch_l2(row_ptr(bk, cn.x & 0x7fffffff, ldb));
+                        prefetch_l2(row_ptr(bk, cn.y & 0x7fffffff, ldb));
+                        prefetch_l2(row_ptr(bk, cn.z & 0x7fffffff, ldb));
+                        prefetch_l2(row_ptr(bk, cn.w & 0x7fffffff, ldb));
                     }
                 } else if (q + 4 * PFD + 4 <= qe) {  // PFD batches ahead: one more 16-B col load (an L1 hit)
                     const int4 cf = A.load4c(q + 4 * PFD);
-                    prefetch_l2(row_ptr(bk, cf.x & 0x7fffffff, N));
-                    prefetch_l2(row_ptr(bk, cf.y & 0x7fffffff, N));
-                    prefetch_l2(row_ptr(bk, cf.z & 0x7fffffff, N));
-                    prefetch_l2(row_ptr(bk, cf.w & 0x7fffffff, N));
+                    prefetch_l2(row_ptr(bk, cf.x & 0x7fffffff, ldb));
+                    prefetch_l2(row_ptr(bk, cf.y & 0x7fffffff, ldb));
+                    prefetch_l2(row_ptr(bk, cf.z & 0x7fffffff, ldb));
+                    prefetch_l2(row_ptr(bk, cf.w & 0x7fffffff, ldb));
                 }
             }
             if (q + 3 < ce) {
@@ -1076,7 +1079,7 @@ __device__ __forceinline__ void eb_walk4_rp(const GlobalA<T> &A, const int *__re
     }
     for (; q < qe; ++q) {  // < 4 tail positions
         Vec<T, V> b;
-        gather_b<T, V, HINT>(b, bk, A.col(q), N);
+        gather_b<T, V, HINT>(b, bk, A.col(q), ldb);
         if (q >= ce) advance(q);
         fma_vec<T, V>(acc, A.val(q), b);
     }
@@ -1200,6 +1203,36 @@ __device__ __forceinline__ void eb_walk(const ASrc &A, long long q0, long long q
     if (own.on && own.end == own.nnz) zero_rows<T, V>(C, N, kcol, (cur & kRowMask) + 1, own.m);
 }
 
+// B (K x N, row-major) -> the panel-major copy hw variant 10 walks: panel p
+// holds columns [p*PW, p*PW + PW) of every row as a contiguous K x PW block
+// (the last panel zero-padded past N).  One 16-byte vector per thread, read
+// coalesced along B's rows.  A strided panel (PW of every N columns) used
+// only a quarter of each B row's L2 lines' neighbourhood and lost most of
+// the panel's L2 reuse (config 3 N=256: 10.3 vs 8.8 ms for contiguous
+// panels).
+template <typename T>
+__global__ void __launch_bounds__(256) k_panelize(const T *__restrict__ B, T *__restrict__ P,
+                                                  long long K, int N, int PW) {
+    constexpr int E = 16 / sizeof(T);
+    const int vpr = PW / E;  // 16-byte vectors per panel row
+    const int panels = (N + PW - 1) / PW;
+    const long long total = K * panels * vpr;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long row = i / ((long long)panels * vpr);
+        const int rest = (int)(i - row * panels * vpr);
+        const int p = rest / vpr, v = rest - p * vpr;
+        const int col = p * PW + v * E;
+        T *dst = P + ((long long)p * K + row) * PW + v * E;
+        if (col + E <= N) {
+            __stcs(reinterpret_cast<int4 *>(dst), __ldg(reinterpret_cast<const int4 *>(B + row * N + col)));
+        } else {
+#pragma unroll
+            for (int e = 0; e < E; ++e) dst[e] = col + e < N ? B[row * N + col + e] : T(0);
+        }
+    }
+}
+
 // A chunk inside an exact-flagged (hub) row, walked by the register walk
 // itself: float64 products (exact for float32 inputs) summed in float64, one
 // flush into the float64 table.  Out of line (noinline) so its float64 state
@@ -1208,10 +1241,10 @@ template <typename T, int V>
 __device__ __noinline__ void eb_chunk_f64(const GlobalA<T> A, long long base, long long end,
                                           const T *__restrict__ B, int N, long long kcol,
                                           T *__restrict__ C, const LongRows lr, int r_first,
-                                          bool vec4) {
+                                          bool vec4, int ldb, long long bcol) {
     Vec<double, V> tot;
     tot.zero();
-    const T *bk = B + kcol;
+    const T *bk = B + bcol;  // B rows: stride ldb (see eb_walk4_rp)
     unsigned q = (unsigned)base;
     const unsigned qe = (unsigned)end;
     for (; vec4 && q + 4 <= qe; q += 4) {
@@ -1219,10 +1252,10 @@ __device__ __noinline__ void eb_chunk_f64(const GlobalA<T> A, long long base, lo
         Vec<T, 4> v;
         A.load4cv(q, c, v);
         Vec<T, V> b0, b1, b2, b3;  // (bit 31: the cold-column hint, not part of the index)
-        ldg_vec<T, V>(b0, row_ptr(bk, c.x & 0x7fffffff, N));
-        ldg_vec<T, V>(b1, row_ptr(bk, c.y & 0x7fffffff, N));
-        ldg_vec<T, V>(b2, row_ptr(bk, c.z & 0x7fffffff, N));
-        ldg_vec<T, V>(b3, row_ptr(bk, c.w & 0x7fffffff, N));
+        ldg_vec<T, V>(b0, row_ptr(bk, c.x & 0x7fffffff, ldb));
+        ldg_vec<T, V>(b1, row_ptr(bk, c.y & 0x7fffffff, ldb));
+        ldg_vec<T, V>(b2, row_ptr(bk, c.z & 0x7fffffff, ldb));
+        ldg_vec<T, V>(b3, row_ptr(bk, c.w & 0x7fffffff, ldb));
 #pragma unroll
         for (int x = 0; x < V; ++x) {
             tot.v[x] = fma((double)v.v[0], (double)b0.v[x], tot.v[x]);
@@ -1233,7 +1266,7 @@ __device__ __noinline__ void eb_chunk_f64(const GlobalA<T> A, long long base, lo
     }
     for (; q < qe; ++q) {
         Vec<T, V> b;
-        ldg_vec<T, V>(b, row_ptr(bk, A.col(q) & 0x7fffffff, N));
+        ldg_vec<T, V>(b, row_ptr(bk, A.col(q) & 0x7fffffff, ldb));
         const double a = (double)A.val(q);
 #pragma unroll
         for (int x = 0; x < V; ++x) tot.v[x] = fma(a, (double)b.v[x], tot.v[x]);
@@ -1242,13 +1275,13 @@ __device__ __noinline__ void eb_chunk_f64(const GlobalA<T> A, long long base, lo
 }
 
 template <typename T, int V, int W, int U, bool RPW = false, bool HINT = false, bool PF = false,
-          int PFD = 1>
+          int PFD = 1, bool PANEL = false>
 __global__ void __launch_bounds__(256, SGAP_EB_MINB)
 k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
                const T *__restrict__ av, const T *__restrict__ B, T *__restrict__ C,
                const int *__restrict__ rp, int M, int N, long long nnz, int g,
                long long total_pos, int vec4, int owner, LongRows lr, unsigned long long *wb,
-               int exact_inline, const int *__restrict__ chunk_rows) {
+               int exact_inline, const int *__restrict__ chunk_rows, int pass = 0) {
     const bool VEC4 = vec4 != 0;  // g % 4 == 0 and 16-byte aligned A arrays
     // row_ptr tracking (no per-position row ids) when the plan has the
     // g-chunk start rows and the walk is vectorised
@@ -1264,12 +1297,19 @@ k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
     const int sl = (int)(lane & (unsigned)(W - 1));
     const GlobalA<T> A{rowid, ci, av};
     unsigned long long nwb = 0;
+    // PANEL (hw variant 10): one launch per column panel.  Launch `pass`
+    // walks every chunk for column tiles [pass*W, pass*W + W) only (one panel
+    // of B, W*V columns), so the B rows live in L2 one panel at a time when
+    // the whole of B does not fit but a panel does.  Each (chunk, tile) is the
+    // same serial walk as without panels: results and writeback counts are
+    // unchanged, only the order of the (chunk, tile) work differs.
     SGAP_WARP_LOOP(item, items) {
         const long long ch = item * SG + sg;
         if (ch >= total_chunks) continue;
         const long long base = ch * g;
         const long long end = min(base + (long long)g, nnz);
-        for (int tile = sl; tile < NT; tile += W) {
+        const int tile_end = PANEL ? min(NT, (pass + 1) * W) : NT;
+        for (int tile = PANEL ? pass * W + sl : sl; tile < tile_end; tile += W) {
             if (base >= end) {  // chunk past nnz: the reference flushes 0 into row M-1
                 // (not nnz-one at r = 1, owner 3: its lanes past nnz break
                 // before the atomic, cuda_nnz_one_serial.cu)
@@ -1287,6 +1327,10 @@ k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
             if constexpr (RP) {
                 const int cur = __ldg(chunk_rows + ch);
                 const long long kcol = (long long)tile * V;
+                // PANEL: B is this pass's panel of the panel-major copy
+                // (K x W*V, contiguous), C stays row-major N wide
+                const int ldb = PANEL ? W * V : N;
+                const long long bcol = PANEL ? (long long)(tile - pass * W) * V : kcol;
                 const long long cs = __ldg(rp + cur), ce = __ldg(rp + cur + 1);
                 if (lr.threshold >= 0 && ce - cs > exact_cut && ce >= end) {
                     // a chunk inside an exact-flagged (hub) row
@@ -1296,10 +1340,11 @@ k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
                     nwb += V;
                     if (exact_inline)
                         eb_chunk_f64<T, V>(A, base, end, B, N, kcol, C, lr,
-                                           cur | kLongFlag | kExactFlag, VEC4);
+                                           cur | kLongFlag | kExactFlag, VEC4, ldb, bcol);
                     continue;
                 }
-                eb_walk4_rp<T, V, HINT, PF, PFD>(A, rp, cur, base, end, B, N, kcol, C, lr, own, nwb);
+                eb_walk4_rp<T, V, HINT, PF, PFD>(A, rp, cur, base, end, B, N, kcol, C, lr, own, nwb,
+                                                 ldb, bcol);
                 continue;
             } else {
             const int r_first = A.row(base);
@@ -1311,7 +1356,7 @@ k_nnz_multiple(const int *__restrict__ rowid, const int *__restrict__ ci,
                     zero_rows<T, V>(C, N, kcol, (r_first & kRowMask) + 1, M);
                 nwb += V;
                 if (exact_inline)  // a chunk inside an exact-flagged (hub) row
-                    eb_chunk_f64<T, V>(A, base, end, B, N, kcol, C, lr, r_first, VEC4);
+                    eb_chunk_f64<T, V>(A, base, end, B, N, kcol, C, lr, r_first, VEC4, N, kcol);
                 continue;
             }
             if (VEC4)

@@ -221,6 +221,7 @@ class KernelAux:
 # B larger than this (1.5x the 126 MB L2) gets cold-column hints by default
 # (config 3 at N=256, B = 238 MB: variant 9 -3.2%, profiles/r02_ab_hints_cfg3_n256.log)
 _L2_HINT_MIN_B_BYTES = 192 << 20
+L2_DEVICE_BYTES = 132_644_864  # B200 cudaDevAttrL2CacheSize (what the planner reads)
 
 
 def plan_workspace_bytes(k: LoweredKernel, a: DeviceCsr, *, split_rows: bool = False,
@@ -236,9 +237,22 @@ def plan_workspace_bytes(k: LoweredKernel, a: DeviceCsr, *, split_rows: bool = F
     return int(out.value)
 
 
+def panel_lanes(num_cols: int, n: int, c: int, esz: int = 4, l2_bytes: int = L2_DEVICE_BYTES) -> int:
+    """hw variant 10's panel width in c-wide column tiles, as the planner
+    picks it (sgap_api.cu panel_lanes): the widest of 32 / 16 / 8 tiles
+    (fewer than n / c) whose num_cols B rows fit half the L2; 0 when none
+    does or the whole of B fits the L2."""
+    if num_cols * n * esz <= l2_bytes:
+        return 0
+    for w in (32, 16, 8):
+        if w < n // c and num_cols * w * c * esz <= l2_bytes // 2:
+            return w
+    return 0
+
+
 def prepare_aux(k: LoweredKernel, a: DeviceCsr, *, stream=None, split_rows: bool = False,
                 validate: bool = False, l2_hints: bool | None = None,
-                row_ptr_host=None) -> KernelAux:
+                panels: bool | None = None, row_ptr_host=None) -> KernelAux:
     """``sgap_plan``: the per-matrix half of ``runner.build_kernel``
     (block_starts, lowering.py:683-696) plus the engine's side data, built on
     the device in one workspace (one 24-byte read-back of row statistics).
@@ -250,16 +264,23 @@ def prepare_aux(k: LoweredKernel, a: DeviceCsr, *, stream=None, split_rows: bool
     ``SgapError`` status FAULT).  ``row_ptr_host`` is accepted for
     compatibility and unused: planning needs no host copy of the matrix.
     ``l2_hints``: build the cold-column cache hints of hw variant 9
-    (nnz-multiple); None = when B is more than 1.5x the L2 (configs 3 at N=256, 5)."""
+    (nnz-multiple); None = when B is more than 1.5x the L2 (configs 3 at N=256, 5).
+    ``panels``: reserve the panel-major copy of B that hw variant 10 walks
+    (nnz-multiple; num_cols x n elements of workspace, only when B exceeds
+    the L2 and a panel fits half of it); None = whenever that applies."""
     del row_ptr_host
     a.check()
     L = _native.lib()
     if l2_hints is None:
         l2_hints = (k.family == "nnz-multiple" and
                     a.num_cols * k.n * a.vals.element_size() > _L2_HINT_MIN_B_BYTES)
+    if panels is None:
+        panels = (k.family == "nnz-multiple" and
+                  panel_lanes(a.num_cols, k.n, k.c, a.vals.element_size()) > 0)
     flags = ((_native.PLAN_SPLIT_ROWS if split_rows else 0) |
              (_native.PLAN_VALIDATE if validate else 0) |
-             (_native.PLAN_L2_HINTS if l2_hints else 0))
+             (_native.PLAN_L2_HINTS if l2_hints else 0) |
+             (_native.PLAN_PANELS if panels else 0))
     ks = kernel_struct(k)
     view = a.view()
     nbytes = plan_workspace_bytes(k, a, flags=flags)
@@ -395,7 +416,11 @@ def launches_per_call(k: LoweredKernel, aux: KernelAux | None, *, accumulate: bo
             # k_nnz_multiple_exact (sgap_api.cu run_nnz_multiple_w)
             w = min(32, max(1, k.n // k.c))
             variant = hw_variant or (2 if (w >= 16 and k.g <= 128) else 1)
-            n += 0 if variant in (1, 5, 9) else 1
+            n += 0 if variant in (1, 5, 9, 10) else 1
+    if k.family == "nnz-multiple" and hw_variant == 10 and aux is not None:
+        lanes = int(aux.plan.aux.panel_lanes)
+        if lanes:  # k_panelize + one walk per column panel (the walk is counted above)
+            n += 1 + (k.n + lanes * k.c - 1) // (lanes * k.c) - 1
     return n
 
 

@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import _native
-from .device import DeviceCsr, prepare_aux, spmm
+from .device import DeviceCsr, panel_lanes, prepare_aux, spmm
 from .lowering import KernelConfig, LoweredKernel, lower
 from .space import enumerate_space, parse_point
 from .templates import algorithm_template
@@ -110,7 +110,11 @@ def candidates(n: int, p_values=(256, 1024), g_values=GPU_G_VALUES,
                 # matrices: configs 3/5), 5: the same walk on per-position row
                 # ids (latency-bound: config 2), 2: TMA-staged, 3: lane-staged
                 # 9: 1 + the plan's cold-column cache hints (B >> L2: config 5)
+                # 10: 1 in column panels (B > L2, a panel fits half of it:
+                # config 3 at N = 256; refused -- and skipped -- elsewhere)
                 vs = (1, 5, 9, 2, 3) if n // tpl.c >= 32 else (1, 5, 9, 2)
+                if n // tpl.c > 8:
+                    vs += (10,)
                 out.extend(Candidate(str(pt), p, 0, v) for v in vs)
             elif variants and tpl.family == "nnz-one":
                 # 0: the shuffle segment scan; 1: each segment group walked
@@ -213,7 +217,12 @@ def heuristic(stats: MatrixStats, n: int) -> Candidate:
     # waits on row_ptr loads, 56% / 48% empty rows); otherwise row_ptr
     # tracking with the column-pipelined batches (config 3 at N = 64 / 256)
     b_bytes = stats.num_cols * n * 4
-    if b_bytes > 16 * L2_BYTES:
+    if panel_lanes(stats.num_cols, n, c) > 0:
+        # B larger than the L2 but a column panel fits half of it: walk the
+        # panels one at a time (config 3 at N = 256: 0.87x of variant 1,
+        # profiles/r02_panel_probe_cfg3_n256.log)
+        variant = 10
+    elif b_bytes > 16 * L2_BYTES:
         variant = 9
     elif stats.mean_row < 32 and stats.empty_frac > 0.2:
         variant = 5

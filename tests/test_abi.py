@@ -36,7 +36,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_status_strings():
     L = _native.lib()
-    assert L.sgap_abi_version() == 4
+    assert L.sgap_abi_version() == 5
     assert _native.status_string(_native.ERR_NO_TEMPLATE) == "no template covers the point"
     assert _native.status_string(99) == "unknown status"
 
@@ -55,7 +55,7 @@ def test_argument_validation_without_device():
     assert L.sgap_long_row_threshold(None, 0) == -1
     k.n, k.c = 4, 1
     a = _native.Csr()
-    # sgap_run takes only a plan built by sgap_plan (ABI v4): a zeroed struct is rejected
+    # sgap_run takes only a plan built by sgap_plan (ABI v4+): a zeroed struct is rejected
     plan = _native.Plan()
     assert L.sgap_run(ctypes.byref(plan), ctypes.byref(a), None, None, 0, None, None) == _native.ERR_ARG
     # the planner: workspace sizing is host-only; bad dtype / config / shape are caught first

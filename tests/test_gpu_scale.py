@@ -305,6 +305,48 @@ def test_cold_column_hint_walk():
             spmm(k, a, b, c, aux=prepare_aux(k, a, l2_hints=False), hw_variant=9)
 
 
+def test_column_panel_walk():
+    """hw variant 10: the row_ptr walk in column-panel order (every chunk for
+    one panel of B's columns, then the next panel) when B exceeds the L2 but a
+    panel fits half of it.  Same results and writeback counts as variant 1
+    on a Chung-Lu matrix with config 3's column count (64-column panels) and
+    an R-MAT one at N = 512 (32-column panels, 16 passes), hub rows included;
+    refused when all of B fits the L2."""
+    from paper_2209_02882_b200 import _native
+    from paper_2209_02882_b200.selector import _first_p
+    cases = ((G.chung_lu(232965, 3_000_000, seed=4, device="cuda"), 256),
+             (G.rmat(18, 4, seed=5, device="cuda"), 512))
+    for g, n in cases:
+        a = _device(g)
+        rp = a.row_ptr.cpu().numpy().astype(np.int64)
+        b = torch.rand((a.num_cols, n), device="cuda") * 2 - 1
+        want = oracle.spmm_f64(rp.astype(np.int32), a.col_idx.cpu().numpy(),
+                               a.vals.cpu().numpy(), b.cpu().numpy(), n)
+        c = torch.empty((a.num_rows, n), device="cuda")
+        for text in ("nnz:512,col:4,r:1", "nnz:64,col:2,r:1"):
+            p = _first_p(text, n)
+            k = lower(algorithm_template(parse_point(text), KernelConfig(n=n, p=p)),
+                      _Rp(a.num_rows, a.num_cols, rp), compute_starts=False)
+            aux = prepare_aux(k, a)
+            wb = {}
+            for v in (1, 10):
+                for acc in (False, True):
+                    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+                    c.zero_() if acc else c.fill_(float("nan"))
+                    spmm(k, a, b, c, aux=aux, hw_variant=v, writebacks=cnt, accumulate=acc)
+                    assert oracle.max_rel_error(c.cpu().numpy(), want) <= TOL, (n, text, v, acc)
+                    wb[v, acc] = int(cnt.item())
+            assert wb[1, False] == wb[10, False] and wb[1, True] == wb[10, True], (n, text, wb)
+    g = G.rmat(16, 8, seed=2, device="cuda")
+    a = _device(g)
+    rp = a.row_ptr.cpu().numpy().astype(np.int64)
+    k = lower(algorithm_template(parse_point("nnz:512,col:4,r:1"), KernelConfig(n=128, p=1024)),
+              _Rp(a.num_rows, a.num_cols, rp), compute_starts=False)
+    with pytest.raises(_native.SgapError):  # B = 32 MB: fits the L2, no panels
+        spmm(k, a, torch.rand((a.num_cols, 128), device="cuda"),
+             torch.empty((a.num_rows, 128), device="cuda"), aux=prepare_aux(k, a), hw_variant=10)
+
+
 def test_cuda_graph_replay_matches_direct_calls():
     """SpmmGraph: a planned call captured once and replayed (new values and
     B written in place between replays) gives the direct call's results for

@@ -32,7 +32,8 @@ def test_heuristic_matrix_classes():
     assert heuristic(RMAT20, 8).hw_variant == 5
     assert heuristic(RMAT24, 128).hw_variant == 9
     assert heuristic(CHUNGLU, 64).hw_variant == 1
-    assert heuristic(CHUNGLU, 256).hw_variant == 9   # B = 238 MB > 1.5 L2: cold-column hints
+    # B = 238 MB > L2 but a 64-column panel (60 MB) fits half of it: column panels
+    assert heuristic(CHUNGLU, 256).hw_variant == 10
     assert heuristic(STENCIL160, 128).point.startswith("row:8")  # regular -> RB
     assert heuristic(STENCIL160, 128).hw_variant == 4             # warp per row
     assert heuristic(STENCIL160, 16).point.startswith("row:4")
@@ -50,7 +51,8 @@ def test_candidate_grid_covers_families_and_walks():
     assert fams == {"nnz-one", "nnz-multiple", "row-multiple", "row-reciprocal"}
     assert any(c.point.startswith("nnz:512") for c in cands)
     # register walks (row_ptr / row ids) and TMA everywhere, lane-staged where N/c >= 32
-    assert {c.hw_variant for c in cands if c.point.startswith("nnz:64,col:4")} == {1, 5, 9, 2, 3}
+    # (+ column panels, variant 10, where N/c > 8)
+    assert {c.hw_variant for c in cands if c.point.startswith("nnz:64,col:4")} == {1, 5, 9, 2, 3, 10}
     assert {c.hw_variant for c in candidates(32) if c.point.startswith("nnz:64,col:4")} == {1, 5, 9, 2}
     # row-multiple: logical / interleaved, plus a warp per row where N/c == 32
     assert {c.hw_variant for c in cands if c.point.startswith("row:4,col:4")} == {0, 2, 4, 6, 7}
