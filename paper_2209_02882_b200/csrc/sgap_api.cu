@@ -97,14 +97,16 @@ int run_row_multiple(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T 
         const long long tiles = ceil_div(nblocks, tile_blocks);
         const unsigned ctas = (unsigned)(tiles < (1LL << 30) ? (tiles > 0 ? tiles : 1) : (1LL << 30));
         const T *Av = static_cast<const T *>(a.d_vals);
+        const size_t smem = (size_t)(blk / 32) * 32 * R * sizeof(T);  // per-warp value slabs
+        if (blk % 32 || smem > 48 * 1024) return SGAP_ERR_ARG;
         if (which == 0)
-            k_row_blocked<T, V, 4, 4><<<ctas, blk, 0, st>>>(a.d_row_ptr, lr.union_e[0],
-                                                            lr.union_off[0], Av, B, C,
-                                                            (int)a.num_rows, N, k.g, acc);
+            k_row_blocked<T, V, 4, 4, 4><<<ctas, blk, smem, st>>>(a.d_row_ptr, lr.union_e[0],
+                                                               lr.union_off[0], Av, B, C,
+                                                               (int)a.num_rows, N, k.g, acc);
         else
-            k_row_blocked<T, V, 8, 4><<<ctas, blk, 0, st>>>(a.d_row_ptr, lr.union_e[1],
-                                                            lr.union_off[1], Av, B, C,
-                                                            (int)a.num_rows, N, k.g, acc);
+            k_row_blocked<T, V, 8, 2, 3><<<ctas, blk, smem, st>>>(a.d_row_ptr, lr.union_e[1],
+                                                               lr.union_off[1], Av, B, C,
+                                                               (int)a.num_rows, N, k.g, acc);
         return launch_status();
     }
     if (k.hw_variant == 3 || k.hw_variant == 4) {  // lane-staged, a warp per row

@@ -363,14 +363,72 @@ k_union_rows(const int *__restrict__ rp, const int *__restrict__ ci, int M, long
     }
 }
 
-template <typename T, int V, int R, int U>
-__global__ void __launch_bounds__(256, 4)
+// Values: a window of 32 union entries is staged once per warp -- lane e
+// holds entry e and fetches, for every row r whose mask bit it carries, that
+// row's value at the row's next position (rank of e among the window's
+// entries of row r, by ballot + popc; consecutive lanes of one row read
+// consecutive positions, so the R loads are coalesced) -- and parks its R
+// values in the warp's shared slab.  The walk then reads one R-wide vector
+// per entry (a broadcast LDS) instead of one dependent scalar load per
+// position, and FMAs only the rows whose mask bit is set (no 0 * inf).
+// (Round-2 first cut loaded each value with a per-(entry, row) predicated
+// __ldg and measured 1.18x slower than the warp-per-row walk.)
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+template <typename T, int R>
+__device__ __forceinline__ void sv_store(T *p, const T (&v)[R]) {
+    if constexpr (sizeof(T) * R % 16 == 0) {
+#pragma unroll
+        for (int q = 0; q < (int)(sizeof(T) * R / 16); ++q) {
+            constexpr int E = 16 / sizeof(T);
+            if constexpr (E == 4)
+                reinterpret_cast<float4 *>(p)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            else
+                reinterpret_cast<double2 *>(p)[q] = make_double2(v[2 * q], v[2 * q + 1]);
+        }
+    } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) p[r] = v[r];
+    }
+}
+
+template <typename T, int R>
+__device__ __forceinline__ void sv_load(T (&v)[R], const T *p) {
+    if constexpr (sizeof(T) * R % 16 == 0) {
+#pragma unroll
+        for (int q = 0; q < (int)(sizeof(T) * R / 16); ++q) {
+            constexpr int E = 16 / sizeof(T);
+            if constexpr (E == 4) {
+                const float4 t = reinterpret_cast<const float4 *>(p)[q];
+                v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+            } else {
+                const double2 t = reinterpret_cast<const double2 *>(p)[q];
+                v[2 * q] = t.x; v[2 * q + 1] = t.y;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = p[r];
+    }
+}
+
+// dynamic shared memory: (blockDim.x / 32) x 32 x R values.  U B-row
+// gathers in flight per warp; MINB CTAs per SM bound the registers.
+template <typename T, int V, int R, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB)
 k_row_blocked(const int *__restrict__ rp, const unsigned *__restrict__ ue,
               const int *__restrict__ uoff, const T *__restrict__ av, const T *__restrict__ B,
               T *__restrict__ C, int M, int N, int g, int accumulate) {
+    extern __shared__ __align__(16) unsigned char sraw[];
     const int warps = (int)(blockDim.x >> 5);
     const int w = (int)(threadIdx.x >> 5);
     const unsigned lane = lane_id();
+    T *sv = reinterpret_cast<T *>(sraw) + (size_t)w * 32 * R;  // this warp's [32][R] slab
+    const unsigned lt = lanemask_lt();
     const long long kcol = (long long)lane * V;
     const T *bk = B + kcol;
     const long long nblocks = ((long long)M + R - 1) / R;
@@ -381,31 +439,56 @@ k_row_blocked(const int *__restrict__ rp, const unsigned *__restrict__ ue,
             const long long b = tile * tile_blocks + (long long)st * warps + w;
             if (b >= nblocks) break;
             const long long i0 = b * R;
-            int pos[R];
+            // one load for the block's bounds: lanes 0..R the row starts,
+            // R+1 / R+2 the union stream's range
+            int t = 0;
+            if ((int)lane <= R)
+                t = __ldg(rp + (i0 + lane < M ? i0 + lane : (long long)M));
+            else if ((int)lane == R + 1)
+                t = __ldg(uoff + b);
+            else if ((int)lane == R + 2)
+                t = __ldg(uoff + b + 1);
+            int cnt[R];
 #pragma unroll
-            for (int r = 0; r < R; ++r) pos[r] = i0 + r < M ? __ldg(rp + i0 + r) : 0;
+            for (int r = 0; r < R; ++r) cnt[r] = __shfl_sync(kFull, t, r);
+            const int e0 = __shfl_sync(kFull, t, R + 1), e1 = __shfl_sync(kFull, t, R + 2);
             Vec<T, V> acc[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) acc[r].zero();
-            const int e0 = __ldg(uoff + b), e1 = __ldg(uoff + b + 1);
             for (int s = e0; s < e1; s += 32) {
-                const unsigned x_l = __ldg(ue + (s + (int)lane < e1 ? s + (int)lane : s));
                 const int nv = min(32, e1 - s);
+                const bool mine = (int)lane < nv;
+                const unsigned x = __ldg(ue + (mine ? s + (int)lane : s));
+                const unsigned m = mine ? (x >> UnionFmt<R>::kShift) : 0u;
+                T v[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const bool has = (m >> r) & 1u;
+                    const unsigned bal = __ballot_sync(kFull, has);
+                    v[r] = has ? __ldg(av + cnt[r] + __popc(bal & lt)) : T(0);
+                    cnt[r] += __popc(bal);
+                }
+                __syncwarp();  // the previous window's readers are done
+                sv_store<T, R>(sv + lane * R, v);
+                __syncwarp();
                 for (int j = 0; j < nv; j += U) {
                     unsigned xx[U];
                     Vec<T, V> bb[U];
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
-                        xx[u] = __shfl_sync(kFull, x_l, (j + u) & 31);
-                        gather_vec<T, V>(bb[u], row_ptr(bk, (int)(xx[u] & UnionFmt<R>::kColMask), N));
+                        xx[u] = __shfl_sync(kFull, x, (j + u) & 31);
+                        if (j + u < nv)
+                            gather_vec<T, V>(bb[u], row_ptr(bk, (int)(xx[u] & UnionFmt<R>::kColMask), N));
                     }
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         if (j + u >= nv) break;
-                        const unsigned mask = xx[u] >> UnionFmt<R>::kShift;
+                        T vv[R];
+                        sv_load<T, R>(vv, sv + (j + u) * R);
+                        const unsigned mk = xx[u] >> UnionFmt<R>::kShift;
 #pragma unroll
                         for (int r = 0; r < R; ++r)
-                            if (mask & (1u << r)) fma_vec<T, V>(acc[r], __ldg(av + pos[r]++), bb[u]);
+                            if ((mk >> r) & 1u) fma_vec<T, V>(acc[r], vv[r], bb[u]);
                     }
                 }
             }
