@@ -89,7 +89,7 @@ def main():
     # the row-blocked union walk (row-multiple variants 6/7) needs rows <= 64:
     # a banded matrix with empty rows and M not a multiple of 8
     rng = np.random.default_rng(5)
-    m2, k2 = 203, 400
+    m2, k2 = 203, 480  # columns up to 2*202 - 40 + 79 = 443
     lens2 = rng.integers(0, 30, m2)
     lens2[::13] = 0
     rp2 = np.concatenate([[0], np.cumsum(lens2)]).astype(np.int64)
@@ -110,6 +110,34 @@ def main():
         spmm(kk, a2, b2, c2, aux=aux, hw_variant=variant)
         assert oracle.max_rel_error(c2.cpu().numpy(), want2) <= 1e-5, variant
     print("union walk ok")
+    # column-panel walk (nnz-multiple variant 10): B must exceed the L2 for
+    # the planner to cut panels -- 140,000 x 256 float32 (143 MB) gives
+    # 64-column panels (4 passes); hub row, float64 table and empty rows kept
+    m3, k3, n3 = 300, 140_000, 256
+    rng = np.random.default_rng(9)
+    lens3 = rng.integers(0, 40, m3)
+    lens3[::11] = 0
+    lens3[7], lens3[40] = 5000, 900
+    rp3 = np.concatenate([[0], np.cumsum(lens3)]).astype(np.int64)
+    cols3 = np.concatenate([np.sort(rng.choice(k3, int(L), replace=False)) for L in lens3 if L])
+    a3 = DeviceCsr(m3, k3, torch.from_numpy(rp3.astype(np.int32)).to(dev),
+                   torch.from_numpy(cols3.astype(np.int32)).to(dev),
+                   torch.from_numpy(rng.uniform(-1, 1, rp3[-1]).astype(np.float32)).to(dev))
+    b3 = torch.rand((k3, n3), device=dev) * 2 - 1
+    want3 = oracle.spmm_f64(rp3.astype(np.int32), cols3.astype(np.int32), a3.vals.cpu().numpy(),
+                            b3.cpu().numpy(), n3)
+    c3 = torch.empty((m3, n3), device=dev)
+    for text in ("nnz:64,col:4,r:1", "nnz:512,col:4,r:1"):
+        kk = lower(algorithm_template(parse_point(text), KernelConfig(n=n3, p=1024)),
+                   _Rp(m3, k3, rp3), compute_starts=False)
+        aux = prepare_aux(kk, a3, validate=True)
+        assert aux.plan.aux.panel_lanes == 16, aux.plan.aux.panel_lanes
+        for acc in (False, True):
+            c3.zero_() if acc else c3.fill_(float("nan"))
+            spmm(kk, a3, b3, c3, aux=aux, accumulate=acc, hw_variant=10)
+            assert oracle.max_rel_error(c3.cpu().numpy(), want3) <= 1e-5, (text, acc)
+    del b3
+    print("column-panel walk ok")
     # group primitives
     out = np.zeros(16)
     assert exec_seg_reduce_group(np.array([5, 5, 7, 7]), np.array([1.0, 2, 3, 4]), out, group_size=4) == 2
