@@ -101,3 +101,39 @@ def test_missing_library_fails_loudly(monkeypatch, tmp_path):
     monkeypatch.setattr(_native, "_lib", None)
     with pytest.raises(_native.NativeLibraryError):
         _native.lib()
+
+
+def test_ctypes_structs_match_the_c_header(tmp_path):
+    """Every ctypes mirror in _native.py has the C header's size and field
+    offsets (gcc on include/sgap.h), so a field added to one side only
+    (ABI v5 added d_panel_b / panel_lanes to sgap_aux_t) fails here, not as
+    a misread plan on the GPU."""
+    import shutil
+    if shutil.which("gcc") is None:
+        pytest.skip("no gcc")
+    mirrors = {"sgap_point_t": _native.Point, "sgap_kernel_t": _native.Kernel,
+               "sgap_csr_t": _native.Csr, "sgap_aux_t": _native.Aux, "sgap_plan_t": _native.Plan}
+    # ctypes names the two elements of the C arrays d_union_off[2] / d_union[2]
+    alias = {"d_union_off4": "d_union_off[0]", "d_union_off8": "d_union_off[1]",
+             "d_union4": "d_union[0]", "d_union8": "d_union[1]"}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "sgap.h"', "int main(void) {"]
+    for cname, py in mirrors.items():
+        lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for fname, _ in py._fields_:
+            member = alias.get(fname, fname) if cname == "sgap_aux_t" else fname
+            lines.append(f'printf("{cname} {fname} %zu\\n", offsetof({cname}, {member}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-std=c11", "-I", str(ROOT / "include"), str(src), "-o", str(exe)],
+                   check=True, capture_output=True)
+    got = {}
+    for line in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n"):
+        if line:
+            cname, field, value = line.split()
+            got[cname, field] = int(value)
+    for cname, py in mirrors.items():
+        assert got[cname, "size"] == ctypes.sizeof(py), cname
+        for fname, _ in py._fields_:
+            assert got[cname, fname] == getattr(py, fname).offset, (cname, fname)
