@@ -110,19 +110,32 @@ int run_row_multiple(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T 
         return launch_status();
     }
     if (k.hw_variant == 3 || k.hw_variant == 4) {  // lane-staged, a warp per row
-        if (L != 32) return SGAP_ERR_ARG;
+        // N/c == 32: one pass.  N/c a multiple of 32 (N >= 256 at c = 4): one
+        // pass per 32c-column panel, in place -- B and C keep their N-wide
+        // rows (the kernel's N is the row stride), each pass walks every row
+        // for its panel only, so the stencil's sliding window of B rows (one
+        // z-plane either side) is 32c columns wide instead of N while it is
+        // re-read (config 4 N=256/512: separate contiguous 128-column
+        // SpMMs 0.82x of the best full-width schedule,
+        // tools/experiments/stencil_panel_probe.py)
+        if (L % 32) return SGAP_ERR_ARG;
         const long long tile_rows = (long long)(blk / 32) * k.g;
         const long long tiles = ceil_div(a.num_rows, tile_rows);
         const unsigned ctas = (unsigned)(tiles < (1LL << 30) ? (tiles > 0 ? tiles : 1) : (1LL << 30));
         const T *Av = static_cast<const T *>(a.d_vals);
         const int M = (int)a.num_rows;
-        if (k.hw_variant == 3)
-            k_row_staged<T, V, 8><<<ctas, blk, 0, st>>>(a.d_row_ptr, a.d_col_idx, Av, B, C, M, N,
-                                                         k.g, vec4, acc, -1);
-        else
-            k_row_staged<T, V, 4><<<ctas, blk, 0, st>>>(a.d_row_ptr, a.d_col_idx, Av, B, C, M, N,
-                                                         k.g, vec4, acc, -1);
-        return launch_status();
+        for (int pan = 0; pan < L / 32; ++pan) {
+            const long long off = (long long)pan * 32 * V;
+            if (k.hw_variant == 3)
+                k_row_staged<T, V, 8><<<ctas, blk, 0, st>>>(a.d_row_ptr, a.d_col_idx, Av, B + off,
+                                                             C + off, M, N, k.g, vec4, acc, -1);
+            else
+                k_row_staged<T, V, 4><<<ctas, blk, 0, st>>>(a.d_row_ptr, a.d_col_idx, Av, B + off,
+                                                             C + off, M, N, k.g, vec4, acc, -1);
+            const int s0 = launch_status();
+            if (s0 != SGAP_OK) return s0;
+        }
+        return SGAP_OK;
     }
     if (k.hw_variant == 2) {
         if (L > blk) return SGAP_ERR_ARG;

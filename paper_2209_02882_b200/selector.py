@@ -123,7 +123,10 @@ def candidates(n: int, p_values=(256, 1024), g_values=GPU_G_VALUES,
             elif variants and tpl.family == "row-multiple" and n // tpl.c <= 256:
                 # 6/7: a warp per 4/8-row block walking the union of the
                 # block's columns (rows <= 64; stencils / meshes)
-                vs = (0, 2, 4, 6, 7) if n // tpl.c == 32 else (0, 2)
+                # 4 at N/c = 64, 96, ...: the warp-per-row walk once per
+                # 32c-column panel (config 4 at N = 256 / 512)
+                L = n // tpl.c
+                vs = (0, 2, 4, 6, 7) if L == 32 else (0, 2, 4) if L % 32 == 0 else (0, 2)
                 out.extend(Candidate(str(pt), p, 0, v) for v in vs)
             else:
                 out.append(Candidate(str(pt), p))
@@ -192,11 +195,14 @@ def heuristic(stats: MatrixStats, n: int) -> Candidate:
             pt = f"row:{8 if n >= 64 else 4},col:{col(widest)},r:1"
             p = _first_p(pt, n)
             if p is not None:
-                # a warp per row when N/c == 32 (config 4 N=128: 3.35 vs 3.82 ms),
+                # a warp per row when N/c == 32 (config 4 N=128: 3.35 vs 3.82 ms)
+                # and once per 32c-column panel when N/c is a larger multiple
+                # of 32 (config 4 N=256 / 512: 6.10 / 12.21 ms vs 7.50 / 15.68
+                # for the best full-width schedule, profiles/r02_rb_panels_cfg4.md),
                 # the logical mapping at N/c == 16 (config 4 / stencil 64^3 at
                 # N=64), adjacent rows per CTA step below (config 4 N=16)
                 lanes = n // widest
-                return Candidate(pt, p, 0, 4 if lanes == 32 else (0 if lanes >= 16 else 2))
+                return Candidate(pt, p, 0, 4 if lanes % 32 == 0 else (0 if lanes >= 16 else 2))
         pt = f"row:1,col:{col(widest)},r:1"
         return Candidate(pt, _first_p(pt, n) or 256)
     c = widest if n >= 16 else min(widest, max(1, n // 4))

@@ -96,7 +96,8 @@ def test_config3_reddit_shaped():
 def test_row_staged_variants():
     """Row-multiple with a warp per row (hw variants 3/4, N/c == 32): stencil
     rows (<= 27, the float32 path) and R-MAT hub rows (> 64, the float64
-    path) at N = 128 / 64 / 32."""
+    path) at N = 128 / 64 / 32; and at N/c = 64 / 128 (N = 256, 512), one
+    pass per 32c-column panel of B and C in place."""
     st = G.stencil27(64, device="cuda")
     rm = G.rmat(16, 16, seed=5, device="cuda")
     for g in (st, rm):
@@ -104,6 +105,18 @@ def test_row_staged_variants():
                               ("row:1,col:4,r:1", 256, 4), ("row:16,col:4,r:1", 256, 4)]))
         print(_check(g, 64, [("row:4,col:2,r:1", 256, 4), ("row:2,col:2,r:1", 256, 3)]))
         print(_check(g, 32, [("row:4,col:1,r:1", 256, 4)]))
+        print(_check(g, 256, [("row:8,col:4,r:1", 256, 4), ("row:4,col:2,r:1", 256, 3),
+                              ("row:2,col:4,r:1", 1024, 3)]))
+        print(_check(g, 512, [("row:8,col:4,r:1", 256, 4)]))
+    # N/c not a multiple of 32 (N = 192: 48 lanes): refused
+    k = lower(algorithm_template(parse_point("row:4,col:4,r:1"), KernelConfig(n=192, p=192)),
+              _Rp(st.num_rows, st.num_cols, st.row_ptr.cpu().numpy().astype(np.int64)),
+              compute_starts=False)
+    a = _device(st)
+    from paper_2209_02882_b200 import _native
+    with pytest.raises(_native.SgapError):
+        spmm(k, a, torch.zeros((a.num_cols, 192), device="cuda"),
+             torch.empty((a.num_rows, 192), device="cuda"), aux=prepare_aux(k, a), hw_variant=4)
 
 
 def test_stencil_small_n():

@@ -36,6 +36,10 @@ def test_heuristic_matrix_classes():
     assert heuristic(CHUNGLU, 256).hw_variant == 10
     assert heuristic(STENCIL160, 128).point.startswith("row:8")  # regular -> RB
     assert heuristic(STENCIL160, 128).hw_variant == 4             # warp per row
+    # and per 128-column panel at N = 256 / 512
+    assert (heuristic(STENCIL160, 512).point, heuristic(STENCIL160, 512).hw_variant) == \
+        ("row:8,col:4,r:1", 4)
+    assert heuristic(STENCIL160, 256).hw_variant == 4
     assert heuristic(STENCIL160, 16).point.startswith("row:4")
     assert heuristic(STENCIL160, 4).point == "row:1,col:4,r:1"
     # narrow B on power-law rows: serial segment groups; N=8: short chunks
@@ -55,5 +59,8 @@ def test_candidate_grid_covers_families_and_walks():
     assert {c.hw_variant for c in cands if c.point.startswith("nnz:64,col:4")} == {1, 5, 9, 2, 3, 10}
     assert {c.hw_variant for c in candidates(32) if c.point.startswith("nnz:64,col:4")} == {1, 5, 9, 2}
     # row-multiple: logical / interleaved, plus a warp per row where N/c == 32
+    # (one pass per 32c-column panel where N/c is a larger multiple of 32)
     assert {c.hw_variant for c in cands if c.point.startswith("row:4,col:4")} == {0, 2, 4, 6, 7}
-    assert {c.hw_variant for c in cands if c.point.startswith("row:4,col:2")} == {0, 2}
+    assert {c.hw_variant for c in cands if c.point.startswith("row:4,col:2")} == {0, 2, 4}
+    assert {c.hw_variant for c in candidates(192, p_values=(192,))
+            if c.point.startswith("row:4,col:4")} == {0, 2}  # N/c = 48
