@@ -304,6 +304,68 @@ k_row_staged(const int *__restrict__ rp, const int *__restrict__ ci, const T *__
     }
 }
 
+// The warp-per-row walk for N/c = 16 or 8 (hw variants 3/4 at N = 64 / 32
+// with c = 4): LPR = N/c lanes per row, 32/LPR adjacent rows per warp, each
+// row's (col, val) lane-staged LPR positions at a time and shuffled within
+// its LPR-lane segment, U B-row gathers in flight per lane.  The rows of a
+// warp share the trip count of the longest one (the shuffles need the whole
+// warp converged); shorter rows gather a valid row and skip the FMA.  Rows of
+// <= 64 nonzeros sum in float32 (as rb_short_staged); a warp holding a longer
+// row walks its rows per lane with rb_row (float64 sums / error-free).
+template <typename T, int V, int U, int LPR>
+__global__ void __launch_bounds__(256, 5)
+k_row_staged_sub(const int *__restrict__ rp, const int *__restrict__ ci,
+                 const T *__restrict__ av, const T *__restrict__ B, T *__restrict__ C, int M,
+                 int N, int g, int vec4, int accumulate) {
+    constexpr int RPW = 32 / LPR;  // rows per warp
+    const int warps = (int)(blockDim.x >> 5);
+    const int w = (int)(threadIdx.x >> 5);
+    const unsigned lane = lane_id();
+    const int sub = (int)(lane % LPR), slot = (int)(lane / LPR);
+    const long long kcol = (long long)sub * V;
+    const T *bk = B + kcol;
+    const long long tile_rows = (long long)warps * g * RPW;
+    const long long tiles = ((long long)M + tile_rows - 1) / tile_rows;
+    for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        for (int s = 0; s < g; ++s) {
+            const long long i0 = tile * tile_rows + ((long long)s * warps + w) * RPW;
+            if (i0 >= M) break;  // warp-uniform
+            const long long i = i0 + slot;
+            const bool ok = i < M;
+            const int beg = ok ? __ldg(rp + i) : 0, end = ok ? __ldg(rp + i + 1) : 0;
+            const int len = end - beg;
+            const int maxlen = __reduce_max_sync(kFull, len);
+            if (maxlen > 64) {  // a long row in this warp's group: per-lane walks
+                if (ok)
+                    store_vec<T, V>(C + i * N + kcol,
+                                    narrow<T, V>(rb_row<T, V>(ci, av, beg, end, bk, N, vec4 != 0)),
+                                    accumulate != 0);
+                continue;
+            }
+            Vec<T, V> acc;
+            acc.zero();
+            for (int s0 = 0; s0 < maxlen; s0 += LPR) {
+                const bool in = s0 + sub < len;
+                const int c_l = in ? __ldg(ci + beg + s0 + sub) : 0;  // column 0: a valid B row
+                const T v_l = in ? __ldg(av + beg + s0 + sub) : T(0);
+                const int nv = min(LPR, maxlen - s0);
+                for (int j = 0; j < nv; j += U) {
+                    Vec<T, V> b[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        gather_vec<T, V>(b[u], row_ptr(bk, __shfl_sync(kFull, c_l, (j + u) & (LPR - 1), LPR), N));
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const T v = __shfl_sync(kFull, v_l, (j + u) & (LPR - 1), LPR);
+                        if (j + u < nv && s0 + j + u < len) fma_vec<T, V>(acc, v, b[u]);
+                    }
+                }
+            }
+            if (ok) store_vec<T, V>(C + i * N + kcol, acc, accumulate != 0);
+        }
+    }
+}
+
 // ===========================================================================
 // Row-blocked RB walk (row-multiple hw variants 6 / 7, N/c == 32): a warp
 // owns R consecutive rows and walks the UNION of their column lists once --

@@ -126,7 +126,9 @@ def candidates(n: int, p_values=(256, 1024), g_values=GPU_G_VALUES,
                 # 4 at N/c = 64, 96, ...: the warp-per-row walk once per
                 # 32c-column panel (config 4 at N = 256 / 512)
                 L = n // tpl.c
-                vs = (0, 2, 4, 6, 7) if L == 32 else (0, 2, 4) if L % 32 == 0 else (0, 2)
+                # 3/4 at N/c = 16 / 8: 2 / 4 rows per warp (config 4 at N = 64 / 32)
+                vs = ((0, 2, 4, 6, 7) if L == 32 else (0, 2, 4) if L % 32 == 0
+                      else (0, 2, 3, 4) if L in (8, 16) else (0, 2))
                 out.extend(Candidate(str(pt), p, 0, v) for v in vs)
             else:
                 out.append(Candidate(str(pt), p))
@@ -199,10 +201,12 @@ def heuristic(stats: MatrixStats, n: int) -> Candidate:
                 # and once per 32c-column panel when N/c is a larger multiple
                 # of 32 (config 4 N=256 / 512: 6.10 / 12.21 ms vs 7.50 / 15.68
                 # for the best full-width schedule, profiles/r02_rb_panels_cfg4.md),
-                # the logical mapping at N/c == 16 (config 4 / stencil 64^3 at
-                # N=64), adjacent rows per CTA step below (config 4 N=16)
+                # and 2 / 4 rows per warp at N/c == 16 / 8 (config 4 N=64 / 32:
+                # 1.60 / 0.92 ms vs 1.94 / 1.11 for the logical mapping,
+                # profiles/r02_rb_subwarp_cfg4.md), adjacent rows per CTA step
+                # below (config 4 N=16)
                 lanes = n // widest
-                return Candidate(pt, p, 0, 4 if lanes % 32 == 0 else (0 if lanes >= 16 else 2))
+                return Candidate(pt, p, 0, 4 if (lanes % 32 == 0 or lanes in (8, 16)) else 2)
         pt = f"row:1,col:{col(widest)},r:1"
         return Candidate(pt, _first_p(pt, n) or 256)
     c = widest if n >= 16 else min(widest, max(1, n // 4))

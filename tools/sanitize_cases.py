@@ -59,7 +59,7 @@ def main():
         ("row:1,col:4,r:1", 256, 0), ("row:4,col:4,r:1", 256, 2), ("row:4,col:4,r:1", 256, 3),
         ("row:4,col:4,r:1", 256, 4), ("row:1/8,col:4,r:8", 256, 0), ("row:1/32,col:1,r:32", 256, 0),
     ]
-    for n in (128, 40):
+    for n in (128, 64, 40):
         b = torch.rand((k, n), device=dev) * 2 - 1
         for prec in (torch.float32, torch.float64):
             aa = DeviceCsr(m, k, a.row_ptr, a.col_idx, a.vals.to(prec))
@@ -71,9 +71,10 @@ def main():
                 tpl = algorithm_template(parse_point(text), KernelConfig(n=n, p=p))
                 if tpl is None:
                     continue
-                if variant in (3, 4) and (n // tpl.c) != 32 and text.startswith("row"):
+                if variant in (3, 4) and text.startswith("row") and not (
+                        (n // tpl.c) % 32 == 0 or (n // tpl.c) in (8, 16)):
                     continue
-                if variant in (3, 4) and (n // tpl.c) < 32:
+                if variant in (3, 4) and text.startswith("nnz") and (n // tpl.c) < 32:
                     continue
                 kk = lower(tpl, _Rp(m, k, rp), compute_starts=False)
                 aux = prepare_aux(kk, aa, validate=True, l2_hints=True)
