@@ -119,7 +119,10 @@ typedef struct {
                                gathers in flight; needs N/c >= 32).
                                row-multiple: 0/1 logical mapping, 2
                                interleaved rows, 3/4 interleaved + warp per
-                               row, lane-staged A (needs N/c == 32), 6/7 a
+                               row, lane-staged A (N/c == 32; N/c a larger
+                               multiple of 32: one pass per 32c-column
+                               panel of B and C in place; N/c == 16 / 8: 2 /
+                               4 rows per warp), 6/7 a
                                warp per 4/8-row block walking the union of
                                its columns (N/c == 32, rows <= 64).
                                nnz-one: 0 the shuffle segment scan, 1 each
