@@ -227,10 +227,12 @@ def heuristic(stats: MatrixStats, n: int) -> Candidate:
     # waits on row_ptr loads, 56% / 48% empty rows); otherwise row_ptr
     # tracking with the column-pipelined batches (config 3 at N = 64 / 256)
     b_bytes = stats.num_cols * n * 4
-    if panel_lanes(stats.num_cols, n, c) > 0:
-        # B larger than the L2 but a column panel fits half of it: walk the
-        # panels one at a time (config 3 at N = 256: 0.87x of variant 1,
-        # profiles/r02_panel_probe_cfg3_n256.log)
+    if b_bytes > 1.5 * L2_BYTES and panel_lanes(stats.num_cols, n, c) >= 16:
+        # B well beyond the L2 but a column panel of >= 16 tiles fits half of
+        # it: walk the panels one at a time (config 3 at N = 256: 0.79x of
+        # variant 1, profiles/r02_sweeps/); not for B just above the L2 with
+        # narrow panels (hold-out Chung-Lu 300k at N = 128, B = 154 MB,
+        # 32-column panels: 1.22x slower than variant 1)
         variant = 10
     elif b_bytes > 16 * L2_BYTES:
         variant = 9
