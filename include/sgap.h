@@ -121,8 +121,8 @@ typedef struct {
                                interleaved rows, 3/4 interleaved + warp per
                                row, lane-staged A (N/c == 32; N/c a larger
                                multiple of 32: one pass per 32c-column
-                               panel of B and C in place; N/c == 16 / 8: 2 /
-                               4 rows per warp), 6/7 a
+                               panel of B and C in place; N/c == 16 / 8 / 4 /
+                               2: 2 / 4 / 8 / 16 rows per warp), 6/7 a
                                warp per 4/8-row block walking the union of
                                its columns (N/c == 32, rows <= 64).
                                nnz-one: 0 the shuffle segment scan, 1 each

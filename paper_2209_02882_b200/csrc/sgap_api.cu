@@ -82,8 +82,9 @@ int launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStr
 // rows rg*g .. rg*g+g-1), 2 the interleaved mapping (a CTA's warps on adjacent
 // rows; needs N/c <= CTA size), 3/4 the interleaved mapping with a warp per
 // row and lane-staged A (8/4 gathers in flight; N/c == 32, once per
-// 32c-column panel when N/c is a larger multiple of 32, and 2 / 4 rows per
-// warp at N/c == 16 / 8), 6/7 the row-blocked union walk (N/c == 32).
+// 32c-column panel when N/c is a larger multiple of 32, and 2 / 4 / 8 / 16
+// rows per warp at N/c == 16 / 8 / 4 / 2), 6/7 the row-blocked union walk
+// (N/c == 32).
 template <typename T, int V>
 int run_row_multiple(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
                      int acc, const LongRows &lr, cudaStream_t st) {
@@ -120,7 +121,7 @@ int run_row_multiple(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T 
         // re-read (config 4 N=256/512: separate contiguous 128-column
         // SpMMs 0.82x of the best full-width schedule,
         // tools/experiments/stencil_panel_probe.py)
-        if (L == 16 || L == 8) {  // N/c = 16 / 8: 2 / 4 rows per warp
+        if (L == 16 || L == 8 || L == 4 || L == 2) {  // 2 / 4 / 8 / 16 rows per warp
             const long long tile_rows = (long long)(blk / 32) * k.g * (32 / L);
             const long long tiles = ceil_div(a.num_rows, tile_rows);
             const unsigned ctas =
@@ -132,11 +133,15 @@ int run_row_multiple(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T 
                     k_row_staged_sub<T, V, 8, 16><<<ctas, blk, 0, st>>>(a.d_row_ptr, a.d_col_idx, Av, B, C, M, N, k.g, vec4, acc);
                 else
                     k_row_staged_sub<T, V, 4, 16><<<ctas, blk, 0, st>>>(a.d_row_ptr, a.d_col_idx, Av, B, C, M, N, k.g, vec4, acc);
-            } else {
+            } else if (L == 8) {
                 if (k.hw_variant == 3)
                     k_row_staged_sub<T, V, 8, 8><<<ctas, blk, 0, st>>>(a.d_row_ptr, a.d_col_idx, Av, B, C, M, N, k.g, vec4, acc);
                 else
                     k_row_staged_sub<T, V, 4, 8><<<ctas, blk, 0, st>>>(a.d_row_ptr, a.d_col_idx, Av, B, C, M, N, k.g, vec4, acc);
+            } else if (L == 4) {  // U > LPR would only re-gather the segment
+                k_row_staged_sub<T, V, 4, 4><<<ctas, blk, 0, st>>>(a.d_row_ptr, a.d_col_idx, Av, B, C, M, N, k.g, vec4, acc);
+            } else {
+                k_row_staged_sub<T, V, 2, 2><<<ctas, blk, 0, st>>>(a.d_row_ptr, a.d_col_idx, Av, B, C, M, N, k.g, vec4, acc);
             }
             return launch_status();
         }

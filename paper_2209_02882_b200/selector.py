@@ -126,9 +126,11 @@ def candidates(n: int, p_values=(256, 1024), g_values=GPU_G_VALUES,
                 # 4 at N/c = 64, 96, ...: the warp-per-row walk once per
                 # 32c-column panel (config 4 at N = 256 / 512)
                 L = n // tpl.c
-                # 3/4 at N/c = 16 / 8: 2 / 4 rows per warp (config 4 at N = 64 / 32)
+                # 3/4 at N/c = 16 / 8 / 4 / 2: 2 / 4 / 8 / 16 rows per warp
+                # (config 4 at N = 64 / 32 / 16)
                 vs = ((0, 2, 4, 6, 7) if L == 32 else (0, 2, 4) if L % 32 == 0
-                      else (0, 2, 3, 4) if L in (8, 16) else (0, 2))
+                      else (0, 2, 3, 4) if L in (8, 16) else (0, 2, 4) if L in (2, 4)
+                      else (0, 2))
                 out.extend(Candidate(str(pt), p, 0, v) for v in vs)
             else:
                 out.append(Candidate(str(pt), p))
@@ -203,10 +205,10 @@ def heuristic(stats: MatrixStats, n: int) -> Candidate:
                 # for the best full-width schedule, profiles/r02_rb_panels_cfg4.md),
                 # and 2 / 4 rows per warp at N/c == 16 / 8 (config 4 N=64 / 32:
                 # 1.60 / 0.92 ms vs 1.94 / 1.11 for the logical mapping,
-                # profiles/r02_rb_subwarp_cfg4.md), adjacent rows per CTA step
-                # below (config 4 N=16)
+                # profiles/r02_rb_subwarp_cfg4.md), 8 rows per warp at N/c == 4
+                # (config 4 N=16: 0.52 vs 0.69 ms for adjacent rows per CTA step)
                 lanes = n // widest
-                return Candidate(pt, p, 0, 4 if (lanes % 32 == 0 or lanes in (8, 16)) else 2)
+                return Candidate(pt, p, 0, 4 if (lanes % 32 == 0 or lanes in (4, 8, 16)) else 2)
         pt = f"row:1,col:{col(widest)},r:1"
         return Candidate(pt, _first_p(pt, n) or 256)
     c = widest if n >= 16 else min(widest, max(1, n // 4))

@@ -97,8 +97,8 @@ def test_row_staged_variants():
     """Row-multiple with a warp per row (hw variants 3/4, N/c == 32): stencil
     rows (<= 27, the float32 path) and R-MAT hub rows (> 64, the float64
     path) at N = 128 / 64 / 32; at N/c = 64 / 128 (N = 256, 512), one pass
-    per 32c-column panel of B and C in place; at N/c = 16 / 8, 2 / 4 rows per
-    warp."""
+    per 32c-column panel of B and C in place; at N/c = 16 / 8 / 4 / 2, 2 / 4 / 8 / 16
+    rows per warp."""
     st = G.stencil27(64, device="cuda")
     rm = G.rmat(16, 16, seed=5, device="cuda")
     for g in (st, rm):
@@ -112,7 +112,8 @@ def test_row_staged_variants():
         # N/c = 16 / 8: 2 / 4 rows per warp (R-MAT hub rows take the per-lane walk)
         print(_check(g, 64, [("row:8,col:4,r:1", 1024, 4), ("row:4,col:4,r:1", 256, 3)]))
         print(_check(g, 32, [("row:8,col:4,r:1", 256, 4), ("row:4,col:2,r:1", 256, 3)]))
-        print(_check(g, 16, [("row:4,col:2,r:1", 256, 4)]))
+        print(_check(g, 16, [("row:4,col:2,r:1", 256, 4), ("row:8,col:4,r:1", 256, 4)]))
+        print(_check(g, 8, [("row:4,col:4,r:1", 256, 4)]))  # 2 lanes per row
     # N/c not a multiple of 32 (N = 192: 48 lanes): refused
     k = lower(algorithm_template(parse_point("row:4,col:4,r:1"), KernelConfig(n=192, p=192)),
               _Rp(st.num_rows, st.num_cols, st.row_ptr.cpu().numpy().astype(np.int64)),

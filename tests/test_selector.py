@@ -40,9 +40,8 @@ def test_heuristic_matrix_classes():
     assert (heuristic(STENCIL160, 512).point, heuristic(STENCIL160, 512).hw_variant) == \
         ("row:8,col:4,r:1", 4)
     assert heuristic(STENCIL160, 256).hw_variant == 4
-    # 2 / 4 rows per warp at N = 64 / 32; adjacent rows per CTA step at N = 16
-    assert heuristic(STENCIL160, 64).hw_variant == 4 and heuristic(STENCIL160, 32).hw_variant == 4
-    assert heuristic(STENCIL160, 16).hw_variant == 2
+    # 2 / 4 / 8 rows per warp at N = 64 / 32 / 16
+    assert {heuristic(STENCIL160, n).hw_variant for n in (16, 32, 64)} == {4}
     assert heuristic(STENCIL160, 16).point.startswith("row:4")
     assert heuristic(STENCIL160, 4).point == "row:1,col:4,r:1"
     # narrow B on power-law rows: serial segment groups; N=8: short chunks

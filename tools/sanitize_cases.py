@@ -72,7 +72,7 @@ def main():
                 if tpl is None:
                     continue
                 if variant in (3, 4) and text.startswith("row") and not (
-                        (n // tpl.c) % 32 == 0 or (n // tpl.c) in (8, 16)):
+                        (n // tpl.c) % 32 == 0 or (n // tpl.c) in (2, 4, 8, 16)):
                     continue
                 if variant in (3, 4) and text.startswith("nnz") and (n // tpl.c) < 32:
                     continue
