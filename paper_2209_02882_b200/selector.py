@@ -160,9 +160,11 @@ def _pow2_floor(x: float) -> int:
     return out
 
 
-def heuristic(stats: MatrixStats, n: int) -> Candidate:
+def heuristic(stats: MatrixStats, n: int, esz: int = 4) -> Candidate:
     """Closed-form schedule choice from row statistics and n, fitted to the
-    round-1 B200 sweeps (profiles/r01_sweep_*.json, r01_paper_claims.md):
+    round-1 B200 sweeps (profiles/r01_sweep_*.json, r01_paper_claims.md);
+    ``esz`` = bytes per value (8 for float64: vectors of at most 2 values,
+    profiles/r02_f64_configs.md):
 
     * regular rows (cv < 1, max <= 8 x mean):
       - n >= 16: RB + serial, 4 rows per logical thread, interleaved CTA
@@ -177,6 +179,8 @@ def heuristic(stats: MatrixStats, n: int) -> Candidate:
       clamped to [32, 512] so every warp slot gets several chunks.
     """
     widest = 4 if n % 4 == 0 else (2 if n % 2 == 0 else 1)
+    if esz == 8:  # float64: 16-byte vectors are 2 values (config 2/3/4 in
+        widest = min(widest, 2)  # float64: col:2 1.4-2.0x faster than col:4)
     col = lambda c: "1" if c == 1 else str(c)  # noqa: E731
     regular = stats.cv_row < 1.0 and stats.max_row <= 8 * max(stats.mean_row, 1.0)
     if regular:
@@ -228,8 +232,8 @@ def heuristic(stats: MatrixStats, n: int) -> Candidate:
     # per-position row ids (config 2: every row change of the row_ptr walk
     # waits on row_ptr loads, 56% / 48% empty rows); otherwise row_ptr
     # tracking with the column-pipelined batches (config 3 at N = 64 / 256)
-    b_bytes = stats.num_cols * n * 4
-    if b_bytes > 1.5 * L2_BYTES and panel_lanes(stats.num_cols, n, c) >= 16:
+    b_bytes = stats.num_cols * n * esz
+    if b_bytes > 1.5 * L2_BYTES and panel_lanes(stats.num_cols, n, c, esz) >= 16:
         # B well beyond the L2 but a column panel of >= 16 tiles fits half of
         # it: walk the panels one at a time (config 3 at N = 256: 0.79x of
         # variant 1, profiles/r02_sweeps/); not for B just above the L2 with

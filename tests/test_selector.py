@@ -51,6 +51,13 @@ def test_heuristic_matrix_classes():
     assert heuristic(UNIFORM1, 32).point == "row:1/2,col:2,r:2"
 
 
+def test_heuristic_float64_uses_16_byte_vectors():
+    # float64 (the reference's default precision): col:2 = one 16-byte vector
+    assert ",col:2," in heuristic(RMAT20, 128, esz=8).point
+    assert heuristic(STENCIL160, 128, esz=8).point == "row:8,col:2,r:1"
+    assert heuristic(STENCIL160, 128, esz=8).hw_variant == 4  # 2 panels of 64 columns
+
+
 def test_candidate_grid_covers_families_and_walks():
     cands = candidates(128)
     fams = {algorithm_template(parse_point(c.point), KernelConfig(128, c.p)).family for c in cands}

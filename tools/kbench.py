@@ -26,15 +26,18 @@ ap.add_argument("--check", action="store_true")
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--out", default="")
 ap.add_argument("--cusparse", action="store_true")
+ap.add_argument("--dtype", default="f32", choices=["f32", "f64"],
+                help="value type of A, B and C (f64: the reference's default precision)")
 args = ap.parse_args()
 dev = torch.device("cuda", 0)
+DT = torch.float64 if args.dtype == "f64" else torch.float32
 n = args.n or bench.default_n(args.config)
 g, desc, _ = bench.build_workload(args.config, 1, 1, dev)
 a = DeviceCsr(g.num_rows, g.num_cols, g.row_ptr.to(torch.int32), g.col_idx.to(torch.int32),
-              g.vals.to(torch.float32))
+              g.vals.to(DT))
 touched = int(torch.unique(a.col_idx).numel())
-b = bench.dense_b(g.num_cols, n, 1, dev)
-c = torch.empty((a.num_rows, n), dtype=torch.float32, device=dev)
+b = bench.dense_b(g.num_cols, n, 1, dev).to(DT)
+c = torch.empty((a.num_rows, n), dtype=DT, device=dev)
 rp = a.row_ptr.cpu().numpy().astype(np.int64)
 if args.all:
     cands = candidates(n)
@@ -46,7 +49,8 @@ else:
             for hv in args.variants.split(","):
                 cands.append(Candidate(pt, int(p), int(hb), int(hv)))
 res = autotune(a, b, c, n, cands, reps=args.reps, row_ptr_host=rp, max_ms=100.0)
-abytes = bench.algorithmic_bytes(a.num_rows, a.nnz, n, touched)
+esz = 8 if args.dtype == "f64" else 4
+abytes = bench.algorithmic_bytes(a.num_rows, a.nnz, n, touched, esz) + (esz - 4) * a.nnz
 print(desc, "nnz", a.nnz, "n", n, "algorithmic MB", abytes / 1e6)
 rows = []
 for cd, ms in res:
@@ -65,7 +69,8 @@ if args.check:
         spmm(k, a, b, c, hw_block=cd.hw_block, hw_variant=cd.hw_variant)
         torch.cuda.synchronize()
         err = oracle.max_rel_error(c.cpu().numpy(), want)
-        print(f"check {cd.label():32s} max_rel_error {err:.3e}", "OK" if err <= 1e-5 else "FAIL")
+        tol = 1e-12 if args.dtype == "f64" else 1e-5
+        print(f"check {cd.label():32s} max_rel_error {err:.3e}", "OK" if err <= tol else "FAIL")
 if args.out:
     Path(args.out).write_text(json.dumps({"workload": desc, "n": n, "rows": rows}, indent=1))
 
