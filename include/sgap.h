@@ -124,7 +124,13 @@ typedef struct {
                                panel of B and C in place; N/c == 16 / 8 / 4 /
                                2: 2 / 4 / 8 / 16 rows per warp), 6/7 a
                                warp per 4/8-row block walking the union of
-                               its columns (N/c == 32, rows <= 64).
+                               its columns (N/c == 32, rows <= 64), 8 a
+                               warp per 4-row block: blocks whose rows are
+                               shifted copies (row i0+r's columns = row
+                               i0's + r, <= 32 each: banded / stencil rows)
+                               gather each shared B row once, other blocks
+                               take 4's walk; bit-identical to 4 (N/c a
+                               multiple of 32, panels as 4).
                                nnz-one: 0 the shuffle segment scan, 1 each
                                segment group walked serially by lanes along
                                the columns (same writebacks).

@@ -84,7 +84,8 @@ int launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStr
 // row and lane-staged A (8/4 gathers in flight; N/c == 32, once per
 // 32c-column panel when N/c is a larger multiple of 32, and 2 / 4 / 8 / 16
 // rows per warp at N/c == 16 / 8 / 4 / 2), 6/7 the row-blocked union walk
-// (N/c == 32).
+// (N/c == 32), 8 the shifted-block walk (4 rows per warp; N/c a multiple
+// of 32, panels as 3/4).
 template <typename T, int V>
 int run_row_multiple(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T *C,
                      int acc, const LongRows &lr, cudaStream_t st) {
@@ -111,6 +112,25 @@ int run_row_multiple(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T 
                                                                lr.union_off[1], Av, B, C,
                                                                (int)a.num_rows, N, k.g, acc);
         return launch_status();
+    }
+    if (k.hw_variant == 8) {  // shifted blocks of 4 rows
+        // N/c == 32, or one pass per 32c-column panel (as variant 4)
+        if (L % 32) return SGAP_ERR_ARG;
+        // 128-thread CTAs by default (config 4 N=128: 2.06 vs 2.27 ms at 256)
+        const int sblk = k.hw_block > 0 ? k.hw_block : 128;
+        const long long nblocks = ceil_div(a.num_rows, 4);
+        const long long want = ceil_div(nblocks, sblk / 32);
+        const unsigned ctas = (unsigned)(want < (1LL << 30) ? (want > 0 ? want : 1) : (1LL << 30));
+        const T *Av = static_cast<const T *>(a.d_vals);
+        const int M = (int)a.num_rows;
+        for (int pan = 0; pan < L / 32; ++pan) {
+            const long long off = (long long)pan * 32 * V;
+            k_row_shifted<T, V, 4><<<ctas, sblk, 0, st>>>(a.d_row_ptr, a.d_col_idx, Av, B + off,
+                                                          C + off, M, N, vec4, acc);
+            const int s0 = launch_status();
+            if (s0 != SGAP_OK) return s0;
+        }
+        return SGAP_OK;
     }
     if (k.hw_variant == 3 || k.hw_variant == 4) {  // lane-staged, a warp per row
         // N/c == 32: one pass.  N/c a multiple of 32 (N >= 256 at c = 4): one

@@ -367,6 +367,122 @@ k_row_staged_sub(const int *__restrict__ rp, const int *__restrict__ ci,
 }
 
 // ===========================================================================
+// Shifted-block RB walk (row-multiple hw variant 8: R = 4 rows per warp,
+// N/c == 32, once per 32c-column panel for larger multiples of 32).
+// A block of R consecutive rows is "shifted" when every row has the same
+// length L <= 32 and row i0+r's column list is row i0's plus r -- the rows of
+// a banded / stencil matrix away from the grid edges (27-point stencil: 9
+// runs of 3 consecutive columns per row).  Row i0's list is cut into pieces
+// of w <= 3 consecutive columns; a piece starting at column cb is needed by
+// the block's rows as B rows cb .. cb + R + w - 2, so the warp gathers those
+// R + w - 1 rows once and each feeds up to w rows' sums (stencil: 90 B-row
+// gathers per 8 rows instead of 216, every FMA useful -- no masks, no zero
+// padding).  The values stay in the CSR: lane p holds position p of each of
+// the R rows (R coalesced loads) and shuffles it to the FMA.  Each row still
+// sums its own nonzeros serially in CSR order in float32, exactly as the
+// warp-per-row walk's rb_short_staged does (lowering.py:573-585), so the
+// results are bit-identical to hw variant 4 and the writebacks are one per
+// (row, tile).  Blocks that are not shifted (grid edges, irregular rows,
+// rows > 32) take the warp-per-row walk inline.  The property is checked per
+// block from the column stream the walk reads anyway: no plan data.
+// Config 4 (N = 128): 2.06 vs 3.07 ms for the warp-per-row walk; ncu: 1.24G
+// instructions (from 2.09G), L2->L1 sectors unchanged (764M: the x-neighbour
+// reuse moved from L1 to registers), long-scoreboard bound.  Measured and not
+// kept (config 4, N = 128/256): R = 8 (124 registers, 2 CTAs/SM) 1.5-1.6x
+// slower; two 3-wide pieces gathered back to back (2(R + 2) rows in flight,
+// 80 registers) 1.03-1.17x slower; 48 registers for 5 CTAs/SM: spills, 1.5x
+// slower; the next piece's B rows prefetched into L1 under this piece's
+// gathers: 1.09x slower.
+// ===========================================================================
+template <typename T, int V, int R, int W>
+__device__ __forceinline__ void shifted_piece(Vec<T, V> (&acc)[R], const T (&v)[R], int p,
+                                              const T *__restrict__ bk, int cb, int N) {
+    Vec<T, V> b[R + W - 1];
+#pragma unroll
+    for (int q = 0; q < R + W - 1; ++q) gather_vec<T, V>(b[q], row_ptr(bk, cb + q, N));
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+#pragma unroll
+        for (int j = 0; j < W; ++j)
+            fma_vec<T, V>(acc[r], __shfl_sync(kFull, v[r], p + j), b[r + j]);
+    }
+}
+
+template <typename T, int V, int R>
+__global__ void __launch_bounds__(256, 4)
+k_row_shifted(const int *__restrict__ rp, const int *__restrict__ ci, const T *__restrict__ av,
+              const T *__restrict__ B, T *__restrict__ C, int M, int N, int vec4,
+              int accumulate) {
+    const int warps = (int)(blockDim.x >> 5);
+    const unsigned lane = lane_id();
+    const long long kcol = (long long)lane * V;
+    const T *bk = B + kcol;
+    const long long nblocks = ((long long)M + R - 1) / R;
+    for (long long blk = (long long)blockIdx.x * warps + (threadIdx.x >> 5); blk < nblocks;
+         blk += (long long)gridDim.x * warps) {
+        const long long i0 = blk * R;
+        // lanes 0..R: the block's row starts (one load)
+        const int t = (int)lane <= R ? __ldg(rp + (i0 + lane < M ? i0 + lane : (long long)M)) : 0;
+        const int p0 = __shfl_sync(kFull, t, 0);
+        const int L = __shfl_sync(kFull, t, 1) - p0;
+        const int nxt = __shfl_down_sync(kFull, t, 1);
+        bool ok = i0 + R <= M && L >= 1 && L <= 32 &&
+                  __all_sync(kFull, (int)lane >= R || nxt - t == L);
+        int c0 = 0;
+        T v[R];
+        if (ok) {
+            const bool in = (int)lane < L;
+            c0 = in ? __ldg(ci + p0 + lane) : 0;
+            bool sh = true;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int q = p0 + r * L + (int)lane;
+                v[r] = in ? __ldg(av + q) : T(0);
+                if (r > 0 && in) sh = sh && __ldg(ci + q) == c0 + r;
+            }
+            ok = __all_sync(kFull, sh);
+        }
+        if (!ok) {  // the warp-per-row walk (hw variant 4) for this block
+#pragma unroll 1
+            for (int r = 0; r < R; ++r) {
+                const long long i = i0 + r;
+                if (i >= M) break;
+                const int beg = __shfl_sync(kFull, t, r), end = __shfl_sync(kFull, t, r + 1);
+                if (end - beg > 64)
+                    rb_long_staged<T, V, 4>(ci, av, beg, end, bk, N, vec4, C + i * N + kcol,
+                                            accumulate);
+                else
+                    store_vec<T, V>(C + i * N + kcol,
+                                    rb_short_staged<T, V, 4>(ci, av, beg, end, bk, N),
+                                    accumulate != 0);
+            }
+            continue;
+        }
+        // bit p: column p of row i0 continues column p - 1 (runs of consecutive columns)
+        const int up = __shfl_up_sync(kFull, c0, 1);
+        const unsigned long long cont =
+            __ballot_sync(kFull, lane > 0 && (int)lane < L && c0 == up + 1);
+        Vec<T, V> acc[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r].zero();
+        for (int p = 0; p < L;) {
+            const int cb = __shfl_sync(kFull, c0, p);
+            const int w = ((cont >> (p + 1)) & 1ull) ? (((cont >> (p + 2)) & 1ull) ? 3 : 2) : 1;
+            if (w == 3)
+                shifted_piece<T, V, R, 3>(acc, v, p, bk, cb, N);
+            else if (w == 2)
+                shifted_piece<T, V, R, 2>(acc, v, p, bk, cb, N);
+            else
+                shifted_piece<T, V, R, 1>(acc, v, p, bk, cb, N);
+            p += w;
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+            store_vec<T, V>(C + (i0 + r) * (long long)N + kcol, acc[r], accumulate != 0);
+    }
+}
+
+// ===========================================================================
 // Row-blocked RB walk (row-multiple hw variants 6 / 7, N/c == 32): a warp
 // owns R consecutive rows and walks the UNION of their column lists once --
 // a plan-time stream of (col | row-mask << (32 - R)) entries per R-row block,

@@ -417,7 +417,7 @@ def launches_per_call(k: LoweredKernel, aux: KernelAux | None, *, accumulate: bo
             w = min(32, max(1, k.n // k.c))
             variant = hw_variant or (2 if (w >= 16 and k.g <= 128) else 1)
             n += 0 if variant in (1, 5, 9, 10) else 1
-    if k.family == "row-multiple" and hw_variant in (3, 4) and k.c and k.n // k.c > 32:
+    if k.family == "row-multiple" and hw_variant in (3, 4, 8) and k.c and k.n // k.c > 32:
         n += k.n // k.c // 32 - 1  # one warp-per-row pass per 32c-column panel
     if k.family == "nnz-multiple" and hw_variant == 10 and aux is not None:
         lanes = int(aux.plan.aux.panel_lanes)

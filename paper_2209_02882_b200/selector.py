@@ -128,7 +128,10 @@ def candidates(n: int, p_values=(256, 1024), g_values=GPU_G_VALUES,
                 L = n // tpl.c
                 # 3/4 at N/c = 16 / 8 / 4 / 2: 2 / 4 / 8 / 16 rows per warp
                 # (config 4 at N = 64 / 32 / 16)
-                vs = ((0, 2, 4, 6, 7) if L == 32 else (0, 2, 4) if L % 32 == 0
+                # 8 at N/c a multiple of 32: shifted blocks of 4 rows
+                # (banded rows share shifted column lists; other blocks fall
+                # back to the warp-per-row walk inline)
+                vs = ((0, 2, 4, 6, 7, 8) if L == 32 else (0, 2, 4, 8) if L % 32 == 0
                       else (0, 2, 3, 4) if L in (8, 16) else (0, 2, 4) if L in (2, 4)
                       else (0, 2))
                 out.extend(Candidate(str(pt), p, 0, v) for v in vs)
@@ -211,8 +214,14 @@ def heuristic(stats: MatrixStats, n: int, esz: int = 4) -> Candidate:
                 # 1.60 / 0.92 ms vs 1.94 / 1.11 for the logical mapping,
                 # profiles/r02_rb_subwarp_cfg4.md), 8 rows per warp at N/c == 4
                 # (config 4 N=16: 0.52 vs 0.69 ms for adjacent rows per CTA step)
+                # At N/c a multiple of 32 the shifted-block walk (variant 8),
+                # which is the warp-per-row walk on blocks whose rows are not
+                # shifted copies of each other (config 4 N=128: 2.06 vs 3.07
+                # ms, N=256 / 512: 0.67x, profiles/r02_rb_shifted_cfg4.md)
                 lanes = n // widest
-                return Candidate(pt, p, 0, 4 if (lanes % 32 == 0 or lanes in (4, 8, 16)) else 2)
+                if lanes % 32 == 0:
+                    return Candidate(pt, p, 0, 8)
+                return Candidate(pt, p, 0, 4 if lanes in (4, 8, 16) else 2)
         pt = f"row:1,col:{col(widest)},r:1"
         return Candidate(pt, _first_p(pt, n) or 256)
     c = widest if n >= 16 else min(widest, max(1, n // 4))

@@ -136,6 +136,7 @@ def test_config4_stencil160_n_sweep(n):
         pts.append((f"row:8,col:{c},r:1", 256, 3))  # warp per row, lane-staged A
     if n // c >= 32:
         pts.append((f"nnz:256,col:{c},r:1", 256, 4))  # lane-staged EB walk
+        pts.append((f"row:8,col:{c},r:1", 256, 8))  # shifted 4-row blocks (panels from N=256)
     _check_points(g, n, pts, label="config4")
 
 

@@ -292,6 +292,76 @@ def test_row_blocked_union_walk(variant):
         spmm(kr, ar, br, cr, aux=prepare_aux(kr, ar), hw_variant=variant)
 
 
+def test_shifted_block_walk_bitwise():
+    """Row-multiple hw variant 8 (shifted 4-row blocks, gathers shared
+    across the block) give C bit-identical to the warp-per-row walk (variant
+    4): each row is summed serially in CSR order either way, and blocks that
+    are not shifted copies (grid edges, ragged or long rows, M not a multiple
+    of the block) take that walk inline.  Stencil, a band with empty rows,
+    a tridiagonal-plus-hub matrix, N/c = 32 and 64 (column panels), float32
+    and float64, overwrite and accumulate; also against the oracle."""
+    import types
+    variant = 8
+    rng = np.random.default_rng(variant)
+    # band with ragged rows (few shifted blocks) and empty rows
+    m, k = 10_003, 9_000
+    lens = rng.integers(0, 40, m)
+    lens[::17] = 0
+    cols = []
+    for i, L in enumerate(lens):
+        lo = max(0, min(k - 80, i * k // m - 40))
+        cols.append(np.sort(rng.choice(np.arange(lo, lo + 80), int(L), replace=False)))
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    band = types.SimpleNamespace(num_rows=m, num_cols=k, row_ptr=torch.from_numpy(rp).cuda(),
+                                 col_idx=torch.from_numpy(np.concatenate(cols)).cuda(),
+                                 vals=torch.from_numpy(rng.uniform(-1, 1, rp[-1])).cuda())
+    # tridiagonal rows (shifted blocks) with runs of 1/2/4/5 and a few hub rows
+    m2 = 5_001
+    offs = np.array([-700, -3, -2, -1, 0, 1, 5, 6, 7, 8, 9, 300])
+    rows2, cols2 = [], []
+    for i in range(m2):
+        cs = i + offs
+        cs = cs[(cs >= 0) & (cs < m2)]
+        if i % 1000 == 500:  # a hub row longer than 64 (float64 path inline)
+            cs = np.unique(np.concatenate([cs, rng.choice(m2, 300, replace=False)]))
+        rows2.append(np.full(cs.size, i))
+        cols2.append(cs)
+    lens2 = np.array([c.size for c in cols2])
+    rp2 = np.concatenate([[0], np.cumsum(lens2)]).astype(np.int64)
+    tri = types.SimpleNamespace(num_rows=m2, num_cols=m2, row_ptr=torch.from_numpy(rp2).cuda(),
+                                col_idx=torch.from_numpy(np.concatenate(cols2)).cuda(),
+                                vals=torch.from_numpy(rng.uniform(-1, 1, rp2[-1])).cuda())
+    for g in (G.stencil27(40, device="cuda"), band, tri):
+        for n, c in ((128, 4), (256, 4), (64, 2)):
+            for dt, tol in ((torch.float32, TOL), (torch.float64, 1e-12)):
+                a0 = _device(g)
+                a = DeviceCsr(a0.num_rows, a0.num_cols, a0.row_ptr, a0.col_idx, g.vals.to(dt))
+                rph = a.row_ptr.cpu().numpy().astype(np.int64)
+                b = torch.rand((a.num_cols, n), dtype=dt, device="cuda") * 2 - 1
+                tpl = algorithm_template(parse_point(f"row:8,col:{c},r:1"),
+                                         KernelConfig(n=n, p=256))
+                kk = lower(tpl, _Rp(a.num_rows, a.num_cols, rph), compute_starts=False)
+                outs = []
+                for v in (4, variant):
+                    for acc in (False, True):
+                        cc = torch.full((a.num_rows, n), 0.5, dtype=dt, device="cuda")
+                        spmm(kk, a, b, cc, aux=prepare_aux(kk, a), accumulate=acc, hw_variant=v)
+                        outs.append(cc)
+                assert torch.equal(outs[0], outs[2]) and torch.equal(outs[1], outs[3]), (n, c, dt)
+                want = oracle.spmm_f64(rph.astype(np.int32), a.col_idx.cpu().numpy(),
+                                       a.vals.cpu().numpy(), b.cpu().numpy(), n)
+                assert oracle.max_rel_error(outs[2].cpu().numpy(), want) <= tol
+                assert oracle.max_rel_error(outs[3].cpu().numpy(), want + 0.5) <= tol
+    # N/c not a multiple of 32: refused (SGAP_ERR_ARG)
+    from paper_2209_02882_b200 import _native
+    a = _device(tri)
+    tpl = algorithm_template(parse_point("row:8,col:4,r:1"), KernelConfig(n=64, p=256))
+    kk = lower(tpl, _Rp(a.num_rows, a.num_cols, rp2), compute_starts=False)
+    with pytest.raises(_native.SgapError):
+        spmm(kk, a, torch.rand((m2, 64), device="cuda"), torch.empty((m2, 64), device="cuda"),
+             aux=prepare_aux(kk, a), hw_variant=variant)
+
+
 def test_cold_column_hint_walk():
     """hw variant 9: the row_ptr walk reading the plan's flagged col_idx copy
     (bit 31 = cold column, gathered with the streaming cache operator):

@@ -35,11 +35,11 @@ def test_heuristic_matrix_classes():
     # B = 238 MB > L2 but a 64-column panel (60 MB) fits half of it: column panels
     assert heuristic(CHUNGLU, 256).hw_variant == 10
     assert heuristic(STENCIL160, 128).point.startswith("row:8")  # regular -> RB
-    assert heuristic(STENCIL160, 128).hw_variant == 4             # warp per row
+    assert heuristic(STENCIL160, 128).hw_variant == 8             # shifted 4-row blocks
     # and per 128-column panel at N = 256 / 512
     assert (heuristic(STENCIL160, 512).point, heuristic(STENCIL160, 512).hw_variant) == \
-        ("row:8,col:4,r:1", 4)
-    assert heuristic(STENCIL160, 256).hw_variant == 4
+        ("row:8,col:4,r:1", 8)
+    assert heuristic(STENCIL160, 256).hw_variant == 8
     # 2 / 4 / 8 rows per warp at N = 64 / 32 / 16
     assert {heuristic(STENCIL160, n).hw_variant for n in (16, 32, 64)} == {4}
     assert heuristic(STENCIL160, 16).point.startswith("row:4")
@@ -55,7 +55,7 @@ def test_heuristic_float64_uses_16_byte_vectors():
     # float64 (the reference's default precision): col:2 = one 16-byte vector
     assert ",col:2," in heuristic(RMAT20, 128, esz=8).point
     assert heuristic(STENCIL160, 128, esz=8).point == "row:8,col:2,r:1"
-    assert heuristic(STENCIL160, 128, esz=8).hw_variant == 4  # 2 panels of 64 columns
+    assert heuristic(STENCIL160, 128, esz=8).hw_variant == 8  # 2 panels of 64 columns
 
 
 def test_candidate_grid_covers_families_and_walks():
@@ -69,7 +69,7 @@ def test_candidate_grid_covers_families_and_walks():
     assert {c.hw_variant for c in candidates(32) if c.point.startswith("nnz:64,col:4")} == {1, 5, 9, 2}
     # row-multiple: logical / interleaved, plus a warp per row where N/c == 32
     # (one pass per 32c-column panel where N/c is a larger multiple of 32)
-    assert {c.hw_variant for c in cands if c.point.startswith("row:4,col:4")} == {0, 2, 4, 6, 7}
-    assert {c.hw_variant for c in cands if c.point.startswith("row:4,col:2")} == {0, 2, 4}
+    assert {c.hw_variant for c in cands if c.point.startswith("row:4,col:4")} == {0, 2, 4, 6, 7, 8}
+    assert {c.hw_variant for c in cands if c.point.startswith("row:4,col:2")} == {0, 2, 4, 8}
     assert {c.hw_variant for c in candidates(192, p_values=(192,))
             if c.point.startswith("row:4,col:4")} == {0, 2}  # N/c = 48
