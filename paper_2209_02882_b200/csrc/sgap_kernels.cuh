@@ -482,6 +482,135 @@ k_row_shifted(const int *__restrict__ rp, const int *__restrict__ ci, const T *_
     }
 }
 
+// Shifted-block walk for N/c = LPR = 16 (hw variant 8 at N = 64 with c = 4):
+// G = 32 / LPR lane groups of LPR lanes, each owning 4 consecutive rows of
+// an 8-row warp block (config 4 N=64: 1.40 vs 1.61 ms for variant 4; LPR = 8
+// was 1.33x slower: its 16 staged values per lane spill at 64 registers).  When the whole warp block is shifted
+// (as k_row_shifted checks it), every group walks the same pieces of row
+// i0's column list -- group g's piece starts at column cb + 4g -- gathering
+// 3 + w LPR-lane B rows per piece for its 4 rows.  Lane (g, l) keeps
+// positions l, l + LPR, ... of its group's rows (32 / LPR slots; the slot of
+// a position is warp-uniform) and serves them with LPR-wide shuffles.  Other
+// warp blocks run k_row_staged_sub's walk (4 rounds of G rows), so C is
+// bit-identical to hw variant 4 at the same N/c.
+template <typename T, int V, int LPR>
+__global__ void __launch_bounds__(256, 4)
+k_row_shifted_sub(const int *__restrict__ rp, const int *__restrict__ ci,
+                  const T *__restrict__ av, const T *__restrict__ B, T *__restrict__ C, int M,
+                  int N, int vec4, int accumulate) {
+    constexpr int G = 32 / LPR;  // lane groups per warp
+    constexpr int S = 32 / LPR;  // staged slots per lane (L <= 32)
+    constexpr int RB = 4 * G;    // rows per warp block
+    constexpr int U = 4;
+    const int warps = (int)(blockDim.x >> 5);
+    const unsigned lane = lane_id();
+    const int sub = (int)(lane % LPR), grp = (int)(lane / LPR);
+    const long long kcol = (long long)sub * V;
+    const T *bk = B + kcol;
+    const long long nblocks = ((long long)M + RB - 1) / RB;
+    for (long long blk = (long long)blockIdx.x * warps + (threadIdx.x >> 5); blk < nblocks;
+         blk += (long long)gridDim.x * warps) {
+        const long long i0 = blk * RB;
+        const int t = (int)lane <= RB ? __ldg(rp + (i0 + lane < M ? i0 + lane : (long long)M)) : 0;
+        const int p0 = __shfl_sync(kFull, t, 0);
+        const int L = __shfl_sync(kFull, t, 1) - p0;
+        const int nxt = __shfl_down_sync(kFull, t, 1);
+        bool ok = i0 + RB <= M && L >= 1 && L <= 32 &&
+                  __all_sync(kFull, (int)lane >= RB || nxt - t == L);
+        int c0 = 0;
+        if (ok) {
+            const bool in = (int)lane < L;
+            c0 = in ? __ldg(ci + p0 + lane) : 0;
+            bool sh = true;
+#pragma unroll 4
+            for (int r = 1; r < RB; ++r)
+                if (in) sh = sh && __ldg(ci + p0 + r * L + (int)lane) == c0 + r;
+            ok = __all_sync(kFull, sh);
+        }
+        if (!ok) {  // k_row_staged_sub's walk: 4 rounds of G adjacent rows (one per
+                    // group, paired as that kernel pairs them: a round whose
+                    // longest row exceeds 64 walks all its rows in float64)
+#pragma unroll 1
+            for (int k = 0; k < 4; ++k) {
+                const long long i = i0 + G * k + grp;
+                const bool in = i < M;
+                const int beg = in ? __ldg(rp + i) : 0, end = in ? __ldg(rp + i + 1) : 0;
+                const int len = end - beg;
+                const int maxlen = __reduce_max_sync(kFull, len);
+                if (maxlen > 64) {
+                    if (in)
+                        store_vec<T, V>(C + i * N + kcol,
+                                        narrow<T, V>(rb_row<T, V>(ci, av, beg, end, bk, N, vec4 != 0)),
+                                        accumulate != 0);
+                    continue;
+                }
+                Vec<T, V> a1;
+                a1.zero();
+                for (int s0 = 0; s0 < maxlen; s0 += LPR) {
+                    const bool q = s0 + sub < len;
+                    const int c_l = q ? __ldg(ci + beg + s0 + sub) : 0;
+                    const T v_l = q ? __ldg(av + beg + s0 + sub) : T(0);
+                    const int nv = min(LPR, maxlen - s0);
+                    for (int j = 0; j < nv; j += U) {
+                        Vec<T, V> b[U];
+#pragma unroll
+                        for (int u = 0; u < U; ++u)
+                            gather_vec<T, V>(b[u], row_ptr(bk, __shfl_sync(kFull, c_l, (j + u) & (LPR - 1), LPR), N));
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            const T v = __shfl_sync(kFull, v_l, (j + u) & (LPR - 1), LPR);
+                            if (j + u < nv && s0 + j + u < len) fma_vec<T, V>(a1, v, b[u]);
+                        }
+                    }
+                }
+                if (in) store_vec<T, V>(C + i * N + kcol, a1, accumulate != 0);
+            }
+            continue;
+        }
+        // group grp's rows i0 + 4 grp + r: positions sub + LPR s in slot s
+        T v[4][S];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const int pos = sub + LPR * s;
+                v[r][s] = pos < L ? __ldg(av + p0 + (4 * grp + r) * L + pos) : T(0);
+            }
+        const int up = __shfl_up_sync(kFull, c0, 1);
+        const unsigned long long cont =
+            __ballot_sync(kFull, lane > 0 && (int)lane < L && c0 == up + 1);
+        Vec<T, V> acc[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[r].zero();
+        for (int p = 0; p < L;) {
+            const int cb = __shfl_sync(kFull, c0, p) + 4 * grp;
+            const int w = ((cont >> (p + 1)) & 1ull) ? (((cont >> (p + 2)) & 1ull) ? 3 : 2) : 1;
+            Vec<T, V> b[6];
+#pragma unroll
+            for (int q = 0; q < 6; ++q)
+                if (q < 3 + w) gather_vec<T, V>(b[q], row_ptr(bk, cb + q, N));
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+#pragma unroll
+                for (int j = 0; j < 3; ++j) {
+                    if (j < w) {
+                        const int pos = p + j;
+                        T x = v[r][0];
+#pragma unroll
+                        for (int s = 1; s < S; ++s)
+                            if (pos / LPR == s) x = v[r][s];
+                        fma_vec<T, V>(acc[r], __shfl_sync(kFull, x, pos & (LPR - 1), LPR), b[r + j]);
+                    }
+                }
+            }
+            p += w;
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+            store_vec<T, V>(C + (i0 + 4 * grp + r) * (long long)N + kcol, acc[r], accumulate != 0);
+    }
+}
+
 // ===========================================================================
 // Row-blocked RB walk (row-multiple hw variants 6 / 7, N/c == 32): a warp
 // owns R consecutive rows and walks the UNION of their column lists once --
