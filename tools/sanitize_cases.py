@@ -58,6 +58,7 @@ def main():
         ("nnz:1,col:4,r:8", 1024, 0), ("nnz:1,col:4,r:1", 256, 0), ("nnz:1,col:1,r:32", 1024, 0),
         ("row:1,col:4,r:1", 256, 0), ("row:4,col:4,r:1", 256, 2), ("row:4,col:4,r:1", 256, 3),
         ("row:4,col:4,r:1", 256, 4), ("row:1/8,col:4,r:8", 256, 0), ("row:1/32,col:1,r:32", 256, 0),
+        ("row:4,col:4,r:1", 256, 8),
     ]
     for n in (128, 64, 40):
         b = torch.rand((k, n), device=dev) * 2 - 1
@@ -75,6 +76,8 @@ def main():
                         (n // tpl.c) % 32 == 0 or (n // tpl.c) in (2, 4, 8, 16)):
                     continue
                 if variant in (3, 4) and text.startswith("nnz") and (n // tpl.c) < 32:
+                    continue
+                if variant == 8 and not ((n // tpl.c) % 32 == 0 or n // tpl.c == 16):
                     continue
                 kk = lower(tpl, _Rp(m, k, rp), compute_starts=False)
                 aux = prepare_aux(kk, aa, validate=True, l2_hints=True)
@@ -139,6 +142,24 @@ def main():
             assert oracle.max_rel_error(c3.cpu().numpy(), want3) <= 1e-5, (text, acc)
     del b3
     print("column-panel walk ok")
+    # shifted-block walk (row-multiple variant 8) on a stencil: shifted blocks,
+    # grid-edge fallback blocks, N/c = 32, 64 (two panels) and 16 (lane groups)
+    from paper_2209_02882_b200 import generators as G
+    st = G.stencil27(12, device=dev)
+    a4 = DeviceCsr(st.num_rows, st.num_cols, st.row_ptr.to(torch.int32), st.col_idx.to(torch.int32),
+                   st.vals.to(torch.float32))
+    rp4 = a4.row_ptr.cpu().numpy().astype(np.int64)
+    for n in (128, 256, 64):
+        b4 = torch.rand((st.num_cols, n), device=dev) * 2 - 1
+        want4 = oracle.spmm_f64(rp4.astype(np.int32), a4.col_idx.cpu().numpy(), a4.vals.cpu().numpy(),
+                                b4.cpu().numpy(), n)
+        kk = lower(algorithm_template(parse_point("row:8,col:4,r:1"), KernelConfig(n=n, p=256)),
+                   _Rp(st.num_rows, st.num_cols, rp4), compute_starts=False)
+        aux = prepare_aux(kk, a4, validate=True)
+        c4 = torch.full((st.num_rows, n), float("nan"), device=dev)
+        spmm(kk, a4, b4, c4, aux=aux, hw_variant=8)
+        assert oracle.max_rel_error(c4.cpu().numpy(), want4) <= 1e-5, n
+    print("shifted-block walk ok")
     # group primitives
     out = np.zeros(16)
     assert exec_seg_reduce_group(np.array([5, 5, 7, 7]), np.array([1.0, 2, 3, 4]), out, group_size=4) == 2
