@@ -118,8 +118,9 @@ int run_row_multiple(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T 
         // 16: 2 lane groups of 4 rows per warp (config 4 N=64: 1.40 vs 1.61 ms;
         // N/c == 8 measured 1.33x slower than variant 4 -- 16 staged values
         // per lane go to local memory at 64 registers -- so refused)
-        // 128-thread CTAs by default (config 4 N=128: 2.06 vs 2.27 ms at 256)
-        const int sblk = k.hw_block > 0 ? k.hw_block : 128;
+        // 64-thread CTAs by default (config 4 N=128 / 256: 0.98 / 0.89-0.97x of
+        // 128 threads, which are 0.91x of 256)
+        const int sblk = k.hw_block > 0 ? k.hw_block : 64;
         if (L == 16) {
             const long long nwb = ceil_div(a.num_rows, 8);
             const long long want = ceil_div(nwb, sblk / 32);
