@@ -116,18 +116,19 @@ int run_row_multiple(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T 
     if (k.hw_variant == 8) {  // shifted blocks of 4 rows
         // N/c == 32, or one pass per 32c-column panel (as variant 4); N/c ==
         // 16: 2 lane groups of 4 rows per warp (config 4 N=64: 1.40 vs 1.61 ms;
-        // N/c == 8 measured 1.33x slower than variant 4 -- 16 staged values
-        // per lane go to local memory at 64 registers -- so refused)
+        // N/c == 8 measured 1.33x slower than variant 4 with 4 lane groups of
+        // 4 rows and 1.38x with 4 groups of 2 -- the staged values go to local
+        // memory at 64 registers -- so refused)
         // 64-thread CTAs by default (config 4 N=128 / 256: 0.98 / 0.89-0.97x of
         // 128 threads, which are 0.91x of 256)
         const int sblk = k.hw_block > 0 ? k.hw_block : 64;
-        if (L == 16) {
+        if (L == 16) {  // 2 lane groups of 4 rows
             const long long nwb = ceil_div(a.num_rows, 8);
             const long long want = ceil_div(nwb, sblk / 32);
             const unsigned ctas = (unsigned)(want < (1LL << 30) ? (want > 0 ? want : 1) : (1LL << 30));
             const T *Av = static_cast<const T *>(a.d_vals);
-            k_row_shifted_sub<T, V, 16><<<ctas, sblk, 0, st>>>(a.d_row_ptr, a.d_col_idx, Av, B, C,
-                                                               (int)a.num_rows, N, vec4, acc);
+            k_row_shifted_sub<T, V, 16, 4><<<ctas, sblk, 0, st>>>(a.d_row_ptr, a.d_col_idx, Av, B, C,
+                                                                  (int)a.num_rows, N, vec4, acc);
             return launch_status();
         }
         if (L % 32) return SGAP_ERR_ARG;

@@ -485,7 +485,8 @@ k_row_shifted(const int *__restrict__ rp, const int *__restrict__ ci, const T *_
 // Shifted-block walk for N/c = LPR = 16 (hw variant 8 at N = 64 with c = 4):
 // G = 32 / LPR lane groups of LPR lanes, each owning 4 consecutive rows of
 // an 8-row warp block (config 4 N=64: 1.40 vs 1.61 ms for variant 4; LPR = 8
-// was 1.33x slower: its 16 staged values per lane spill at 64 registers).  When the whole warp block is shifted
+// was 1.33x / 1.38x slower with R = 4 / 2 rows per group: the slot-indexed
+// staged values land in local memory at 64 registers).  When the whole warp block is shifted
 // (as k_row_shifted checks it), every group walks the same pieces of row
 // i0's column list -- group g's piece starts at column cb + 4g -- gathering
 // 3 + w LPR-lane B rows per piece for its 4 rows.  Lane (g, l) keeps
@@ -493,14 +494,14 @@ k_row_shifted(const int *__restrict__ rp, const int *__restrict__ ci, const T *_
 // a position is warp-uniform) and serves them with LPR-wide shuffles.  Other
 // warp blocks run k_row_staged_sub's walk (4 rounds of G rows), so C is
 // bit-identical to hw variant 4 at the same N/c.
-template <typename T, int V, int LPR>
+template <typename T, int V, int LPR, int R>
 __global__ void __launch_bounds__(256, 4)
 k_row_shifted_sub(const int *__restrict__ rp, const int *__restrict__ ci,
                   const T *__restrict__ av, const T *__restrict__ B, T *__restrict__ C, int M,
                   int N, int vec4, int accumulate) {
     constexpr int G = 32 / LPR;  // lane groups per warp
     constexpr int S = 32 / LPR;  // staged slots per lane (L <= 32)
-    constexpr int RB = 4 * G;    // rows per warp block
+    constexpr int RB = R * G;    // rows per warp block (R rows per lane group)
     constexpr int U = 4;
     const int warps = (int)(blockDim.x >> 5);
     const unsigned lane = lane_id();
@@ -531,7 +532,7 @@ k_row_shifted_sub(const int *__restrict__ rp, const int *__restrict__ ci,
                     // group, paired as that kernel pairs them: a round whose
                     // longest row exceeds 64 walks all its rows in float64)
 #pragma unroll 1
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < R; ++k) {
                 const long long i = i0 + G * k + grp;
                 const bool in = i < M;
                 const int beg = in ? __ldg(rp + i) : 0, end = in ? __ldg(rp + i + 1) : 0;
@@ -567,30 +568,30 @@ k_row_shifted_sub(const int *__restrict__ rp, const int *__restrict__ ci,
             }
             continue;
         }
-        // group grp's rows i0 + 4 grp + r: positions sub + LPR s in slot s
-        T v[4][S];
+        // group grp's rows i0 + R grp + r: positions sub + LPR s in slot s
+        T v[R][S];
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
+        for (int r = 0; r < R; ++r)
 #pragma unroll
             for (int s = 0; s < S; ++s) {
                 const int pos = sub + LPR * s;
-                v[r][s] = pos < L ? __ldg(av + p0 + (4 * grp + r) * L + pos) : T(0);
+                v[r][s] = pos < L ? __ldg(av + p0 + (R * grp + r) * L + pos) : T(0);
             }
         const int up = __shfl_up_sync(kFull, c0, 1);
         const unsigned long long cont =
             __ballot_sync(kFull, lane > 0 && (int)lane < L && c0 == up + 1);
-        Vec<T, V> acc[4];
+        Vec<T, V> acc[R];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) acc[r].zero();
+        for (int r = 0; r < R; ++r) acc[r].zero();
         for (int p = 0; p < L;) {
-            const int cb = __shfl_sync(kFull, c0, p) + 4 * grp;
+            const int cb = __shfl_sync(kFull, c0, p) + R * grp;
             const int w = ((cont >> (p + 1)) & 1ull) ? (((cont >> (p + 2)) & 1ull) ? 3 : 2) : 1;
-            Vec<T, V> b[6];
+            Vec<T, V> b[R + 2];
 #pragma unroll
-            for (int q = 0; q < 6; ++q)
-                if (q < 3 + w) gather_vec<T, V>(b[q], row_ptr(bk, cb + q, N));
+            for (int q = 0; q < R + 2; ++q)
+                if (q < R - 1 + w) gather_vec<T, V>(b[q], row_ptr(bk, cb + q, N));
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
+            for (int r = 0; r < R; ++r) {
 #pragma unroll
                 for (int j = 0; j < 3; ++j) {
                     if (j < w) {
@@ -606,8 +607,8 @@ k_row_shifted_sub(const int *__restrict__ rp, const int *__restrict__ ci,
             p += w;
         }
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
-            store_vec<T, V>(C + (i0 + 4 * grp + r) * (long long)N + kcol, acc[r], accumulate != 0);
+        for (int r = 0; r < R; ++r)
+            store_vec<T, V>(C + (i0 + R * grp + r) * (long long)N + kcol, acc[r], accumulate != 0);
     }
 }
 
