@@ -245,8 +245,18 @@ def ncu_traffic(workload: str, point: str, hw_variant: int):
         return None
     try:
         rec = json.loads(p.read_text())
+
+        def same_kernel(a: str, b: str) -> bool:
+            # the shifted-block walk (row-multiple variant 8) ignores g: every
+            # row:g point with the same c runs the same kernel
+            if a == b:
+                return True
+            return (hw_variant == 8 and a.startswith("row:") and b.startswith("row:")
+                    and "/" not in a.split(",")[0] and "/" not in b.split(",")[0]
+                    and a.split(",")[1:] == b.split(",")[1:])
+
         for r in rec.get("entries", []):
-            if (r.get("workload") == workload and r.get("point") == point
+            if (r.get("workload") == workload and same_kernel(r.get("point", ""), point)
                     and int(r.get("hw_variant", 0)) == hw_variant):
                 return {"bytes": r.get("dram_bytes"), "kernel": r.get("kernel"),
                         "captured": r.get("captured"), "source": "profiles/ncu_traffic.json"}
