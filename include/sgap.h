@@ -130,8 +130,8 @@ typedef struct {
                                i0's + r, <= 32 each: banded / stencil rows)
                                gather each shared B row once, other blocks
                                take 4's walk; bit-identical to 4 (N/c a
-                               multiple of 32, panels as 4; N/c == 16: two
-                               4-row lane groups per warp).
+                               multiple of 32, panels as 4; N/c == 16 / 8:
+                               two / four 4-row lane groups per warp).
                                nnz-one: 0 the shuffle segment scan, 1 each
                                segment group walked serially by lanes along
                                the columns (same writebacks).

@@ -1,6 +1,7 @@
 // sgap_api.cu -- the C ABI (include/sgap.h): host-side planning that mirrors
 // the reference's template gates and launch geometry, and stream-ordered
 // dispatch of the sm_100a kernels.  No allocation, no global mutable state.
+#include <cstdlib>
 #include <climits>
 #include <cstdint>
 #include <cstring>
@@ -115,20 +116,32 @@ int run_row_multiple(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T 
     }
     if (k.hw_variant == 8) {  // shifted blocks of 4 rows
         // N/c == 32, or one pass per 32c-column panel (as variant 4); N/c ==
-        // 16: 2 lane groups of 4 rows per warp (config 4 N=64: 1.40 vs 1.61 ms;
-        // N/c == 8 measured 1.33x slower than variant 4 with 4 lane groups of
-        // 4 rows and 1.38x with 4 groups of 2 -- the staged values go to local
-        // memory at 64 registers -- so refused)
+        // 16 / 8: 2 / 4 lane groups of 4 rows per warp.  The block's values sit
+        // in a per-warp shared slab (RB rows x 33, padded against bank
+        // conflicts) read as broadcasts: config 4 N=128 / 256 / 64 / 32 0.94 /
+        // 0.94 / 0.89 / 0.95x of shuffling them from lane registers (which at
+        // N/c == 8 spilled to local memory: 1.33x slower than variant 4)
         // 64-thread CTAs by default (config 4 N=128 / 256: 0.98 / 0.89-0.97x of
         // 128 threads, which are 0.91x of 256)
         const int sblk = k.hw_block > 0 ? k.hw_block : 64;
+        if (L == 8) {  // 4 lane groups of 4 rows
+            const long long nwb = ceil_div(a.num_rows, 16);
+            const long long want = ceil_div(nwb, sblk / 32);
+            const unsigned ctas = (unsigned)(want < (1LL << 30) ? (want > 0 ? want : 1) : (1LL << 30));
+            const size_t smem = (size_t)(sblk / 32) * 16 * 33 * sizeof(T);
+            k_row_shifted_sub<T, V, 8, 4, true><<<ctas, sblk, smem, st>>>(
+                a.d_row_ptr, a.d_col_idx, static_cast<const T *>(a.d_vals), B, C, (int)a.num_rows, N,
+                vec4, acc);
+            return launch_status();
+        }
         if (L == 16) {  // 2 lane groups of 4 rows
             const long long nwb = ceil_div(a.num_rows, 8);
             const long long want = ceil_div(nwb, sblk / 32);
             const unsigned ctas = (unsigned)(want < (1LL << 30) ? (want > 0 ? want : 1) : (1LL << 30));
             const T *Av = static_cast<const T *>(a.d_vals);
-            k_row_shifted_sub<T, V, 16, 4><<<ctas, sblk, 0, st>>>(a.d_row_ptr, a.d_col_idx, Av, B, C,
-                                                                  (int)a.num_rows, N, vec4, acc);
+            const size_t smem = (size_t)(sblk / 32) * 8 * 33 * sizeof(T);
+            k_row_shifted_sub<T, V, 16, 4, true><<<ctas, sblk, smem, st>>>(a.d_row_ptr, a.d_col_idx, Av, B, C,
+                                                                           (int)a.num_rows, N, vec4, acc);
             return launch_status();
         }
         if (L % 32) return SGAP_ERR_ARG;
@@ -139,8 +152,8 @@ int run_row_multiple(const sgap_kernel_t &k, const sgap_csr_t &a, const T *B, T 
         const int M = (int)a.num_rows;
         for (int pan = 0; pan < L / 32; ++pan) {
             const long long off = (long long)pan * 32 * V;
-            k_row_shifted<T, V, 4><<<ctas, sblk, 0, st>>>(a.d_row_ptr, a.d_col_idx, Av, B + off,
-                                                          C + off, M, N, vec4, acc);
+            k_row_shifted<T, V, 4, true><<<ctas, sblk, (size_t)(sblk / 32) * 4 * 33 * sizeof(T), st>>>(
+                a.d_row_ptr, a.d_col_idx, Av, B + off, C + off, M, N, vec4, acc);
             const int s0 = launch_status();
             if (s0 != SGAP_OK) return s0;
         }

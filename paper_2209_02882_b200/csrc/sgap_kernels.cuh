@@ -394,21 +394,26 @@ k_row_staged_sub(const int *__restrict__ rp, const int *__restrict__ ci,
 // slower; the next piece's B rows prefetched into L1 under this piece's
 // gathers: 1.09x slower.
 // ===========================================================================
-template <typename T, int V, int R, int W>
+template <typename T, int V, int R, int W, bool SMEM>
 __device__ __forceinline__ void shifted_piece(Vec<T, V> (&acc)[R], const T (&v)[R], int p,
-                                              const T *__restrict__ bk, int cb, int N) {
+                                              const T *__restrict__ bk, int cb, int N,
+                                              const T *slab) {
     Vec<T, V> b[R + W - 1];
 #pragma unroll
     for (int q = 0; q < R + W - 1; ++q) gather_vec<T, V>(b[q], row_ptr(bk, cb + q, N));
 #pragma unroll
     for (int r = 0; r < R; ++r) {
 #pragma unroll
-        for (int j = 0; j < W; ++j)
-            fma_vec<T, V>(acc[r], __shfl_sync(kFull, v[r], p + j), b[r + j]);
+        for (int j = 0; j < W; ++j) {
+            if constexpr (SMEM)
+                fma_vec<T, V>(acc[r], slab[r * 33 + p + j], b[r + j]);
+            else
+                fma_vec<T, V>(acc[r], __shfl_sync(kFull, v[r], p + j), b[r + j]);
+        }
     }
 }
 
-template <typename T, int V, int R>
+template <typename T, int V, int R, bool SMEM = false>
 __global__ void __launch_bounds__(256, 4)
 k_row_shifted(const int *__restrict__ rp, const int *__restrict__ ci, const T *__restrict__ av,
               const T *__restrict__ B, T *__restrict__ C, int M, int N, int vec4,
@@ -418,6 +423,8 @@ k_row_shifted(const int *__restrict__ rp, const int *__restrict__ ci, const T *_
     const long long kcol = (long long)lane * V;
     const T *bk = B + kcol;
     const long long nblocks = ((long long)M + R - 1) / R;
+    extern __shared__ __align__(16) unsigned char shifted_raw[];
+    T *slab = reinterpret_cast<T *>(shifted_raw) + (size_t)(threadIdx.x >> 5) * R * 33;
     for (long long blk = (long long)blockIdx.x * warps + (threadIdx.x >> 5); blk < nblocks;
          blk += (long long)gridDim.x * warps) {
         const long long i0 = blk * R;
@@ -458,6 +465,14 @@ k_row_shifted(const int *__restrict__ rp, const int *__restrict__ ci, const T *_
             }
             continue;
         }
+        if constexpr (SMEM) {  // the block's values in the warp's shared slab
+            __syncwarp();          // (broadcast reads; the previous block's are done)
+            if ((int)lane < L) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) slab[r * 33 + (int)lane] = v[r];
+            }
+            __syncwarp();
+        }
         // bit p: column p of row i0 continues column p - 1 (runs of consecutive columns)
         const int up = __shfl_up_sync(kFull, c0, 1);
         const unsigned long long cont =
@@ -469,11 +484,11 @@ k_row_shifted(const int *__restrict__ rp, const int *__restrict__ ci, const T *_
             const int cb = __shfl_sync(kFull, c0, p);
             const int w = ((cont >> (p + 1)) & 1ull) ? (((cont >> (p + 2)) & 1ull) ? 3 : 2) : 1;
             if (w == 3)
-                shifted_piece<T, V, R, 3>(acc, v, p, bk, cb, N);
+                shifted_piece<T, V, R, 3, SMEM>(acc, v, p, bk, cb, N, slab);
             else if (w == 2)
-                shifted_piece<T, V, R, 2>(acc, v, p, bk, cb, N);
+                shifted_piece<T, V, R, 2, SMEM>(acc, v, p, bk, cb, N, slab);
             else
-                shifted_piece<T, V, R, 1>(acc, v, p, bk, cb, N);
+                shifted_piece<T, V, R, 1, SMEM>(acc, v, p, bk, cb, N, slab);
             p += w;
         }
 #pragma unroll
@@ -494,7 +509,7 @@ k_row_shifted(const int *__restrict__ rp, const int *__restrict__ ci, const T *_
 // a position is warp-uniform) and serves them with LPR-wide shuffles.  Other
 // warp blocks run k_row_staged_sub's walk (4 rounds of G rows), so C is
 // bit-identical to hw variant 4 at the same N/c.
-template <typename T, int V, int LPR, int R>
+template <typename T, int V, int LPR, int R, bool SMEM = false>
 __global__ void __launch_bounds__(256, 4)
 k_row_shifted_sub(const int *__restrict__ rp, const int *__restrict__ ci,
                   const T *__restrict__ av, const T *__restrict__ B, T *__restrict__ C, int M,
@@ -509,6 +524,9 @@ k_row_shifted_sub(const int *__restrict__ rp, const int *__restrict__ ci,
     const long long kcol = (long long)sub * V;
     const T *bk = B + kcol;
     const long long nblocks = ((long long)M + RB - 1) / RB;
+    extern __shared__ __align__(16) unsigned char shifted_raw[];
+    T *slab = reinterpret_cast<T *>(shifted_raw) + (size_t)(threadIdx.x >> 5) * RB * 33;
+    (void)slab;
     for (long long blk = (long long)blockIdx.x * warps + (threadIdx.x >> 5); blk < nblocks;
          blk += (long long)gridDim.x * warps) {
         const long long i0 = blk * RB;
@@ -569,14 +587,26 @@ k_row_shifted_sub(const int *__restrict__ rp, const int *__restrict__ ci,
             continue;
         }
         // group grp's rows i0 + R grp + r: positions sub + LPR s in slot s
-        T v[R][S];
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-#pragma unroll
-            for (int s = 0; s < S; ++s) {
-                const int pos = sub + LPR * s;
-                v[r][s] = pos < L ? __ldg(av + p0 + (R * grp + r) * L + pos) : T(0);
+        // (SMEM, the launched form: the warp's block in a shared slab of RB
+        // rows x 33 values, padded so the groups' rows fall in different
+        // banks; the register form measured 0.89-0.95x slower)
+        T v[SMEM ? 1 : R][SMEM ? 1 : S];
+        if constexpr (SMEM) {
+            __syncwarp();  // the previous block's readers are done
+            if ((int)lane < L) {
+#pragma unroll 4
+                for (int rr = 0; rr < RB; ++rr) slab[rr * 33 + (int)lane] = __ldg(av + p0 + rr * L + (int)lane);
             }
+            __syncwarp();
+        } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    const int pos = sub + LPR * s;
+                    v[r][s] = pos < L ? __ldg(av + p0 + (R * grp + r) * L + pos) : T(0);
+                }
+        }
         const int up = __shfl_up_sync(kFull, c0, 1);
         const unsigned long long cont =
             __ballot_sync(kFull, lane > 0 && (int)lane < L && c0 == up + 1);
@@ -596,11 +626,15 @@ k_row_shifted_sub(const int *__restrict__ rp, const int *__restrict__ ci,
                 for (int j = 0; j < 3; ++j) {
                     if (j < w) {
                         const int pos = p + j;
-                        T x = v[r][0];
+                        if constexpr (SMEM) {
+                            fma_vec<T, V>(acc[r], slab[(R * grp + r) * 33 + pos], b[r + j]);
+                        } else {
+                            T x = v[r][0];
 #pragma unroll
-                        for (int s = 1; s < S; ++s)
-                            if (pos / LPR == s) x = v[r][s];
-                        fma_vec<T, V>(acc[r], __shfl_sync(kFull, x, pos & (LPR - 1), LPR), b[r + j]);
+                            for (int s = 1; s < S; ++s)
+                                if (pos / LPR == s) x = v[r][s];
+                            fma_vec<T, V>(acc[r], __shfl_sync(kFull, x, pos & (LPR - 1), LPR), b[r + j]);
+                        }
                     }
                 }
             }

@@ -132,7 +132,7 @@ def candidates(n: int, p_values=(256, 1024), g_values=GPU_G_VALUES,
                 # (banded rows share shifted column lists; other blocks fall
                 # back to the warp-per-row walk inline)
                 vs = ((0, 2, 4, 6, 7, 8) if L == 32 else (0, 2, 4, 8) if L % 32 == 0
-                      else (0, 2, 3, 4, 8) if L == 16 else (0, 2, 3, 4) if L == 8
+                      else (0, 2, 3, 4, 8) if L in (8, 16)
                       else (0, 2, 4) if L in (2, 4)
                       else (0, 2))
                 out.extend(Candidate(str(pt), p, 0, v) for v in vs)
@@ -220,7 +220,7 @@ def heuristic(stats: MatrixStats, n: int, esz: int = 4) -> Candidate:
                 # shifted copies of each other (config 4 N=128: 2.06 vs 3.07
                 # ms, N=256 / 512: 0.67x, profiles/r02_rb_shifted_cfg4.md)
                 lanes = n // widest
-                if lanes % 32 == 0 or lanes == 16:  # (N=64: 1.40 vs 1.61 ms)
+                if lanes % 32 == 0 or lanes in (8, 16):  # (N=64 / 32: 1.24 / 0.88 vs 1.61 / 0.93 ms)
                     return Candidate(pt, p, 0, 8)
                 return Candidate(pt, p, 0, 4 if lanes in (4, 8, 16) else 2)
         pt = f"row:1,col:{col(widest)},r:1"

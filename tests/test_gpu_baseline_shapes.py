@@ -134,8 +134,8 @@ def test_config4_stencil160_n_sweep(n):
            (f"row:4,col:{c},r:1", 256, 2), (f"row:1/4,col:{c},r:4", 256, 0)]
     if n // c == 32:
         pts.append((f"row:8,col:{c},r:1", 256, 3))  # warp per row, lane-staged A
-    if n // c == 16:
-        pts.append((f"row:8,col:{c},r:1", 256, 8))  # shifted blocks, 2 lane groups
+    if n // c in (8, 16):
+        pts.append((f"row:8,col:{c},r:1", 256, 8))  # shifted blocks, lane groups
     if n // c >= 32:
         pts.append((f"nnz:256,col:{c},r:1", 256, 4))  # lane-staged EB walk
         pts.append((f"row:8,col:{c},r:1", 256, 8))  # shifted 4-row blocks (panels from N=256)

@@ -332,7 +332,7 @@ def test_shifted_block_walk_bitwise():
                                 col_idx=torch.from_numpy(np.concatenate(cols2)).cuda(),
                                 vals=torch.from_numpy(rng.uniform(-1, 1, rp2[-1])).cuda())
     for g in (G.stencil27(40, device="cuda"), band, tri):
-        for n, c in ((128, 4), (256, 4), (64, 2), (64, 4)):
+        for n, c in ((128, 4), (256, 4), (64, 2), (64, 4), (32, 4)):
             for dt, tol in ((torch.float32, TOL), (torch.float64, 1e-12)):
                 a0 = _device(g)
                 a = DeviceCsr(a0.num_rows, a0.num_cols, a0.row_ptr, a0.col_idx, g.vals.to(dt))
@@ -352,13 +352,13 @@ def test_shifted_block_walk_bitwise():
                                        a.vals.cpu().numpy(), b.cpu().numpy(), n)
                 assert oracle.max_rel_error(outs[2].cpu().numpy(), want) <= tol
                 assert oracle.max_rel_error(outs[3].cpu().numpy(), want + 0.5) <= tol
-    # N/c neither 16 nor a multiple of 32: refused (SGAP_ERR_ARG)
+    # N/c not 8, 16 or a multiple of 32: refused (SGAP_ERR_ARG)
     from paper_2209_02882_b200 import _native
     a = _device(tri)
-    tpl = algorithm_template(parse_point("row:8,col:4,r:1"), KernelConfig(n=32, p=256))
+    tpl = algorithm_template(parse_point("row:8,col:4,r:1"), KernelConfig(n=16, p=256))
     kk = lower(tpl, _Rp(a.num_rows, a.num_cols, rp2), compute_starts=False)
     with pytest.raises(_native.SgapError):
-        spmm(kk, a, torch.rand((m2, 32), device="cuda"), torch.empty((m2, 32), device="cuda"),
+        spmm(kk, a, torch.rand((m2, 16), device="cuda"), torch.empty((m2, 16), device="cuda"),
              aux=prepare_aux(kk, a), hw_variant=variant)
 
 

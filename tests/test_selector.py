@@ -41,8 +41,8 @@ def test_heuristic_matrix_classes():
         ("row:8,col:4,r:1", 8)
     assert heuristic(STENCIL160, 256).hw_variant == 8
     # 2 / 4 / 8 rows per warp at N = 64 / 32 / 16
-    assert {heuristic(STENCIL160, n).hw_variant for n in (16, 32)} == {4}
-    assert heuristic(STENCIL160, 64).hw_variant == 8  # shifted blocks, 2 lane groups
+    assert heuristic(STENCIL160, 16).hw_variant == 4
+    assert {heuristic(STENCIL160, n).hw_variant for n in (32, 64)} == {8}  # shifted, lane groups
     assert heuristic(STENCIL160, 16).point.startswith("row:4")
     assert heuristic(STENCIL160, 4).point == "row:1,col:4,r:1"
     # narrow B on power-law rows: serial segment groups; N=8: short chunks
